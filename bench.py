@@ -1,0 +1,488 @@
+#!/usr/bin/env python
+"""bench.py — batched IPv6 LPM throughput on B200 (BASELINE.json metric).
+
+A step = one pass of the lookup over one batch of synthetic queries (default:
+workload C1 = the 200K-prefix backbone FIB and 268,435,456 queries per GPU,
+BASELINE.json configs[1]). Prints ONE JSON line (rank 0).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C1]
+  python bench.py --impl reference ...   # the reference's CPU lookup on host cores
+
+Multi-GPU (N > 1) is launched by torchrun: rank 0 builds the FIB on the host,
+NCCL broadcasts keys/values to every GPU, each GPU generates and looks up its own
+query batch (no inter-GPU traffic during lookups; weak scaling), device time is
+the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "IPv6 lookups/sec (G/s) per B200 and at 1/2/4/8 GPUs; % of roofline"
+UNIT = "G lookups/s"
+HBM_FALLBACK_GBS = 6650.0
+CPU_SAMPLE = 1 << 25  # bounded CPU-baseline sample (33.5M queries)
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="C1")
+    ap.add_argument("--lanes", type=int, default=0, help="lanes per query (4/8/16), 0 = auto")
+    ap.add_argument("--smem-levels", type=int, default=None, help="levels staged in smem, default auto")
+    ap.add_argument("--ctas-per-sm", type=int, default=0)
+    ap.add_argument("--queries", type=int, default=0, help="override queries per GPU (testing only)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="also time every kernel shape (extra key)")
+    return ap.parse_args()
+
+
+# ---- distributed plumbing ------------------------------------------------------------
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def init_dist(ws, local, backend="nccl"):
+    import torch
+    import torch.distributed as dist
+    if ws > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    return dist if ws > 1 else None
+
+
+# ---- clocks ---------------------------------------------------------------------------
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---- roofline -----------------------------------------------------------------------------
+
+def hbm_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
+        except Exception:
+            pass
+    return HBM_FALLBACK_GBS, "B200_PROFILING.md fallback"
+
+
+def roofline(geom, w, l2_gbs, smem_gbs, hbm_gbs, smem_cap=232448):
+    """roofline_lps = max_T min(HBM/(16+w), SMEM/(128 T), L2/(128 (d+1-T) + w))."""
+    d = geom.depth
+    levels = d + 1
+    best = None
+    for T in range(0, levels + 1):
+        staged = (geom.total_keys if T >= levels else geom.level_start[T]) * 8 if T else 0
+        if staged > smem_cap:
+            break
+        terms = {"hbm": hbm_gbs * 1e9 / (16 + w)}
+        if T:
+            terms["smem"] = smem_gbs * 1e9 / (128 * T)
+        l2_bytes = 128 * (levels - T) + w
+        terms["l2"] = l2_gbs * 1e9 / l2_bytes
+        bound = min(terms, key=terms.get)
+        cand = {"T": T, "lps": terms[bound], "bound": bound, "terms_glps": {k: v / 1e9 for k, v in terms.items()},
+                "bytes_per_query": {"hbm": 16 + w, "smem": 128 * T, "l2": l2_bytes}}
+        if best is None or cand["lps"] > best["lps"]:
+            best = cand
+    return best
+
+
+# ---- reference arm ---------------------------------------------------------------------------
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def reference_sample(lpm, workload, n):
+    info = lpm.workload_info(workload)
+    fib = lpm.workload_fib(info.fib_kind)
+    addrs = lpm.workload_queries_host(workload, fib, 0, n, threads=cpu_threads())
+    return info, fib, addrs
+
+
+def time_reference_cpu(fib, addrs, threads, repeats=1):
+    """The reference's own lpm6::lookup_interval_oracle (oracle/_ref, intervals.cpp:142-145)
+    on `threads` std::threads, or the C restatement when _ref was not built."""
+    from oracle.oracle import REF_SO, Oracle, RefOracle
+    keys = np.ascontiguousarray(addrs[:, 1])
+    if REF_SO.exists():
+        r = RefOracle()
+        st, rmap = r.build_intervals(fib.rules, fib.default_next_hop)
+        assert st == 0, r.error()
+        rmap.lookup(keys[: 1 << 16], threads)  # warm-up
+        times = []
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            rmap.lookup(keys, threads)
+            times.append(time.perf_counter() - t0)
+        return times, "reference", "oracle/_ref lpm6::lookup_interval_oracle (reference fib.cpp+intervals.cpp)"
+    o = Oracle()
+    st, b, nh = o.build_intervals(fib.rules, fib.default_next_hop)
+    times = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        o.lookup_batch(0, b, nh, addrs, threads)
+        times.append(time.perf_counter() - t0)
+    return times, "port", "oracle/lpm6_oracle.c orc_lookup_interval (restatement)"
+
+
+def time_restated_planb(fib, addrs, threads):
+    """Restated PlanB AVX-512 Listing 1 + B=16 batched search, k=8 (oracle/lpm6_oracle_avx512.c)."""
+    from oracle.oracle import Oracle
+    o = Oracle()
+    st, b, nh = o.build_intervals(fib.rules, fib.default_next_hop)
+    tree = o.build_tree(b, nh, 8)
+    o.lookup_batch(2, b, nh, addrs[: 1 << 16], threads, tree=tree)
+    t0 = time.perf_counter()
+    _, ran = o.lookup_batch(2, b, nh, addrs, threads, tree=tree)
+    dt = time.perf_counter() - t0
+    return dt, {2: "avx512_batch16", 1: "branchfree_scalar"}[ran]
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import paper_2604_14650_b200 as lpm
+    threads = cpu_threads()
+    info, fib, addrs = reference_sample(lpm, args.workload, CPU_SAMPLE)
+    n = len(addrs)
+    times, kind, what = time_reference_cpu(fib, addrs, threads, repeats=args.warmup + args.steps)
+    timed = times[args.warmup:]
+    total = sum(timed)
+    value = n * len(timed) / total / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total / len(timed) * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "impl": "reference",
+        "data": f"synthetic seeded {info.name} workload, first {n} queries per step (bounded CPU sample)",
+        "config": {"workload": info.name, "fib_prefixes": len(fib), "queries_per_step": n,
+                   "full_workload_queries": info.n_queries},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{n} queries of {info.name} per step", "what": what, "cpu": cpu_model()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    try:
+        dt, variant = time_restated_planb(fib, addrs, threads)
+        line["restated_planb_cpu"] = {"value": n / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
+                                      "variant": variant, "sample": f"{n} queries"}
+    except Exception as e:  # the restatement is extra context only
+        line["restated_planb_cpu"] = {"error": str(e)}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---- our arm ------------------------------------------------------------------------------------
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    ws, rank, local = dist_env()
+    dist = init_dist(ws, local)
+    torch.cuda.set_device(local)
+    dev_index = local
+    import paper_2604_14650_b200 as lpm
+    from paper_2604_14650_b200.fib import Geometry
+
+    info = lpm.workload_info(args.workload)
+    fib = lpm.workload_fib(info.fib_kind)
+    n = args.queries or info.n_queries
+    vb = info.value_bytes
+
+    # -- FIB: host build on rank 0, NCCL broadcast to the others -----------------------------
+    t0 = time.perf_counter()
+    if rank == 0:
+        imap = lpm.build_intervals(fib)
+        tree = lpm.build_tree(imap, 16, vb)
+        geom = tree.geometry
+    build_ms = (time.perf_counter() - t0) * 1e3
+    if dist is not None:
+        obj = [geom if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        geom = obj[0]
+        nk, nv = geom.total_keys, geom.leaf_nodes * geom.k * geom.value_bytes
+        keys_t = torch.empty(nk, dtype=torch.int64, device="cuda")
+        vals_t = torch.empty(nv, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            keys_t.copy_(torch.from_numpy(tree.keys.view(np.int64)))
+            vals_t.copy_(torch.from_numpy(tree.values.view(np.uint8)))
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dist.broadcast(keys_t, 0)
+        dist.broadcast(vals_t, 0)
+        e1.record()
+        torch.cuda.synchronize()
+        bcast_ms = e0.elapsed_time(e1)
+        t = torch.tensor([bcast_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        bcast_ms = float(t.item())
+        fdev = lpm.Fib.wrap_device(geom, keys_t, vals_t, dev_index)
+    else:
+        fdev = lpm.Fib.from_tree(tree, dev_index)
+        bcast_ms = 0.0
+    cfg = fdev.set_kernel_config(lanes_per_query=args.lanes, smem_levels=args.smem_levels,
+                                 ctas_per_sm=args.ctas_per_sm)
+
+    # -- queries: this rank's slice, generated on the device ------------------------------------
+    addrs = torch.empty((n, 16), dtype=torch.uint8, device="cuda")
+    out = torch.empty(n * vb, dtype=torch.uint8, device="cuda")
+    gen = lpm.QueryGen(args.workload, fib, dev_index)
+    gen.run(rank * n, n, addrs)
+    torch.cuda.synchronize()
+
+    # -- roofline denominators measured on this device --------------------------------------------
+    tree_bytes = geom.total_keys * 8
+    l2_gbs = lpm.probe_l2_gather(dev_index, max(tree_bytes, 1 << 22), 128)
+    smem_gbs = lpm.probe_smem(dev_index)
+    hbm_gbs, hbm_src = hbm_peak()
+
+    stream = torch.cuda.current_stream()
+
+    def step():
+        fdev.lookup_batch(addrs, out, stream)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    with ClockSampler(dev_index) as clk:
+        ev[0].record(stream)
+        for i in range(args.steps):
+            step()
+            ev[i + 1].record(stream)
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    total_ms = sum(step_ms)
+    if dist is not None:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = ws * n * args.steps / (total_ms * 1e-3) / 1e9  # aggregate G lookups/s
+    lps_gpu = n / (ms_per_step * 1e-3)
+
+    # -- parity sample of the timed output ----------------------------------------------------------
+    parity = None
+    if rank == 0:
+        from oracle.oracle import Oracle
+        o = Oracle()
+        m_s = min(n, 1 << 20)
+        st, b, nh = o.build_intervals(fib.rules, fib.default_next_hop)
+        ha = addrs[:m_s].cpu().numpy().view(np.uint64).reshape(-1, 2)
+        want, _ = o.lookup_batch(0, b, nh, ha, threads=cpu_threads())
+        got = out[: m_s * vb].cpu().numpy().view({1: np.uint8, 2: np.uint16, 4: np.uint32}[vb]).astype(np.uint32)
+        parity = {"checked": m_s, "mismatches": int(np.count_nonzero(got != want)),
+                  "oracle": "oracle/lpm6_oracle.c interval oracle"}
+
+    # -- end to end through the C ABI with host buffers -------------------------------------------
+    e2e = None
+    if not args.no_e2e:
+        h_addrs = torch.empty((n, 16), dtype=torch.uint8, pin_memory=True)
+        h_out = torch.empty(n * vb, dtype=torch.uint8, pin_memory=True)
+        h_addrs.copy_(addrs)
+        torch.cuda.synchronize()
+        ha_np, ho_np = h_addrs.numpy(), h_out.numpy()
+        fdev.lookup_batch(ha_np, ho_np)  # warm-up: allocates the staging pipeline
+        if dist is not None:
+            dist.barrier()
+        k_e2e = max(1, min(args.steps, 5))
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(k_e2e):
+            fdev.lookup_batch(ha_np, ho_np)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = s0.elapsed_time(s1)
+        if dist is not None:
+            t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": ws * n * k_e2e / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": n * 16,
+               "d2h_bytes_per_step": n * vb, "steps": k_e2e,
+               "path": "lpm6cu_lookup_batch(host pinned buffers): 8M-address chunks, H2D/kernel/D2H on 3 streams"}
+        same = bool(np.array_equal(ho_np[: 1 << 20], out[: 1 << 20].cpu().numpy()))
+        e2e["matches_device_path"] = same
+        del h_addrs, h_out
+
+    # -- optional shape sweep --------------------------------------------------------------------------
+    sweep = None
+    if args.sweep and rank == 0:
+        sweep = []
+        for g in (4, 8, 16):
+            for t_lv in range(0, geom.depth + 2):
+                try:
+                    fdev.set_kernel_config(lanes_per_query=g, smem_levels=t_lv)
+                except Exception:
+                    continue
+                for _ in range(2):
+                    step()
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(stream)
+                for _ in range(3):
+                    step()
+                a1.record(stream)
+                torch.cuda.synchronize()
+                ms = a0.elapsed_time(a1) / 3
+                sweep.append({"lanes": g, "smem_levels": t_lv, "ms": ms, "glps": n / ms / 1e6})
+        fdev.set_kernel_config(lanes_per_query=args.lanes, smem_levels=args.smem_levels,
+                               ctas_per_sm=args.ctas_per_sm)
+
+    # -- CPU baseline (rank 0, N = 1) ---------------------------------------------------------------------
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        threads = cpu_threads()
+        m_cpu = min(n, CPU_SAMPLE)
+        ha = lpm.workload_queries_host(args.workload, fib, 0, m_cpu, threads=threads)
+        times, kind, what = time_reference_cpu(fib, ha, threads, repeats=1)
+        cpu = {"value": m_cpu / times[0] / 1e9, "unit": UNIT, "cores": threads, "kind": kind,
+               "sample": f"first {m_cpu} queries of {info.name}", "what": what, "cpu": cpu_model()}
+        try:
+            dt, variant = time_restated_planb(fib, ha, threads)
+            cpu["restated_planb"] = {"value": m_cpu / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
+                                     "variant": variant}
+        except Exception as e:
+            cpu["restated_planb"] = {"error": str(e)}
+
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+        return 0
+
+    rl = roofline(geom, vb, l2_gbs, smem_gbs, hbm_gbs)
+    bpq = rl["bytes_per_query"][rl["bound"]]
+    peak = {"hbm": hbm_gbs, "smem": smem_gbs, "l2": l2_gbs}[rl["bound"]]
+    achieved = lps_gpu * bpq / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u64",
+        "data": f"synthetic: seeded {info.name} FIB ({len(fib)} prefixes) and query generator, "
+                f"{n} queries per GPU generated on device",
+        "config": {"workload": info.name, "fib_prefixes": len(fib), "intervals": geom.num_keys,
+                   "tree_depth": geom.depth, "node_keys": geom.k, "tree_bytes": tree_bytes,
+                   "queries_per_gpu": n, "value_bytes": vb, "kernel": cfg,
+                   "l2_flush": f"not needed: each step streams {n * 16 / 1e9:.1f} GB of addresses (> 126 MB L2)",
+                   "parallelism": f"dp{ws} (query batches; FIB replicated by NCCL broadcast)"},
+        "roofline": {"bound": rl["bound"], "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "lps_achieved_per_gpu": lps_gpu / 1e9, "lps_roofline_per_gpu": rl["lps"] / 1e9,
+                     "smem_levels_for_roofline": rl["T"], "terms_glps": rl["terms_glps"],
+                     "bytes_per_query": rl["bytes_per_query"],
+                     "measured": {"l2_gather_gbs": l2_gbs, "smem_gbs": smem_gbs, "hbm_gbs": hbm_gbs,
+                                  "hbm_source": hbm_src},
+                     "hbm_frac": lps_gpu * (16 + vb) / 1e9 / hbm_gbs},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+        "parity_sample": parity,
+        "fib_build_ms": build_ms,
+        "fib_broadcast_ms": bcast_ms,
+        "step_ms": step_ms,
+    }
+    if sweep is not None:
+        line["sweep"] = sweep
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

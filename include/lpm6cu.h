@@ -1,0 +1,200 @@
+/* lpm6cu — C ABI of the B200-native batched IPv6 longest-prefix-match lookup.
+ *
+ * This is the drop-in boundary for PlanB's hot path. It replaces, on the GPU,
+ * the reference interfaces below (all under /root/reference/proj/):
+ *
+ *   reference                                            here
+ *   ---------------------------------------------------  ------------------------------
+ *   FibTable -> build_intervals -> build_tree            lpm6cu_fib_build
+ *     (fib.hpp:74-105, intervals.hpp:34, tree.hpp:74)
+ *   build_intervals (intervals.hpp:34)                   lpm6_build_intervals
+ *   plan_geometry / build_tree (tree.hpp:36, :74)        lpm6_plan_layout / lpm6_build_tree
+ *   search_batch / lookup (bodies absent,     lpm6cu_lookup_batch
+ *     CMakeLists.txt:27-28,35,42) behind the runtime
+ *     backend table detail::vector_backend()
+ *     (intervals.cpp:121, CMakeLists.txt:18-46)
+ *   lpm6::Error{Errc} (types.hpp:27-49)                  int status = (int)Errc + 1, lpm6cu_last_error()
+ *
+ * Conventions
+ *   - Every function returns 0 on success or a status code below; the message of
+ *     the last failure on the calling thread is lpm6cu_last_error(). No C++
+ *     exception crosses this boundary.
+ *   - Addresses are 16-byte little-endian unsigned __int128 values (lo word first),
+ *     the type lpm6::lookup_linear_oracle takes (intervals.hpp:37). The lookup key
+ *     is the top 64 bits (fib.hpp:27), clamped to 0xFFFF_FFFF_FFFF_FFFE (types.hpp:25).
+ *   - Next hops are written at the FIB's value width (1, 2 or 4 bytes, little-endian).
+ *   - A FIB handle is immutable after creation: any number of lookups on any
+ *     streams may run on it concurrently (the reference's contract).
+ *   - There is no CPU fallback: a lookup without a usable CUDA device fails with
+ *     LPM6CU_E_CUDA.
+ */
+#ifndef LPM6CU_H
+#define LPM6CU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  LPM6CU_OK = 0,
+  LPM6CU_E_MALFORMED_ADDRESS = 1,       /* Errc::MalformedAddress */
+  LPM6CU_E_UNSUPPORTED_PREFIX_LENGTH = 2,
+  LPM6CU_E_MISSING_NEXT_HOP = 3,
+  LPM6CU_E_RESERVED_NEXT_HOP = 4,
+  LPM6CU_E_DUPLICATE_PREFIX = 5,
+  LPM6CU_E_UNKNOWN_PREFIX = 6,
+  LPM6CU_E_SENTINEL_COLLISION = 7,
+  LPM6CU_E_EXHAUSTED_PREFIX_SPACE = 8,
+  LPM6CU_E_INVALID_ARGUMENT = 9,
+  LPM6CU_E_BAD_TRACE_FILE = 10,
+  LPM6CU_E_BAD_SNAPSHOT_FILE = 11,
+  LPM6CU_E_IO = 12,
+  LPM6CU_E_CUDA = 13,
+  LPM6CU_E_NCCL = 14,
+};
+
+/* Same memory layout as lpm6::Prefix (fib.hpp:22-29): u128 value (text order,
+ * canonical), int length 0..64, u32 next hop; 32 bytes. A reference
+ * FibTable::entries().data() can be passed directly. */
+typedef struct {
+  uint64_t value_lo;
+  uint64_t value_hi;
+  int32_t length;
+  uint32_t next_hop;
+  uint64_t reserved;
+} lpm6cu_prefix;
+
+#define LPM6CU_MAX_LEVELS 9
+
+/* Geometry of the B200 tree layout (compact levels of 128-byte, 16-key nodes).
+ * Counterpart of lpm6::TreeGeometry (tree.hpp:18-33). */
+typedef struct {
+  uint32_t k;           /* keys per node (16) */
+  uint32_t b;           /* arity, k + 1 */
+  uint32_t depth;       /* internal levels; a lookup visits depth + 1 nodes */
+  uint32_t value_bytes; /* 1, 2 or 4 */
+  uint64_t num_keys;    /* m, real interval boundaries */
+  uint64_t leaf_nodes;  /* ceil(m / k) */
+  uint64_t total_keys;  /* length of the key array */
+  uint64_t level_nodes[LPM6CU_MAX_LEVELS]; /* reachable nodes per level (level depth = leaves) */
+  uint64_t level_start[LPM6CU_MAX_LEVELS]; /* key offset of each level */
+  uint32_t default_next_hop;
+  uint32_t reserved;
+} lpm6cu_geometry;
+
+typedef struct {
+  uint32_t merge_adjacent; /* IntervalBuildOptions::merge_adjacent (intervals.hpp:28); default 1 */
+  uint32_t value_bytes;    /* 0 = narrowest width holding every next hop */
+  uint32_t k;              /* keys per node; 0 = 16 (the only width the kernels take) */
+  uint32_t reserved;
+} lpm6cu_build_opts;
+
+/* Kernel shape; 0 in a field = automatic. */
+typedef struct {
+  uint32_t lanes_per_query; /* 4, 8 or 16 lanes cooperate on one 128-byte node */
+  uint32_t smem_levels;     /* top tree levels staged in shared memory by TMA; 0xFF = auto */
+  uint32_t ctas_per_sm;
+  uint32_t threads_per_cta;
+} lpm6cu_kernel_config;
+
+typedef struct lpm6cu_fib lpm6cu_fib;
+typedef struct lpm6cu_querygen lpm6cu_querygen;
+
+const char* lpm6cu_last_error(void);
+const char* lpm6cu_status_name(int status);
+const char* lpm6cu_version(void);
+
+/* ---- host-side FIB build (no GPU needed) ---------------------------------- */
+
+/* build_intervals (intervals.cpp:33-93): boundaries/next_hops need capacity >= 2n+1. */
+int lpm6_build_intervals(const lpm6cu_prefix* rules, uint64_t n, uint32_t default_next_hop,
+                         int merge_adjacent, uint64_t* boundaries, uint32_t* next_hops,
+                         uint64_t capacity, uint64_t* m_out);
+
+/* Geometry for m boundaries at k keys per node. */
+int lpm6_plan_layout(uint64_t m, uint32_t k, lpm6cu_geometry* g);
+
+/* Lay out the tree. With keys == NULL only *g is filled (to size the arrays:
+ * g->total_keys u64 keys, g->leaf_nodes * k * g->value_bytes value bytes). */
+int lpm6_build_tree(const uint64_t* boundaries, const uint32_t* next_hops, uint64_t m,
+                    uint32_t default_next_hop, uint32_t k, uint32_t value_bytes,
+                    lpm6cu_geometry* g, uint64_t* keys, void* values);
+
+/* Parse "<ipv6>/<len> <next_hop>" (fib.cpp:72-105). */
+int lpm6_parse_prefix(const char* text, lpm6cu_prefix* out, int* host_bits_masked);
+
+/* ---- device FIB ----------------------------------------------------------- */
+
+/* FibTable -> intervals -> B200 layout -> device memory of `device`. */
+int lpm6cu_fib_build(int device, const lpm6cu_prefix* rules, uint64_t n, uint32_t default_next_hop,
+                     const lpm6cu_build_opts* opts, lpm6cu_fib** out);
+
+/* From a host layout (lpm6_build_tree output); copies into device memory it owns. */
+int lpm6cu_fib_create(int device, const lpm6cu_geometry* g, const uint64_t* keys,
+                      const void* values, lpm6cu_fib** out);
+
+/* Over device arrays the caller owns (e.g. filled by an NCCL broadcast); not freed
+ * by lpm6cu_fib_destroy. */
+int lpm6cu_fib_wrap_device(int device, const lpm6cu_geometry* g, const void* d_keys,
+                           const void* d_values, lpm6cu_fib** out);
+
+int lpm6cu_fib_geometry(const lpm6cu_fib* fib, lpm6cu_geometry* g);
+int lpm6cu_fib_device_arrays(const lpm6cu_fib* fib, const void** d_keys, const void** d_values);
+int lpm6cu_fib_set_kernel_config(lpm6cu_fib* fib, const lpm6cu_kernel_config* cfg);
+int lpm6cu_fib_kernel_config(const lpm6cu_fib* fib, lpm6cu_kernel_config* cfg);
+void lpm6cu_fib_destroy(lpm6cu_fib* fib);
+
+/* ---- lookup --------------------------------------------------------------- */
+
+/* n next hops for n addresses. With device pointers: one kernel launch on
+ * `stream` (a cudaStream_t; NULL = legacy default), asynchronous, no host sync,
+ * no allocation. With host pointers (pinned or pageable): chunked host->device
+ * copy / lookup / device->host copy pipeline on internal streams ordered after
+ * `stream`; returns when `out` holds the results. */
+int lpm6cu_lookup_batch(const lpm6cu_fib* fib, const void* addrs, uint64_t n, void* out,
+                        void* stream);
+
+/* ---- synthetic workloads C0..C4 (BASELINE.json configs) ---------------------- */
+
+typedef struct {
+  int32_t id;         /* 0 C0, 1 C1, 2 C2, 3 C3a, 4 C3b, 5 C4 */
+  int32_t fib_kind;   /* 0: C0 FIB, 1: 200K backbone FIB, 2: 1M projected FIB */
+  uint64_t n_queries;
+  uint64_t chunk;     /* queries per chunk (C4), 0 = one */
+  uint32_t value_bytes;
+  uint32_t reserved;
+  char name[8];
+} lpm6_workload_info;
+
+int lpm6_workload_info_get(int workload, lpm6_workload_info* info);
+
+/* The FIB of fib_kind; with out == NULL only *n_out / *default_next_hop are set. */
+int lpm6_workload_fib(int fib_kind, lpm6cu_prefix* out, uint64_t capacity, uint64_t* n_out,
+                      uint32_t* default_next_hop);
+
+/* Queries [first, first+n) of `workload` over `rules`, generated on the host. */
+int lpm6_workload_queries_host(int workload, const lpm6cu_prefix* rules, uint64_t nrules,
+                               uint64_t first, uint64_t n, void* out_addrs, int threads);
+
+/* The same queries generated on the GPU (bit-identical to the host generator). */
+int lpm6cu_querygen_create(int device, int workload, const lpm6cu_prefix* rules, uint64_t nrules,
+                           lpm6cu_querygen** out);
+int lpm6cu_querygen_run(const lpm6cu_querygen* gen, uint64_t first, uint64_t n, void* d_out_addrs,
+                        void* stream);
+void lpm6cu_querygen_destroy(lpm6cu_querygen* gen);
+
+/* ---- measurement probes (roofline denominators) ----------------------------- */
+
+/* Random gather of `line_bytes`-sized lines (32 or 128) from an L2-resident
+ * buffer of `buffer_bytes`; returns achieved GB/s of requested bytes. */
+int lpm6cu_probe_l2_gather(int device, uint64_t buffer_bytes, uint32_t line_bytes, double* gbps);
+/* Shared-memory read bandwidth (all SMs, conflict-free 128-byte rows), GB/s. */
+int lpm6cu_probe_smem(int device, double* gbps);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LPM6CU_H */

@@ -1,0 +1,18 @@
+// Helpers shared by the host and device halves of the C ABI.
+#pragma once
+
+#include <vector>
+
+#include "capi_util.hpp"
+#include "lpm6/fib.hpp"
+#include "lpm6/layout.hpp"
+#include "lpm6cu.h"
+
+namespace lpm6::capi {
+
+std::vector<Prefix> to_prefixes(const lpm6cu_prefix* rules, uint64_t n);
+void export_geometry(const TreeLayout& t, lpm6cu_geometry* g);
+Tree build_device_tree(const lpm6cu_prefix* rules, uint64_t n, uint32_t default_nh,
+                       const lpm6cu_build_opts* opts);
+
+}  // namespace lpm6::capi

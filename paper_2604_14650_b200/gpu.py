@@ -1,0 +1,192 @@
+"""Device side: the B200 FIB handle and ``lookup_batch`` (include/lpm6cu.h).
+
+``Fib.build(fib).lookup_batch(addrs, out)`` is the drop-in for the reference's
+FibTable -> build_intervals -> build_tree -> search_batch/lookup path
+(fib.hpp:74-105, intervals.hpp:34, tree.hpp:74). Lookups run only in
+the sm_100a kernels of ``csrc/lookup.cu``; without a CUDA device they fail with
+``Lpm6Error(code="CudaError")`` — there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from ._lib import Geometry_t, KernelConfig_t, Lpm6Error, check, lib
+from .fib import FibTable, Geometry, Tree, _rules_ptr, build_opts
+
+_NP_VDT = {1: np.uint8, 2: np.uint16, 4: np.uint32}
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_handle(stream) -> int | None:
+    if stream is None:
+        torch = _torch()
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _ptr_len(buf, item: int) -> tuple[int, int, bool]:
+    """(pointer, element count, is_device) of a torch tensor or numpy array of `item`-byte elements."""
+    if isinstance(buf, np.ndarray):
+        if not buf.flags.c_contiguous:
+            raise Lpm6Error(9, "buffer must be contiguous")
+        return buf.ctypes.data, buf.nbytes // item, False
+    torch = _torch()
+    if isinstance(buf, torch.Tensor):
+        if not buf.is_contiguous():
+            raise Lpm6Error(9, "buffer must be contiguous")
+        return buf.data_ptr(), buf.numel() * buf.element_size() // item, buf.is_cuda
+    raise TypeError(f"unsupported buffer type {type(buf)}")
+
+
+class Fib:
+    """An immutable FIB resident in one GPU's HBM (lpm6cu_fib)."""
+
+    def __init__(self, handle: int, device: int, keepalive=None):
+        self._h = C.c_void_p(handle)
+        self.device = device
+        self._keepalive = keepalive
+
+    # -- construction ---------------------------------------------------------
+    @classmethod
+    def build(cls, fib: FibTable, device: int = 0, merge_adjacent: bool = True, value_bytes: int = 0) -> "Fib":
+        h = C.c_void_p()
+        opts = build_opts(merge_adjacent, value_bytes)
+        rules = fib.rules
+        check(lib().lpm6cu_fib_build(device, _rules_ptr(rules), len(rules), fib.default_next_hop, C.byref(opts),
+                                     C.byref(h)))
+        return cls(h.value, device)
+
+    @classmethod
+    def from_tree(cls, tree: Tree, device: int = 0) -> "Fib":
+        h = C.c_void_p()
+        g = tree.geometry.to_c()
+        check(lib().lpm6cu_fib_create(device, C.byref(g), tree.keys.ctypes.data, tree.values.ctypes.data,
+                                      C.byref(h)))
+        return cls(h.value, device)
+
+    @classmethod
+    def wrap_device(cls, geometry: Geometry, keys, values, device: int) -> "Fib":
+        """Over device tensors the caller owns (e.g. filled by an NCCL broadcast)."""
+        h = C.c_void_p()
+        g = geometry.to_c()
+        check(lib().lpm6cu_fib_wrap_device(device, C.byref(g), keys.data_ptr(), values.data_ptr(), C.byref(h)))
+        return cls(h.value, device, keepalive=(keys, values))
+
+    def close(self) -> None:
+        if self._h and self._h.value:
+            lib().lpm6cu_fib_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- introspection --------------------------------------------------------
+    @property
+    def geometry(self) -> Geometry:
+        g = Geometry_t()
+        check(lib().lpm6cu_fib_geometry(self._h, C.byref(g)))
+        return Geometry.from_c(g)
+
+    def device_arrays(self) -> tuple[int, int]:
+        k, v = C.c_void_p(), C.c_void_p()
+        check(lib().lpm6cu_fib_device_arrays(self._h, C.byref(k), C.byref(v)))
+        return k.value, v.value
+
+    def kernel_config(self) -> dict:
+        c = KernelConfig_t()
+        check(lib().lpm6cu_fib_kernel_config(self._h, C.byref(c)))
+        return {"lanes_per_query": c.lanes_per_query, "smem_levels": c.smem_levels,
+                "ctas_per_sm": c.ctas_per_sm, "threads_per_cta": c.threads_per_cta}
+
+    def set_kernel_config(self, lanes_per_query: int = 0, smem_levels: int | None = None,
+                          ctas_per_sm: int = 0, threads_per_cta: int = 0) -> dict:
+        c = KernelConfig_t()
+        c.lanes_per_query = lanes_per_query
+        c.smem_levels = 0xFF if smem_levels is None else smem_levels
+        c.ctas_per_sm = ctas_per_sm
+        c.threads_per_cta = threads_per_cta
+        check(lib().lpm6cu_fib_set_kernel_config(self._h, C.byref(c)))
+        return self.kernel_config()
+
+    # -- lookup ---------------------------------------------------------------
+    def lookup_batch(self, addrs, out=None, stream=None):
+        """Next hops of n 16-byte little-endian u128 addresses.
+
+        ``addrs``: torch CUDA tensor or numpy array whose bytes are n x 16-byte
+        addresses (e.g. uint64[n, 2] as (lo, hi) or uint8[n, 16]). ``out``: a
+        buffer of n value-width elements on the same side (allocated when None).
+        Device buffers: one asynchronous kernel launch on ``stream`` (default:
+        torch's current stream). Host buffers: pipelined copy-in/lookup/copy-out,
+        returns when ``out`` is filled.
+        """
+        vb = self.geometry.value_bytes
+        aptr, n, adev = _ptr_len(addrs, 16)
+        if out is None:
+            if adev:
+                torch = _torch()
+                dt = {1: torch.uint8, 2: torch.int16, 4: torch.int32}[vb]
+                out = torch.empty(n, dtype=dt, device=addrs.device)
+            else:
+                out = np.empty(n, _NP_VDT[vb])
+        optr, nout, odev = _ptr_len(out, vb)
+        if nout < n:
+            raise Lpm6Error(9, f"out holds {nout} next hops, need {n}")
+        if adev != odev:
+            raise Lpm6Error(9, "addrs and out must both be device or both be host buffers")
+        s = _stream_handle(stream) if adev else None
+        check(lib().lpm6cu_lookup_batch(self._h, aptr, n, optr, s))
+        return out
+
+
+class QueryGen:
+    """Device-side generator of a workload's address stream (bit-identical to the host one)."""
+
+    def __init__(self, workload: int | str, fib: FibTable, device: int = 0):
+        from .fib import WORKLOADS
+        wid = WORKLOADS[workload] if isinstance(workload, str) else int(workload)
+        h = C.c_void_p()
+        rules = fib.rules
+        check(lib().lpm6cu_querygen_create(device, wid, _rules_ptr(rules), len(rules), C.byref(h)))
+        self._h = h
+        self.device = device
+
+    def run(self, first: int, n: int, out, stream=None):
+        ptr, cap, dev = _ptr_len(out, 16)
+        if not dev or cap < n:
+            raise Lpm6Error(9, "out must be a device buffer of >= n 16-byte addresses")
+        check(lib().lpm6cu_querygen_run(self._h, first, n, ptr, _stream_handle(stream)))
+        return out
+
+    def close(self):
+        if self._h and self._h.value:
+            lib().lpm6cu_querygen_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def probe_l2_gather(device: int, buffer_bytes: int, line_bytes: int = 128) -> float:
+    v = C.c_double(0)
+    check(lib().lpm6cu_probe_l2_gather(device, buffer_bytes, line_bytes, C.byref(v)))
+    return v.value
+
+
+def probe_smem(device: int) -> float:
+    v = C.c_double(0)
+    check(lib().lpm6cu_probe_smem(device, C.byref(v)))
+    return v.value

@@ -1,0 +1,159 @@
+"""GPU parity: the sm_100a lookup (through the C ABI) vs the CPU oracle.
+
+Every comparison is bit-exact. The oracle is the C restatement
+(oracle/lpm6_oracle.c, pinned to the reference in test_oracle.py); where
+oracle/_ref is present the reference's own lookup_interval_oracle is checked too.
+"""
+import numpy as np
+import pytest
+
+from _util import addrs_from_keys, boundary_probe_keys, random_fib_rules
+
+pytestmark = pytest.mark.gpu
+
+LANES = (4, 8, 16)
+
+
+def oracle_next_hops(orc, imap_b, imap_nh, addrs):
+    out, _ = orc.lookup_batch(0, imap_b, imap_nh, addrs, threads=8)
+    return out
+
+
+def run_lookup(cuda, fib_dev, addrs_np):
+    torch = cuda
+    a = torch.from_numpy(addrs_np.view(np.uint8).reshape(-1, 16)).cuda()
+    out = fib_dev.lookup_batch(a)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().view({1: np.uint8, 2: np.uint16, 4: np.uint32}[out.element_size()])
+
+
+def check_fib(lpm, orc, cuda, fib, addrs, lanes=LANES, smem_levels=(None, 0)):
+    imap = lpm.build_intervals(fib)
+    st, ob, onh = orc.build_intervals(fib.rules, fib.default_next_hop)
+    assert st == 0
+    np.testing.assert_array_equal(imap.boundaries, ob)
+    np.testing.assert_array_equal(imap.next_hops, onh)
+    want = oracle_next_hops(orc, ob, onh, addrs)
+    dev = lpm.Fib.build(fib)
+    for g in lanes:
+        for t in smem_levels:
+            dev.set_kernel_config(lanes_per_query=g, smem_levels=t)
+            got = run_lookup(cuda, dev, addrs).astype(np.uint32)
+            bad = np.nonzero(got != want)[0]
+            assert len(bad) == 0, (f"G={g} T={t}: {len(bad)} mismatches, first key "
+                                   f"{int(addrs[bad[0], 1]):#x} want {want[bad[0]]} got {got[bad[0]]}")
+    return dev, want
+
+
+def test_c0_full_workload(lpm, orc, cuda):
+    """C0: 1,048,576 queries, whole-tree-in-smem and L2 variants, device query generator == host."""
+    info = lpm.workload_info("C0")
+    fib = lpm.workload_fib(info.fib_kind)
+    addrs = lpm.workload_queries_host("C0", fib, 0, info.n_queries)
+    torch = cuda
+    gen = lpm.QueryGen("C0", fib)
+    d = torch.empty((info.n_queries, 16), dtype=torch.uint8, device="cuda")
+    gen.run(0, info.n_queries, d)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(d.cpu().numpy().view(np.uint64).reshape(-1, 2), addrs)
+    check_fib(lpm, orc, cuda, fib, addrs, smem_levels=(None, 0, 1, 2, 3))
+
+
+@pytest.mark.parametrize("n,with_default", [(0, False), (0, True), (1, False), (10, True), (1000, False),
+                                            (10000, True), (100000, False)])
+def test_random_fibs_boundaries(lpm, orc, cuda, n, with_default):
+    """Random FIBs (depth 0..4): every boundary and boundary+-1, ::, all-ones, random and in-prefix keys."""
+    from paper_2604_14650_b200.fib import PREFIX_DTYPE
+    rng = np.random.default_rng(1000 + n)
+    rules = random_fib_rules(rng, n, PREFIX_DTYPE, with_default)
+    fib = lpm.FibTable(default_next_hop=int(rng.integers(0, 200)), rules=rules)
+    imap = lpm.build_intervals(fib)
+    keys = np.concatenate([boundary_probe_keys(imap.boundaries), rng.integers(0, 2**64, 20000, dtype=np.uint64)])
+    if len(rules):
+        pick = rules[rng.integers(0, len(rules), 20000)]
+        ln = pick["length"].astype(np.uint64)
+        keep = np.where(ln == 0, np.uint64(0), (~np.uint64(0)) << (np.uint64(64) - ln))
+        keys = np.concatenate([keys, (pick["value_hi"] & keep) | (rng.integers(0, 2**64, 20000, dtype=np.uint64) & ~keep)])
+    addrs = addrs_from_keys(keys, rng)
+    check_fib(lpm, orc, cuda, fib, addrs)
+
+
+@pytest.mark.parametrize("vb", [1, 2, 4])
+def test_value_widths(lpm, orc, cuda, vb):
+    from paper_2604_14650_b200.fib import PREFIX_DTYPE
+    rng = np.random.default_rng(vb)
+    rules = random_fib_rules(rng, 3000, PREFIX_DTYPE, True)
+    top = {1: 255, 2: 65535, 4: 0xFFFFFFFE}[vb]
+    rules["next_hop"] = rng.integers(1, top + 1, len(rules), dtype=np.uint64).astype(np.uint32)
+    fib = lpm.FibTable(7, rules)
+    imap = lpm.build_intervals(fib)
+    addrs = addrs_from_keys(np.concatenate([boundary_probe_keys(imap.boundaries),
+                                            rng.integers(0, 2**64, 5000, dtype=np.uint64)]), rng)
+    dev, _ = check_fib(lpm, orc, cuda, fib, addrs, lanes=(8,), smem_levels=(None,))
+    assert dev.geometry.value_bytes == vb
+
+
+def test_reference_oracle_agrees(lpm, orc, ref, cuda):
+    """The compiled reference's lookup_interval_oracle on the same C1 sample."""
+    info = lpm.workload_info("C1")
+    fib = lpm.workload_fib(info.fib_kind)
+    addrs = lpm.workload_queries_host("C1", fib, 0, 1 << 20)
+    st, rmap = ref.build_intervals(fib.rules, fib.default_next_hop)
+    assert st == 0
+    want = rmap.lookup(addrs[:, 1], threads=8)
+    dev = lpm.Fib.build(fib)
+    got = run_lookup(cuda, dev, addrs)
+    np.testing.assert_array_equal(got.astype(np.uint32), want)
+
+
+def test_host_buffers_pipeline(lpm, orc, cuda):
+    """lookup_batch with host (numpy) buffers: chunked H2D/lookup/D2H path."""
+    info = lpm.workload_info("C1")
+    fib = lpm.workload_fib(info.fib_kind)
+    n = (1 << 24) + 12345  # > 2 staging chunks, ragged tail
+    addrs = lpm.workload_queries_host("C1", fib, 5, n)
+    imap = lpm.build_intervals(fib)
+    want = oracle_next_hops(orc, imap.boundaries, imap.next_hops, addrs)
+    dev = lpm.Fib.build(fib)
+    got = dev.lookup_batch(addrs)
+    np.testing.assert_array_equal(got.astype(np.uint32), want)
+
+
+def test_corrupted_device_fib_is_detected(lpm, orc, cuda):
+    """Fault injection: flipping a leaf key on the device must surface as a parity failure."""
+    torch = cuda
+    info = lpm.workload_info("C0")
+    fib = lpm.workload_fib(info.fib_kind)
+    imap = lpm.build_intervals(fib)
+    tree = lpm.build_tree(imap)
+    g = tree.geometry
+    keys = tree.keys.copy()
+    victim = g.level_start[g.depth] + g.num_keys // 2
+    keys[victim] += np.uint64(1)  # the boundary moves one key to the right
+    dk = torch.from_numpy(keys.view(np.int64)).cuda()
+    dv = torch.from_numpy(tree.values.view(np.uint8)).cuda()
+    dev = lpm.Fib.wrap_device(g, dk, dv, 0)
+    probe = addrs_from_keys(np.array([tree.keys[victim]], np.uint64))
+    want = oracle_next_hops(orc, imap.boundaries, imap.next_hops, probe)
+    got = run_lookup(cuda, dev, probe).astype(np.uint32)
+    assert got[0] != want[0]
+
+
+def test_c1_full_size(lpm, orc, cuda):
+    """C1 at BASELINE size: 268,435,456 queries, every one checked against the oracle."""
+    torch = cuda
+    info = lpm.workload_info("C1")
+    fib = lpm.workload_fib(info.fib_kind)
+    imap = lpm.build_intervals(fib)
+    dev = lpm.Fib.build(fib)
+    gen = lpm.QueryGen("C1", fib)
+    chunk = 1 << 26
+    d = torch.empty((chunk, 16), dtype=torch.uint8, device="cuda")
+    mism = 0
+    for c in range(info.n_queries // chunk):
+        gen.run(c * chunk, chunk, d)
+        out = dev.lookup_batch(d)
+        host_addrs = d.cpu().numpy().view(np.uint64).reshape(-1, 2)
+        want = oracle_next_hops(orc, imap.boundaries, imap.next_hops, host_addrs)
+        mism += int(np.count_nonzero(out.cpu().numpy().astype(np.uint32) != want))
+    assert mism == 0
