@@ -145,7 +145,7 @@ def roofline(geom, w, l2_gbs, smem_gbs, hbm_gbs, smem_cap=232448):
     levels = d + 1
     best = None
     for T in range(0, levels + 1):
-        staged = (geom.total_keys if T >= levels else geom.level_start[T]) * 8 if T else 0
+        staged = (geom.total_words if T >= levels else geom.level_start[T]) * 8 if T else 0
         if staged > smem_cap:
             break
         terms = {"hbm": hbm_gbs * 1e9 / (16 + w)}
@@ -283,31 +283,27 @@ def main():
     t0 = time.perf_counter()
     if rank == 0:
         imap = lpm.build_intervals(fib)
-        tree = lpm.build_tree(imap, 16, vb)
+        tree = lpm.build_tree(imap, vb)
         geom = tree.geometry
     build_ms = (time.perf_counter() - t0) * 1e3
     if dist is not None:
         obj = [geom if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         geom = obj[0]
-        nk, nv = geom.total_keys, geom.leaf_nodes * geom.k * geom.value_bytes
-        keys_t = torch.empty(nk, dtype=torch.int64, device="cuda")
-        vals_t = torch.empty(nv, dtype=torch.uint8, device="cuda")
+        lines_t = torch.empty(geom.total_words, dtype=torch.int64, device="cuda")
         if rank == 0:
-            keys_t.copy_(torch.from_numpy(tree.keys.view(np.int64)))
-            vals_t.copy_(torch.from_numpy(tree.values.view(np.uint8)))
+            lines_t.copy_(torch.from_numpy(tree.lines.view(np.int64)))
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        dist.broadcast(keys_t, 0)
-        dist.broadcast(vals_t, 0)
+        dist.broadcast(lines_t, 0)
         e1.record()
         torch.cuda.synchronize()
         bcast_ms = e0.elapsed_time(e1)
         t = torch.tensor([bcast_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         bcast_ms = float(t.item())
-        fdev = lpm.Fib.wrap_device(geom, keys_t, vals_t, dev_index)
+        fdev = lpm.Fib.wrap_device(geom, lines_t, dev_index)
     else:
         fdev = lpm.Fib.from_tree(tree, dev_index)
         bcast_ms = 0.0
@@ -322,7 +318,7 @@ def main():
     torch.cuda.synchronize()
 
     # -- roofline denominators measured on this device --------------------------------------------
-    tree_bytes = geom.total_keys * 8
+    tree_bytes = geom.tree_bytes
     l2_gbs = lpm.probe_l2_gather(dev_index, max(tree_bytes, 1 << 22), 128)
     smem_gbs = lpm.probe_smem(dev_index)
     hbm_gbs, hbm_src = hbm_peak()
@@ -404,8 +400,8 @@ def main():
     sweep = None
     if args.sweep and rank == 0:
         sweep = []
-        for g in (4, 8, 16):
-            for t_lv in range(0, geom.depth + 2):
+        for g in (4,):
+            for t_lv in range(0, geom.depth + 1):
                 try:
                     fdev.set_kernel_config(lanes_per_query=g, smem_levels=t_lv)
                 except Exception:
@@ -455,7 +451,8 @@ def main():
         "data": f"synthetic: seeded {info.name} FIB ({len(fib)} prefixes) and query generator, "
                 f"{n} queries per GPU generated on device",
         "config": {"workload": info.name, "fib_prefixes": len(fib), "intervals": geom.num_keys,
-                   "tree_depth": geom.depth, "node_keys": geom.k, "tree_bytes": tree_bytes,
+                   "tree_depth": geom.depth, "node_keys": geom.k, "leaf_keys": geom.leaf_keys,
+                   "tree_bytes": tree_bytes,
                    "queries_per_gpu": n, "value_bytes": vb, "kernel": cfg,
                    "l2_flush": f"not needed: each step streams {n * 16 / 1e9:.1f} GB of addresses (> 126 MB L2)",
                    "parallelism": f"dp{ws} (query batches; FIB replicated by NCCL broadcast)"},

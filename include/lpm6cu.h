@@ -69,18 +69,22 @@ typedef struct {
 
 #define LPM6CU_MAX_LEVELS 9
 
-/* Geometry of the B200 tree layout (compact levels of 128-byte, 16-key nodes).
- * Counterpart of lpm6::TreeGeometry (tree.hpp:18-33). */
+/* Geometry of the B200 tree layout: one array of 128-byte lines. Internal
+ * lines hold k = 16 separator keys; leaf lines hold leaf_keys boundary keys
+ * followed by their next hops. Counterpart of lpm6::TreeGeometry (tree.hpp:18-33). */
 typedef struct {
-  uint32_t k;           /* keys per node (16) */
+  uint32_t k;           /* keys per internal node (16) */
   uint32_t b;           /* arity, k + 1 */
-  uint32_t depth;       /* internal levels; a lookup visits depth + 1 nodes */
-  uint32_t value_bytes; /* 1, 2 or 4 */
+  uint32_t depth;       /* internal levels; a lookup visits depth + 1 lines */
+  uint32_t value_bytes; /* next-hop width: 1, 2 or 4 */
+  uint32_t leaf_keys;   /* keys per leaf line: 14, 12 or 8 for 1-, 2-, 4-byte next hops */
+  uint32_t image_levels;/* the shared-memory image covers levels [1, image_levels) */
   uint64_t num_keys;    /* m, real interval boundaries */
-  uint64_t leaf_nodes;  /* ceil(m / k) */
-  uint64_t total_keys;  /* length of the key array */
+  uint64_t leaf_nodes;  /* ceil(m / leaf_keys) */
+  uint64_t total_words; /* length of the array in u64 words: tree lines, then the image */
+  uint64_t image_start; /* word offset of the bank-swizzled copy of levels 1.. staged by TMA */
   uint64_t level_nodes[LPM6CU_MAX_LEVELS]; /* reachable nodes per level (level depth = leaves) */
-  uint64_t level_start[LPM6CU_MAX_LEVELS]; /* key offset of each level */
+  uint64_t level_start[LPM6CU_MAX_LEVELS]; /* u64-word offset of each level */
   uint32_t default_next_hop;
   uint32_t reserved;
 } lpm6cu_geometry;
@@ -88,14 +92,15 @@ typedef struct {
 typedef struct {
   uint32_t merge_adjacent; /* IntervalBuildOptions::merge_adjacent (intervals.hpp:28); default 1 */
   uint32_t value_bytes;    /* 0 = narrowest width holding every next hop */
-  uint32_t k;              /* keys per node; 0 = 16 (the only width the kernels take) */
+  uint32_t reserved0;
   uint32_t reserved;
 } lpm6cu_build_opts;
 
 /* Kernel shape; 0 in a field = automatic. */
 typedef struct {
-  uint32_t lanes_per_query; /* 4, 8 or 16 lanes cooperate on one 128-byte node */
-  uint32_t smem_levels;     /* top tree levels staged in shared memory by TMA; 0xFF = auto */
+  uint32_t lanes_per_query; /* lanes cooperating on one 128-byte line in the L2 levels (4) */
+  uint32_t smem_levels;     /* top levels staged in shared memory by TMA and searched one
+                               thread per query; 0xFF = auto */
   uint32_t ctas_per_sm;
   uint32_t threads_per_cta;
 } lpm6cu_kernel_config;
@@ -114,14 +119,15 @@ int lpm6_build_intervals(const lpm6cu_prefix* rules, uint64_t n, uint32_t defaul
                          int merge_adjacent, uint64_t* boundaries, uint32_t* next_hops,
                          uint64_t capacity, uint64_t* m_out);
 
-/* Geometry for m boundaries at k keys per node. */
-int lpm6_plan_layout(uint64_t m, uint32_t k, lpm6cu_geometry* g);
+/* Geometry for m boundaries at a next-hop width of value_bytes. */
+int lpm6_plan_layout(uint64_t m, uint32_t value_bytes, lpm6cu_geometry* g);
 
-/* Lay out the tree. With keys == NULL only *g is filled (to size the arrays:
- * g->total_keys u64 keys, g->leaf_nodes * k * g->value_bytes value bytes). */
+/* Lay out the tree. With lines == NULL only *g is filled (to size the arrays:
+ * g->total_words u64 words of lines, g->leaf_nodes * g->leaf_keys leaf values).
+ * leaf_values (optional) receives the next hop of every leaf slot as u32. */
 int lpm6_build_tree(const uint64_t* boundaries, const uint32_t* next_hops, uint64_t m,
-                    uint32_t default_next_hop, uint32_t k, uint32_t value_bytes,
-                    lpm6cu_geometry* g, uint64_t* keys, void* values);
+                    uint32_t default_next_hop, uint32_t value_bytes, lpm6cu_geometry* g,
+                    uint64_t* lines, uint32_t* leaf_values);
 
 /* Parse "<ipv6>/<len> <next_hop>" (fib.cpp:72-105). */
 int lpm6_parse_prefix(const char* text, lpm6cu_prefix* out, int* host_bits_masked);
@@ -133,16 +139,14 @@ int lpm6cu_fib_build(int device, const lpm6cu_prefix* rules, uint64_t n, uint32_
                      const lpm6cu_build_opts* opts, lpm6cu_fib** out);
 
 /* From a host layout (lpm6_build_tree output); copies into device memory it owns. */
-int lpm6cu_fib_create(int device, const lpm6cu_geometry* g, const uint64_t* keys,
-                      const void* values, lpm6cu_fib** out);
+int lpm6cu_fib_create(int device, const lpm6cu_geometry* g, const uint64_t* lines, lpm6cu_fib** out);
 
-/* Over device arrays the caller owns (e.g. filled by an NCCL broadcast); not freed
- * by lpm6cu_fib_destroy. */
-int lpm6cu_fib_wrap_device(int device, const lpm6cu_geometry* g, const void* d_keys,
-                           const void* d_values, lpm6cu_fib** out);
+/* Over a device line array the caller owns (e.g. filled by an NCCL broadcast); not
+ * freed by lpm6cu_fib_destroy. */
+int lpm6cu_fib_wrap_device(int device, const lpm6cu_geometry* g, const void* d_lines, lpm6cu_fib** out);
 
 int lpm6cu_fib_geometry(const lpm6cu_fib* fib, lpm6cu_geometry* g);
-int lpm6cu_fib_device_arrays(const lpm6cu_fib* fib, const void** d_keys, const void** d_values);
+int lpm6cu_fib_device_lines(const lpm6cu_fib* fib, const void** d_lines);
 int lpm6cu_fib_set_kernel_config(lpm6cu_fib* fib, const lpm6cu_kernel_config* cfg);
 int lpm6cu_fib_kernel_config(const lpm6cu_fib* fib, lpm6cu_kernel_config* cfg);
 void lpm6cu_fib_destroy(lpm6cu_fib* fib);

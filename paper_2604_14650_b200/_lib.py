@@ -38,13 +38,15 @@ class Prefix_t(C.Structure):
 
 class Geometry_t(C.Structure):
     _fields_ = [("k", C.c_uint32), ("b", C.c_uint32), ("depth", C.c_uint32), ("value_bytes", C.c_uint32),
-                ("num_keys", C.c_uint64), ("leaf_nodes", C.c_uint64), ("total_keys", C.c_uint64),
+                ("leaf_keys", C.c_uint32), ("image_levels", C.c_uint32),
+                ("num_keys", C.c_uint64), ("leaf_nodes", C.c_uint64), ("total_words", C.c_uint64),
+                ("image_start", C.c_uint64),
                 ("level_nodes", C.c_uint64 * MAX_LEVELS), ("level_start", C.c_uint64 * MAX_LEVELS),
                 ("default_next_hop", C.c_uint32), ("reserved", C.c_uint32)]
 
 
 class BuildOpts_t(C.Structure):
-    _fields_ = [("merge_adjacent", C.c_uint32), ("value_bytes", C.c_uint32), ("k", C.c_uint32),
+    _fields_ = [("merge_adjacent", C.c_uint32), ("value_bytes", C.c_uint32), ("reserved0", C.c_uint32),
                 ("reserved", C.c_uint32)]
 
 
@@ -70,13 +72,13 @@ SIGNATURES = {
     "lpm6cu_version": (C.c_char_p, []),
     "lpm6_build_intervals": (I32, [P, U64, U32, I32, P, P, U64, C.POINTER(U64)]),
     "lpm6_plan_layout": (I32, [U64, U32, C.POINTER(Geometry_t)]),
-    "lpm6_build_tree": (I32, [P, P, U64, U32, U32, U32, C.POINTER(Geometry_t), P, P]),
+    "lpm6_build_tree": (I32, [P, P, U64, U32, U32, C.POINTER(Geometry_t), P, P]),
     "lpm6_parse_prefix": (I32, [C.c_char_p, C.POINTER(Prefix_t), C.POINTER(I32)]),
     "lpm6cu_fib_build": (I32, [I32, P, U64, U32, C.POINTER(BuildOpts_t), C.POINTER(P)]),
-    "lpm6cu_fib_create": (I32, [I32, C.POINTER(Geometry_t), P, P, C.POINTER(P)]),
-    "lpm6cu_fib_wrap_device": (I32, [I32, C.POINTER(Geometry_t), P, P, C.POINTER(P)]),
+    "lpm6cu_fib_create": (I32, [I32, C.POINTER(Geometry_t), P, C.POINTER(P)]),
+    "lpm6cu_fib_wrap_device": (I32, [I32, C.POINTER(Geometry_t), P, C.POINTER(P)]),
     "lpm6cu_fib_geometry": (I32, [P, C.POINTER(Geometry_t)]),
-    "lpm6cu_fib_device_arrays": (I32, [P, C.POINTER(P), C.POINTER(P)]),
+    "lpm6cu_fib_device_lines": (I32, [P, C.POINTER(P)]),
     "lpm6cu_fib_set_kernel_config": (I32, [P, C.POINTER(KernelConfig_t)]),
     "lpm6cu_fib_kernel_config": (I32, [P, C.POINTER(KernelConfig_t)]),
     "lpm6cu_fib_destroy": (None, [P]),

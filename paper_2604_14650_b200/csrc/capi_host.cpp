@@ -32,9 +32,12 @@ void export_geometry(const TreeLayout& t, lpm6cu_geometry* g) {
   g->b = t.b;
   g->depth = t.depth;
   g->value_bytes = t.value_bytes;
+  g->leaf_keys = t.leaf_keys;
   g->num_keys = t.num_keys;
   g->leaf_nodes = t.leaf_nodes;
-  g->total_keys = t.total_keys;
+  g->total_words = t.total_words;
+  g->image_levels = t.image_levels;
+  g->image_start = t.image_start;
   for (int l = 0; l < kMaxLevels; ++l) {
     g->level_nodes[l] = t.level_nodes[l];
     g->level_start[l] = t.level_start[l];
@@ -45,16 +48,14 @@ void export_geometry(const TreeLayout& t, lpm6cu_geometry* g) {
 Tree build_device_tree(const lpm6cu_prefix* rules, uint64_t n, uint32_t default_nh,
                        const lpm6cu_build_opts* opts) {
   IntervalBuildOptions io;
-  u32 k = 16, vb = 0;
+  u32 vb = 0;
   if (opts) {
     io.merge_adjacent = opts->merge_adjacent != 0;
     vb = opts->value_bytes;
-    if (opts->k) k = opts->k;
   }
-  if (k != 16) throw Error(Errc::InvalidArgument, "the B200 kernels take 16-key (128-byte) nodes");
   auto prefixes = to_prefixes(rules, n);
   IntervalMap map = build_intervals(std::span<const Prefix>(prefixes), default_nh, io);
-  return build_tree(map, k, vb);
+  return build_tree(map, vb);
 }
 
 }  // namespace lpm6::capi
@@ -103,23 +104,23 @@ int lpm6_build_intervals(const lpm6cu_prefix* rules, uint64_t n, uint32_t defaul
   });
 }
 
-int lpm6_plan_layout(uint64_t m, uint32_t k, lpm6cu_geometry* g) {
-  return guard([&] { export_geometry(plan_layout(m, k ? k : 16), g); });
+int lpm6_plan_layout(uint64_t m, uint32_t value_bytes, lpm6cu_geometry* g) {
+  return guard([&] { export_geometry(plan_layout(m, value_bytes), g); });
 }
 
 int lpm6_build_tree(const uint64_t* boundaries, const uint32_t* next_hops, uint64_t m,
-                    uint32_t default_nh, uint32_t k, uint32_t value_bytes, lpm6cu_geometry* g,
-                    uint64_t* keys, void* values) {
+                    uint32_t default_nh, uint32_t value_bytes, lpm6cu_geometry* g, uint64_t* lines,
+                    uint32_t* leaf_values) {
   return guard([&] {
     if (m < 1 || !boundaries || !next_hops) throw Error(Errc::InvalidArgument, "empty interval map");
     IntervalMap map;
     map.boundaries.assign(boundaries, boundaries + m);
     map.next_hops.assign(next_hops, next_hops + m);
     map.default_next_hop = default_nh;
-    Tree t = build_tree(map, k ? k : 16, value_bytes);
+    Tree t = build_tree(map, value_bytes);
     export_geometry(t.g, g);
-    if (keys) std::memcpy(keys, t.keys.data(), t.keys.size() * sizeof(u64));
-    if (values) std::memcpy(values, t.values.data(), t.values.size());
+    if (lines) std::memcpy(lines, t.lines.data(), t.lines.size() * sizeof(u64));
+    if (leaf_values) std::memcpy(leaf_values, t.leaf_values.data(), t.leaf_values.size() * sizeof(u32));
   });
 }
 

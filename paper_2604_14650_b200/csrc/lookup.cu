@@ -1,31 +1,38 @@
-// sm_100a batched LPM lookup kernels and the device half of the C ABI.
+// sm_100a batched LPM lookup kernel and the device half of the C ABI.
 //
-// One query = one predecessor search down the compact 16-key / 128-byte-node
-// tree (layout.hpp). The kernel is the GPU form of the reference's
-// search_batch + Listing 1:
+// One query = one predecessor search down the B200 tree (layout.hpp): internal
+// 128-byte lines of 16 separators, leaf lines of kL keys + kL next hops. The
+// kernel is the GPU form of the reference's search_batch (S:299-307,
+// P:812-847) over Listing 1's node search, in two phases per
+// 32-query warp tile (lane L owns query L):
 //
-//  * a group of G lanes (G = 4, 8 or 16) cooperates on one node: lane j holds
-//    keys [j*16/G, (j+1)*16/G) of the node, so one warp-wide load instruction
-//    fetches one full 128-byte line per query (256-bit LDG for G = 4);
-//  * the node rank is computed branch-free: every lane compares its keys
-//    against the broadcast query, then __ballot_sync/__popc (G = 8, 16) or a
-//    two-step shuffle sum (G = 4) gives the count of keys <= query — the rank
-//    of Listing 1's cmpge-mask + popcnt;
-//  * each group carries G queries at once and the descent is fully unrolled
-//    over the tree depth (template), so every level issues G independent node
-//    loads per group before the first compare (the batching of P:812-847 as
-//    memory-level parallelism);
-//  * the top `smem_levels` levels are staged into shared memory once per CTA
-//    with cp.async.bulk (TMA bulk copy) on an mbarrier; deeper levels are read
-//    through L2 (the whole 1M-prefix tree fits in B200's L2);
-//  * query addresses are read with coalesced 16-byte loads (one per lane,
-//    L1::no_allocate, L2 evict_first) and next hops written with coalesced
-//    streaming stores; lane L of a warp owns query L of the warp's 32-query tile;
-//  * CTAs are persistent (grid = SMs x resident CTAs) and stride over tiles.
+//  Phase A — top `smem_levels` levels, one thread per query. These levels are
+//    staged into shared memory once per CTA by cp.async.bulk (TMA bulk copy)
+//    on an mbarrier. Each thread ranks its own query in a 16-key node with a
+//    branch-free 5-probe binary search (count of keys <= q, i.e. Listing 1's
+//    popcnt(cmpge)). Upper levels are touched by every query, so a
+//    thread-per-query search here costs a fraction of a shared-memory
+//    wavefront per query per level instead of a full 128-byte line.
+//  Phase B — the remaining levels through L1/L2, four lanes per query: lane j of
+//    a 4-lane group loads bytes [32j, 32j+32) of the line with one 256-bit load,
+//    so a warp-wide load fetches exactly one full 128-byte line per query; the
+//    lanes compare their keys against the broadcast query and __ballot_sync +
+//    __popc give the rank. Each group carries its 4 queries at once and the
+//    descent is unrolled over the depth (template), so every level has 4
+//    independent line loads in flight per group (the batching of P:812-847 as
+//    memory-level parallelism).
+//  Leaf — the leaf line carries the next hops (P:695-705 folded into the leaf
+//    fetch): after the leaf rank, the lane holding the value bytes extracts the
+//    group's 4 next hops and writes them with one coalesced streaming store.
+//
+// Query addresses are read with coalesced 16-byte-stride loads of the top word
+// (L1::no_allocate, L2 evict_first) — each step streams GBs of addresses
+// through L2 while the tree stays resident (evict_last on tree lines). CTAs are
+// persistent (grid = SMs x resident CTAs) and stride over tiles.
 //
 // Results are the reference's: key = min(addr >> 64, 0xFFFF...FFFE)
 // (types.hpp:25), internal child = node * 17 + rank, leaf ordinal =
-// leaf_node * 16 + rank - 1, next hop = values[ordinal].
+// rank - 1, next hop = the value of that leaf slot.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -45,7 +52,6 @@ namespace {
 
 constexpr int kMaxKernelDepth = 7;
 constexpr unsigned kFull = 0xFFFFFFFFu;
-constexpr int kK = 16;  // keys per node
 
 void check_cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess)
@@ -72,30 +78,10 @@ __device__ __forceinline__ uint4 ld_stream_v4(const uint4* p, uint64_t pol) {
   return r;
 }
 
-template <int KPL>
-__device__ __forceinline__ void ld_node_global(const unsigned long long* p, unsigned long long (&k)[KPL]) {
-  if constexpr (KPL == 1) {
-    asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(k[0]) : "l"(p));
-  } else if constexpr (KPL == 2) {
-    asm volatile("ld.global.nc.v2.u64 {%0,%1}, [%2];" : "=l"(k[0]), "=l"(k[1]) : "l"(p));
-  } else {
-    asm volatile("ld.global.nc.L2::evict_last.v4.u64 {%0,%1,%2,%3}, [%4];"
-                 : "=l"(k[0]), "=l"(k[1]), "=l"(k[2]), "=l"(k[3])
-                 : "l"(p));
-  }
-}
-
-template <int KPL>
-__device__ __forceinline__ void ld_node_shared(const unsigned long long* p, unsigned long long (&k)[KPL]) {
-  const uint32_t a = smem_u32(p);
-  if constexpr (KPL == 1) {
-    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(k[0]) : "r"(a));
-  } else if constexpr (KPL == 2) {
-    asm volatile("ld.shared.v2.u64 {%0,%1}, [%2];" : "=l"(k[0]), "=l"(k[1]) : "r"(a));
-  } else {
-    asm volatile("ld.shared.v2.u64 {%0,%1}, [%2];" : "=l"(k[0]), "=l"(k[1]) : "r"(a));
-    asm volatile("ld.shared.v2.u64 {%0,%1}, [%2];" : "=l"(k[2]), "=l"(k[3]) : "r"(a + 16));
-  }
+__device__ __forceinline__ void ld_line_quarter(const unsigned long long* p, unsigned long long (&w)[4]) {
+  asm volatile("ld.global.nc.L2::evict_last.v4.u64 {%0,%1,%2,%3}, [%4];"
+               : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
+               : "l"(p));
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -132,42 +118,71 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // ---- kernel -----------------------------------------------------------------
 
 struct LookupParams {
-  const unsigned long long* keys;
-  const unsigned char* values;
-  unsigned long long level_start[LPM6CU_MAX_LEVELS];
+  const unsigned long long* lines;                     // the tree, 16 u64 words per line
+  unsigned long long level_start[LPM6CU_MAX_LEVELS];  // word offset of each level
   const uint4* addrs;
   unsigned char* out;
   unsigned long long n;
-  unsigned int smem_levels;  // levels [0, smem_levels) read from shared memory
-  unsigned int smem_bytes;   // = level_start[smem_levels] * 8
-  unsigned int value_bytes;
+  unsigned long long root[16];  // level 0, compared from the constant bank
+  const unsigned long long* image;  // bank-swizzled copy of levels 1.. (layout.hpp)
+  unsigned int smem_levels;  // phase A levels [0, smem_levels), <= depth
+  unsigned int smem_bytes;   // image bytes staged: (level_start[smem_levels] - 16) * 8
 };
 
-// Count of node keys <= q across the G lanes of this group (Listing 1's
-// popcnt(cmpge(q, node))). Every lane of the group gets the same value.
-template <int G, int KPL>
-__device__ __forceinline__ unsigned group_rank(unsigned long long q, const unsigned long long (&k)[KPL],
-                                               unsigned gmask) {
-  if constexpr (KPL <= 2) {
-    unsigned r = 0;
-#pragma unroll
-    for (int t = 0; t < KPL; ++t) r += __popc(__ballot_sync(kFull, q >= k[t]) & gmask);
-    return r;
-  } else {
-    unsigned c = 0;
-#pragma unroll
-    for (int t = 0; t < KPL; ++t) c += (q >= k[t]) ? 1u : 0u;
-#pragma unroll
-    for (int o = 1; o < G; o <<= 1) c += __shfl_xor_sync(kFull, c, o, G);
-    return c;
-  }
+// Count of the 16 keys of node n of a swizzled shared-memory level that are
+// <= q: branch-free binary search (4 halving probes leave c in [0,15]; the fifth
+// adds key 15). Key p of node n lives at n*16 + ((p + n) & 15) (layout.hpp).
+__device__ __forceinline__ unsigned node_rank_smem(const unsigned long long* lvl, unsigned n, unsigned long long q) {
+  const unsigned long long* nd = lvl + n * 16u;
+  const unsigned rot = n & 15u;
+  unsigned c = (nd[(7u + rot) & 15u] <= q) ? 8u : 0u;
+  c += (nd[(c + 3u + rot) & 15u] <= q) ? 4u : 0u;
+  c += (nd[(c + 1u + rot) & 15u] <= q) ? 2u : 0u;
+  c += (nd[(c + rot) & 15u] <= q) ? 1u : 0u;
+  c += (nd[(c + rot) & 15u] <= q) ? 1u : 0u;
+  return c;
 }
 
-template <int G, int DEPTH>
+// Root rank, one thread per query, against the root keys in the launch
+// parameters (constant bank operands: no load through the LSU at all).
+__device__ __forceinline__ unsigned root_rank(const unsigned long long (&root)[16], unsigned long long q) {
+  unsigned c = 0;
+#pragma unroll
+  for (int p = 0; p < 16; ++p) c += (q >= root[p]) ? 1u : 0u;
+  return c;
+}
+
+// Rank of q over the 4-lane group's line quarter: lane j holds keys 4j..4j+3;
+// `nvalid` of them (per lane) are keys. Listing 1's popcnt(cmpge(q, node)).
+__device__ __forceinline__ unsigned group_rank(unsigned long long q, const unsigned long long (&w)[4], unsigned nvalid,
+                                               unsigned gmask) {
+  unsigned r = 0;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) r += __popc(__ballot_sync(kFull, (t < static_cast<int>(nvalid)) && q >= w[t]) & gmask);
+  return r;
+}
+
+template <int VB>
+struct LeafFmt {
+  static constexpr int kL = VB == 1 ? 14 : VB == 2 ? 12 : 8;  // keys per leaf line
+  static constexpr int kValueLane = (kL * 8) / 32;             // lane holding the next hops
+  static constexpr int kValueOff = kL * 8 - kValueLane * 32;   // their byte offset in that lane's 32 B
+};
+
+template <int VB>
+__device__ __forceinline__ unsigned leaf_value(const unsigned long long (&w)[4], unsigned ord) {
+  const unsigned o = LeafFmt<VB>::kValueOff + ord * VB;  // byte offset within the lane's quarter
+  const unsigned wi = o >> 3;
+  const unsigned long long x = wi == 0 ? w[0] : wi == 1 ? w[1] : wi == 2 ? w[2] : w[3];
+  const unsigned long long v = x >> ((o & 7u) * 8u);
+  return VB == 1 ? static_cast<unsigned>(v & 0xFFu) : VB == 2 ? static_cast<unsigned>(v & 0xFFFFu)
+                                                              : static_cast<unsigned>(v & 0xFFFFFFFFu);
+}
+
+template <int DEPTH, int VB>
 __global__ void __launch_bounds__(256) lpm6_lookup_kernel(const LookupParams p) {
-  constexpr int KPL = kK / G;  // keys per lane
-  constexpr int Q = G;         // queries in flight per group: lane L owns query L of the tile
-  extern __shared__ __align__(128) unsigned long long s_keys[];
+  using F = LeafFmt<VB>;
+  extern __shared__ __align__(128) unsigned long long s_lines[];
   __shared__ __align__(8) uint64_t s_bar;
 
   if (p.smem_bytes > 0) {
@@ -177,7 +192,7 @@ __global__ void __launch_bounds__(256) lpm6_lookup_kernel(const LookupParams p) 
       constexpr uint32_t kChunk = 32768;
       for (uint32_t off = 0; off < p.smem_bytes; off += kChunk) {
         const uint32_t sz = min(kChunk, p.smem_bytes - off);
-        bulk_g2s(reinterpret_cast<char*>(s_keys) + off, reinterpret_cast<const char*>(p.keys) + off, sz,
+        bulk_g2s(reinterpret_cast<char*>(s_lines) + off, reinterpret_cast<const char*>(p.image) + off, sz,
                  &s_bar);
       }
     }
@@ -186,12 +201,16 @@ __global__ void __launch_bounds__(256) lpm6_lookup_kernel(const LookupParams p) 
   }
 
   const unsigned lane = threadIdx.x & 31u;
-  const unsigned j = lane & (G - 1);
-  const unsigned gmask = (G == 32 ? kFull : ((1u << G) - 1u)) << (lane & ~(G - 1u));
+  const unsigned j = lane & 3u;                 // lane within the 4-lane group
+  const unsigned gbase = lane & ~3u;            // first lane (= first query) of the group
+  const unsigned gmask = 0xFu << gbase;
   const unsigned long long warp0 = (static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const unsigned long long nwarps = (static_cast<unsigned long long>(gridDim.x) * blockDim.x) >> 5;
   const uint64_t pol_stream = policy_evict_first();
-  const unsigned T = p.smem_levels;
+  const unsigned TA = p.smem_levels;
+  const unsigned leaf_valid = (F::kL - 4 * static_cast<int>(j)) < 0 ? 0u
+                              : (F::kL - 4 * static_cast<int>(j)) > 4 ? 4u
+                                                                      : static_cast<unsigned>(F::kL - 4 * j);
 
   for (unsigned long long tile = warp0; tile * 32ull < p.n; tile += nwarps) {
     const unsigned long long qi = tile * 32ull + lane;
@@ -202,47 +221,62 @@ __global__ void __launch_bounds__(256) lpm6_lookup_kernel(const LookupParams p) 
     }
     key = key > kMaxQueryKey ? kMaxQueryKey : key;  // types.hpp:25
 
-    unsigned long long qk[Q];
-    unsigned node[Q];
+    // Phase A: this thread's own query through the shared-memory levels.
+    unsigned node = 0;
+    if (DEPTH > 0 && TA > 0) node = root_rank(p.root, key);
 #pragma unroll
-    for (int s = 0; s < Q; ++s) {
-      qk[s] = __shfl_sync(kFull, key, s, G);
-      node[s] = 0;
-    }
+    for (int l = 1; l < DEPTH; ++l)
+      if (static_cast<unsigned>(l) < TA)
+        node = node * 17u + node_rank_smem(s_lines + (p.level_start[l] - 16u), node, key);
 
+    // Phase B: the group's 4 queries, one 128-byte line per query per level.
+    unsigned long long qk[4];
+    unsigned nd[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      qk[s] = __shfl_sync(kFull, key, s, 4);
+      nd[s] = __shfl_sync(kFull, node, s, 4);
+    }
+    unsigned long long w[4][4];
 #pragma unroll
     for (int l = 0; l <= DEPTH; ++l) {
-      unsigned long long kk[Q][KPL];
-      if (static_cast<unsigned>(l) < T) {
-        const unsigned long long* lvl = s_keys + p.level_start[l];
+      if (l < DEPTH && static_cast<unsigned>(l) < TA) continue;
+      const unsigned long long* lvl = p.lines + p.level_start[l] + j * 4u;
 #pragma unroll
-        for (int s = 0; s < Q; ++s) ld_node_shared<KPL>(lvl + node[s] * kK + j * KPL, kk[s]);
-      } else {
-        const unsigned long long* lvl = p.keys + p.level_start[l];
+      for (int s = 0; s < 4; ++s) ld_line_quarter(lvl + nd[s] * 16u, w[s]);
 #pragma unroll
-        for (int s = 0; s < Q; ++s) ld_node_global<KPL>(lvl + node[s] * kK + j * KPL, kk[s]);
-      }
-#pragma unroll
-      for (int s = 0; s < Q; ++s) {
-        const unsigned r = group_rank<G, KPL>(qk[s], kk[s], gmask);
-        node[s] = (l < DEPTH) ? node[s] * (kK + 1) + r : node[s] * kK + r - 1;
+      for (int s = 0; s < 4; ++s) {
+        const unsigned r = group_rank(qk[s], w[s], l < DEPTH ? 4u : leaf_valid, gmask);
+        nd[s] = (l < DEPTH) ? nd[s] * 17u + r : r - 1u;  // leaf: ordinal within the line
       }
     }
 
-    unsigned ord = node[0];
+    // Leaf values: the value lane extracts the group's 4 next hops and stores them.
+    if (j == static_cast<unsigned>(F::kValueLane)) {
+      unsigned v[4];
 #pragma unroll
-    for (int s = 1; s < Q; ++s) ord = (j == static_cast<unsigned>(s)) ? node[s] : ord;
-
-    if (qi < p.n) {
-      if (p.value_bytes == 1) {
-        const unsigned char v = __ldg(p.values + ord);
-        asm volatile("st.global.cs.u8 [%0], %1;" ::"l"(p.out + qi), "h"(static_cast<unsigned short>(v)));
-      } else if (p.value_bytes == 2) {
-        const unsigned short v = __ldg(reinterpret_cast<const unsigned short*>(p.values) + ord);
-        asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(p.out + 2 * qi), "h"(v));
+      for (int s = 0; s < 4; ++s) v[s] = leaf_value<VB>(w[s], nd[s]);
+      const unsigned long long q0 = tile * 32ull + gbase;
+      if (q0 + 3 < p.n) {
+        if constexpr (VB == 1) {
+          const unsigned x = v[0] | (v[1] << 8) | (v[2] << 16) | (v[3] << 24);
+          asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p.out + q0), "r"(x));
+        } else if constexpr (VB == 2) {
+          const unsigned long long x = static_cast<unsigned long long>(v[0] | (v[1] << 16)) |
+                                       (static_cast<unsigned long long>(v[2] | (v[3] << 16)) << 32);
+          asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p.out + 2 * q0), "l"(x));
+        } else {
+          asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p.out + 4 * q0), "r"(v[0]), "r"(v[1]),
+                       "r"(v[2]), "r"(v[3]));
+        }
       } else {
-        const unsigned v = __ldg(reinterpret_cast<const unsigned*>(p.values) + ord);
-        asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p.out + 4 * qi), "r"(v));
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          if (q0 + s >= p.n) break;
+          if constexpr (VB == 1) p.out[q0 + s] = static_cast<unsigned char>(v[s]);
+          else if constexpr (VB == 2) reinterpret_cast<unsigned short*>(p.out)[q0 + s] = static_cast<unsigned short>(v[s]);
+          else reinterpret_cast<unsigned*>(p.out)[q0 + s] = v[s];
+        }
       }
     }
   }
@@ -250,26 +284,26 @@ __global__ void __launch_bounds__(256) lpm6_lookup_kernel(const LookupParams p) 
 
 using KernelFn = void (*)(const LookupParams);
 
-template <int G>
+template <int VB>
 KernelFn pick_depth(int depth) {
   switch (depth) {
-    case 0: return lpm6_lookup_kernel<G, 0>;
-    case 1: return lpm6_lookup_kernel<G, 1>;
-    case 2: return lpm6_lookup_kernel<G, 2>;
-    case 3: return lpm6_lookup_kernel<G, 3>;
-    case 4: return lpm6_lookup_kernel<G, 4>;
-    case 5: return lpm6_lookup_kernel<G, 5>;
-    case 6: return lpm6_lookup_kernel<G, 6>;
-    case 7: return lpm6_lookup_kernel<G, 7>;
+    case 0: return lpm6_lookup_kernel<0, VB>;
+    case 1: return lpm6_lookup_kernel<1, VB>;
+    case 2: return lpm6_lookup_kernel<2, VB>;
+    case 3: return lpm6_lookup_kernel<3, VB>;
+    case 4: return lpm6_lookup_kernel<4, VB>;
+    case 5: return lpm6_lookup_kernel<5, VB>;
+    case 6: return lpm6_lookup_kernel<6, VB>;
+    case 7: return lpm6_lookup_kernel<7, VB>;
     default: return nullptr;
   }
 }
 
-KernelFn pick_kernel(int g, int depth) {
-  switch (g) {
+KernelFn pick_kernel(int vb, int depth) {
+  switch (vb) {
+    case 1: return pick_depth<1>(depth);
+    case 2: return pick_depth<2>(depth);
     case 4: return pick_depth<4>(depth);
-    case 8: return pick_depth<8>(depth);
-    case 16: return pick_depth<16>(depth);
     default: return nullptr;
   }
 }
@@ -314,8 +348,8 @@ struct HostPipeline {
 struct lpm6cu_fib {
   int device = 0;
   lpm6cu_geometry g{};
-  unsigned long long* d_keys = nullptr;
-  unsigned char* d_values = nullptr;
+  unsigned long long* d_lines = nullptr;
+  unsigned long long root[16] = {};  // host copy of level 0 (launch parameter)
   bool owns = true;
   lpm6cu_kernel_config cfg{};  // resolved
   int num_sms = 0;
@@ -335,10 +369,7 @@ struct lpm6cu_fib {
       }
       if (pipe->start) cudaEventDestroy(pipe->start);
     }
-    if (owns) {
-      if (d_keys) cudaFree(d_keys);
-      if (d_values) cudaFree(d_values);
-    }
+    if (owns && d_lines) cudaFree(d_lines);
     if (prev >= 0) cudaSetDevice(prev);
   }
 };
@@ -366,27 +397,25 @@ namespace {
 void resolve_config(lpm6cu_fib* f, const lpm6cu_kernel_config* req) {
   lpm6cu_kernel_config c{};
   if (req) c = *req;
-  if (c.lanes_per_query == 0) c.lanes_per_query = 8;
-  if (c.lanes_per_query != 4 && c.lanes_per_query != 8 && c.lanes_per_query != 16)
-    throw Error(Errc::InvalidArgument, "lanes_per_query must be 4, 8 or 16");
+  if (c.lanes_per_query == 0) c.lanes_per_query = 4;
+  if (c.lanes_per_query != 4) throw Error(Errc::InvalidArgument, "lanes_per_query must be 4");
   if (c.threads_per_cta == 0) c.threads_per_cta = 256;
   if (c.threads_per_cta != 256) throw Error(Errc::InvalidArgument, "threads_per_cta must be 256");
-  const unsigned levels = f->g.depth + 1;
+  const unsigned depth = f->g.depth;
   const size_t budget = std::min<size_t>(f->max_smem_optin, 200 * 1024);
   if (req == nullptr || req->smem_levels == 0xFF) {
-    // Auto: stage the deepest prefix of levels that fits 48 KiB (keeps >= 4 CTAs/SM).
+    // Auto: the deepest prefix of internal levels that fits 48 KiB (keeps >= 4 CTAs/SM).
     unsigned t = 0;
-    for (unsigned cand = 1; cand <= levels; ++cand) {
-      const unsigned long long bytes = (cand >= levels ? f->g.total_keys : f->g.level_start[cand]) * 8ull;
-      if (bytes > 48 * 1024) break;
+    const unsigned tmax = depth == 0 ? 0u : std::min<unsigned>(depth, std::max<unsigned>(1u, f->g.image_levels));
+    for (unsigned cand = 1; cand <= tmax; ++cand) {
+      if (cand >= 2 && (f->g.level_start[cand] - 16) * 8ull > 48 * 1024) break;
       t = cand;
     }
     c.smem_levels = t;
   }
-  if (c.smem_levels > levels) c.smem_levels = levels;
-  const unsigned long long staged =
-      c.smem_levels == 0 ? 0
-                         : (c.smem_levels >= levels ? f->g.total_keys : f->g.level_start[c.smem_levels]) * 8ull;
+  const unsigned tmax = depth == 0 ? 0u : std::min<unsigned>(depth, std::max<unsigned>(1u, f->g.image_levels));
+  if (c.smem_levels > tmax) c.smem_levels = tmax;  // phase A: internal levels held by the image
+  const unsigned long long staged = c.smem_levels >= 2 ? (f->g.level_start[c.smem_levels] - 16) * 8ull : 0ull;
   if (staged > budget)
     throw Error(Errc::InvalidArgument, "smem_levels=" + std::to_string(c.smem_levels) + " needs " +
                                            std::to_string(staged) + " B of shared memory");
@@ -394,27 +423,24 @@ void resolve_config(lpm6cu_fib* f, const lpm6cu_kernel_config* req) {
 }
 
 unsigned long long staged_bytes(const lpm6cu_fib* f) {
-  const unsigned levels = f->g.depth + 1;
-  const unsigned T = f->cfg.smem_levels;
-  if (T == 0) return 0;
-  return (T >= levels ? f->g.total_keys : f->g.level_start[T]) * 8ull;
+  return f->cfg.smem_levels >= 2 ? (f->g.level_start[f->cfg.smem_levels] - 16) * 8ull : 0ull;
 }
 
 void launch_lookup(const lpm6cu_fib* f, const void* d_addrs, unsigned long long n, void* d_out,
                    cudaStream_t stream) {
   if (n == 0) return;
-  KernelFn fn = pick_kernel(static_cast<int>(f->cfg.lanes_per_query), static_cast<int>(f->g.depth));
+  KernelFn fn = pick_kernel(static_cast<int>(f->g.value_bytes), static_cast<int>(f->g.depth));
   if (!fn) throw Error(Errc::InvalidArgument, "no kernel for depth " + std::to_string(f->g.depth));
   LookupParams p{};
-  p.keys = f->d_keys;
-  p.values = f->d_values;
+  p.lines = f->d_lines;
   for (int l = 0; l < LPM6CU_MAX_LEVELS; ++l) p.level_start[l] = f->g.level_start[l];
   p.addrs = static_cast<const uint4*>(d_addrs);
   p.out = static_cast<unsigned char*>(d_out);
   p.n = n;
   p.smem_bytes = static_cast<unsigned>(staged_bytes(f));
   p.smem_levels = f->cfg.smem_levels;
-  p.value_bytes = f->g.value_bytes;
+  p.image = f->d_lines + f->g.image_start;
+  std::memcpy(p.root, f->root, sizeof p.root);
   const int threads = static_cast<int>(f->cfg.threads_per_cta);
   const size_t smem = p.smem_bytes;
   if (smem > 48 * 1024)
@@ -434,7 +460,8 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_addrs, unsigned long long 
 
 lpm6cu_fib* new_fib(int device, const lpm6cu_geometry* g) {
   if (!g) throw Error(Errc::InvalidArgument, "geometry is NULL");
-  if (g->k != kK) throw Error(Errc::InvalidArgument, "the kernels take k = 16");
+  if (g->k != kNodeKeys || g->b != kNodeKeys + 1) throw Error(Errc::InvalidArgument, "the kernels take k = 16");
+  if (g->leaf_keys != leaf_keys_for(g->value_bytes)) throw Error(Errc::InvalidArgument, "leaf_keys mismatch");
   if (g->depth > kMaxKernelDepth) throw Error(Errc::InvalidArgument, "tree depth above 7");
   if (g->value_bytes != 1 && g->value_bytes != 2 && g->value_bytes != 4)
     throw Error(Errc::InvalidArgument, "value_bytes must be 1, 2 or 4");
@@ -495,31 +522,29 @@ void lookup_host(lpm6cu_fib* f, const void* addrs, unsigned long long n, void* o
 
 extern "C" {
 
-int lpm6cu_fib_create(int device, const lpm6cu_geometry* g, const uint64_t* keys, const void* values,
-                      lpm6cu_fib** out) {
+int lpm6cu_fib_create(int device, const lpm6cu_geometry* g, const uint64_t* lines, lpm6cu_fib** out) {
   return guard([&] {
-    if (!keys || !values || !out) throw Error(Errc::InvalidArgument, "NULL argument");
+    if (!lines || !out) throw Error(Errc::InvalidArgument, "NULL argument");
     DeviceGuard dg(device);
     std::unique_ptr<lpm6cu_fib> f(new_fib(device, g));
-    const size_t kbytes = g->total_keys * 8;
-    const size_t vbytes = g->leaf_nodes * kK * g->value_bytes;
-    check_cuda(cudaMalloc(&f->d_keys, kbytes), "cudaMalloc keys");
-    check_cuda(cudaMalloc(&f->d_values, vbytes), "cudaMalloc values");
-    check_cuda(cudaMemcpy(f->d_keys, keys, kbytes, cudaMemcpyHostToDevice), "copy keys");
-    check_cuda(cudaMemcpy(f->d_values, values, vbytes, cudaMemcpyHostToDevice), "copy values");
+    const size_t bytes = g->total_words * 8;
+    check_cuda(cudaMalloc(&f->d_lines, bytes), "cudaMalloc lines");
+    check_cuda(cudaMemcpy(f->d_lines, lines, bytes, cudaMemcpyHostToDevice), "copy lines");
+    std::memcpy(f->root, lines, sizeof f->root);
     *out = f.release();
   });
 }
 
-int lpm6cu_fib_wrap_device(int device, const lpm6cu_geometry* g, const void* d_keys, const void* d_values,
-                           lpm6cu_fib** out) {
+int lpm6cu_fib_wrap_device(int device, const lpm6cu_geometry* g, const void* d_lines, lpm6cu_fib** out) {
   return guard([&] {
-    if (!d_keys || !d_values || !out) throw Error(Errc::InvalidArgument, "NULL argument");
+    if (!d_lines || !out) throw Error(Errc::InvalidArgument, "NULL argument");
+    if (reinterpret_cast<uintptr_t>(d_lines) % 128 != 0)
+      throw Error(Errc::InvalidArgument, "device lines must be 128-byte aligned");
     DeviceGuard dg(device);
     std::unique_ptr<lpm6cu_fib> f(new_fib(device, g));
-    f->d_keys = static_cast<unsigned long long*>(const_cast<void*>(d_keys));
-    f->d_values = static_cast<unsigned char*>(const_cast<void*>(d_values));
+    f->d_lines = static_cast<unsigned long long*>(const_cast<void*>(d_lines));
     f->owns = false;
+    check_cuda(cudaMemcpy(f->root, d_lines, sizeof f->root, cudaMemcpyDeviceToHost), "copy root");
     *out = f.release();
   });
 }
@@ -533,10 +558,9 @@ int lpm6cu_fib_build(int device, const lpm6cu_prefix* rules, uint64_t n, uint32_
     capi::export_geometry(t.g, &g);
     DeviceGuard dg(device);
     std::unique_ptr<lpm6cu_fib> f(new_fib(device, &g));
-    check_cuda(cudaMalloc(&f->d_keys, t.keys.size() * 8), "cudaMalloc keys");
-    check_cuda(cudaMalloc(&f->d_values, t.values.size()), "cudaMalloc values");
-    check_cuda(cudaMemcpy(f->d_keys, t.keys.data(), t.keys.size() * 8, cudaMemcpyHostToDevice), "copy keys");
-    check_cuda(cudaMemcpy(f->d_values, t.values.data(), t.values.size(), cudaMemcpyHostToDevice), "copy values");
+    check_cuda(cudaMalloc(&f->d_lines, t.lines.size() * 8), "cudaMalloc lines");
+    check_cuda(cudaMemcpy(f->d_lines, t.lines.data(), t.lines.size() * 8, cudaMemcpyHostToDevice), "copy lines");
+    std::memcpy(f->root, t.lines.data(), sizeof f->root);
     *out = f.release();
   });
 }
@@ -548,11 +572,10 @@ int lpm6cu_fib_geometry(const lpm6cu_fib* f, lpm6cu_geometry* g) {
   });
 }
 
-int lpm6cu_fib_device_arrays(const lpm6cu_fib* f, const void** k, const void** v) {
+int lpm6cu_fib_device_lines(const lpm6cu_fib* f, const void** d_lines) {
   return guard([&] {
-    if (!f) throw Error(Errc::InvalidArgument, "NULL fib");
-    if (k) *k = f->d_keys;
-    if (v) *v = f->d_values;
+    if (!f || !d_lines) throw Error(Errc::InvalidArgument, "NULL argument");
+    *d_lines = f->d_lines;
   });
 }
 

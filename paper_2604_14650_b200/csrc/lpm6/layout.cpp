@@ -4,39 +4,40 @@
 
 namespace lpm6 {
 
-TreeLayout plan_layout(u64 m, u32 k) {
+TreeLayout plan_layout(u64 m, u32 value_bytes) {
   if (m < 1) throw Error(Errc::InvalidArgument, "a tree needs at least one boundary");
-  if (k < 2) throw Error(Errc::InvalidArgument, "k must be >= 2");
+  if (value_bytes != 1 && value_bytes != 2 && value_bytes != 4)
+    throw Error(Errc::InvalidArgument, "value_bytes must be 1, 2 or 4");
   TreeLayout g;
-  g.k = k;
-  g.b = k + 1;
+  g.value_bytes = value_bytes;
+  g.leaf_keys = leaf_keys_for(value_bytes);
   g.num_keys = m;
-  // Minimal depth with k * b^depth >= m.
   u32 d = 0;
-  for (unsigned __int128 cap = k; cap < m; cap *= g.b) ++d;
+  for (unsigned __int128 cap = g.leaf_keys; cap < m; cap *= g.b) ++d;
   if (d + 1 > static_cast<u32>(kMaxLevels))
     throw Error(Errc::InvalidArgument, "tree deeper than supported (" + std::to_string(d) + ")");
   g.depth = d;
-  g.leaf_nodes = (m + k - 1) / k;
+  g.leaf_nodes = (m + g.leaf_keys - 1) / g.leaf_keys;
   g.level_nodes[d] = g.leaf_nodes;
-  for (int l = static_cast<int>(d) - 1; l >= 0; --l)
-    g.level_nodes[l] = (g.level_nodes[l + 1] + g.b - 1) / g.b;
+  for (int l = static_cast<int>(d) - 1; l >= 0; --l) g.level_nodes[l] = (g.level_nodes[l + 1] + g.b - 1) / g.b;
   u64 off = 0;
   for (u32 l = 0; l <= d; ++l) {
     g.level_start[l] = off;
-    off += g.level_nodes[l] * k;
+    off += g.level_nodes[l] * kLineWords;
   }
-  g.total_keys = off;
+  // Image of internal levels [1, S) for the largest S whose image fits the budget.
+  u32 s = d >= 1 ? 1 : 0;
+  while (s + 1 <= d && (g.level_start[s + 1] - kLineWords) * 8 <= kImageMaxBytes) ++s;
+  g.image_levels = s;
+  g.image_start = off;
+  g.total_words = off + (s > 1 ? g.level_start[s] - kLineWords : 0);
   return g;
 }
 
-Tree build_tree(const IntervalMap& map, u32 k, u32 value_bytes) {
+Tree build_tree(const IntervalMap& map, u32 value_bytes) {
   const u64 m = map.size();
-  Tree t;
-  t.g = plan_layout(m, k);
-  t.g.default_next_hop = map.default_next_hop;
-  if (map.boundaries.front() != 0)
-    throw Error(Errc::InvalidArgument, "interval map must start at key 0");
+  if (m < 1) throw Error(Errc::InvalidArgument, "empty interval map");
+  if (map.boundaries.front() != 0) throw Error(Errc::InvalidArgument, "interval map must start at key 0");
   for (u64 b : map.boundaries)
     if (b == kSentinelKey) throw Error(Errc::SentinelCollision, "boundary at the sentinel key");
 
@@ -49,33 +50,52 @@ Tree build_tree(const IntervalMap& map, u32 k, u32 value_bytes) {
   if (value_bytes < need)
     throw Error(Errc::InvalidArgument, "next hop " + std::to_string(max_nh) + " does not fit in " +
                                            std::to_string(value_bytes) + " byte(s)");
-  t.g.value_bytes = value_bytes;
 
+  Tree t;
+  t.g = plan_layout(m, value_bytes);
+  t.g.default_next_hop = map.default_next_hop;
   const TreeLayout& g = t.g;
-  t.keys.assign(g.total_keys, kSentinelKey);
+  const u32 kl = g.leaf_keys;
+  t.lines.assign(g.total_words, kSentinelKey);
   const u64* bnd = map.boundaries.data();
 
-  // Internal level l: separator j of node n = first key of child n*b + j + 1,
-  // i.e. boundary[(n*b + j + 1) * span], span = keys under one child = k*b^(d-l-1).
-  u64 span = k;
+  // Internal levels, deepest first: span = boundaries under one child.
+  u64 span = kl;
   for (int l = static_cast<int>(g.depth) - 1; l >= 0; --l) {
-    u64* lvl = t.keys.data() + g.level_start[l];
+    u64* lvl = t.lines.data() + g.level_start[l];
     for (u64 n = 0; n < g.level_nodes[l]; ++n)
-      for (u32 j = 0; j < k; ++j) {
+      for (u32 j = 0; j < g.k; ++j) {
         const unsigned __int128 idx = (static_cast<unsigned __int128>(n) * g.b + j + 1) * span;
-        lvl[n * k + j] = idx < m ? bnd[static_cast<u64>(idx)] : kSentinelKey;
+        lvl[n * kLineWords + j] = idx < m ? bnd[static_cast<u64>(idx)] : kSentinelKey;
       }
     span *= g.b;
   }
-  // Leaves: the boundaries, then sentinels.
-  std::memcpy(t.keys.data() + g.level_start[g.depth], bnd, m * sizeof(u64));
 
-  // Values parallel to leaf slots; padding replicates the last real value.
-  const u64 slots = g.leaf_nodes * k;
-  t.values.assign(slots * value_bytes, 0);
-  for (u64 s = 0; s < slots; ++s) {
-    const u32 v = map.next_hops[s < m ? s : m - 1];
-    std::memcpy(t.values.data() + s * value_bytes, &v, value_bytes);  // little-endian
+  // Leaf lines: kL keys (sentinel past m), then kL little-endian next hops
+  // (padding replicates the last real value), then zero padding.
+  t.leaf_values.resize(g.leaf_nodes * kl);
+  u64* leaves = t.lines.data() + g.level_start[g.depth];
+  for (u64 n = 0; n < g.leaf_nodes; ++n) {
+    u64* line = leaves + n * kLineWords;
+    unsigned char bytes[128];
+    std::memset(bytes, 0, sizeof bytes);
+    for (u32 j = 0; j < kl; ++j) {
+      const u64 s = n * kl + j;
+      const u64 key = s < m ? bnd[s] : kSentinelKey;
+      const u32 v = map.next_hops[s < m ? s : m - 1];
+      t.leaf_values[s] = v;
+      std::memcpy(bytes + 8 * j, &key, 8);
+      std::memcpy(bytes + 8 * kl + value_bytes * j, &v, value_bytes);
+    }
+    std::memcpy(line, bytes, sizeof bytes);
+  }
+
+  // Shared-memory image: levels [1, image_levels), keys rotated by node index.
+  for (u32 l = 1; l < g.image_levels; ++l) {
+    const u64* src = t.lines.data() + g.level_start[l];
+    u64* dst = t.lines.data() + g.image_start + (g.level_start[l] - kLineWords);
+    for (u64 n = 0; n < g.level_nodes[l]; ++n)
+      for (u32 p = 0; p < kLineWords; ++p) dst[image_slot(n, p)] = src[n * kLineWords + p];
   }
   return t;
 }

@@ -1,19 +1,24 @@
 // B200 layout of the linearized B+-tree.
 //
 // The reference lays the tree out as one dense key array of 64-byte, 8-key
-// nodes — internal levels breadth-first and fully allocated, then the leaves
-// (tree.hpp:14-74). On B200 the node is one 128-byte L2
-// line: k = 16 keys, arity b = 17 (the paper's own rule for 128-byte lines,
-// P:601-604). Two changes from the reference layout, neither of which changes a
-// single lookup result:
-//   * each level holds only its reachable prefix of nodes, ceil(leaves / b^(d-l))
+// nodes — internal levels breadth-first and fully allocated, then the leaves —
+// with next hops in a separate array indexed by leaf slot (tree.hpp:14-74,
+// S:179-223). On B200 every node is one 128-byte L2 line:
+//
+//   * internal nodes hold k = 16 separator keys (arity b = 17, the paper's own
+//     rule for 128-byte lines);
+//   * a leaf line holds kL boundary keys followed by their kL next hops
+//     (kL = 14 for 1-byte, 12 for 2-byte, 8 for 4-byte next hops), so the
+//     final value load of the reference (values[i - leaf_start])
+//     is served by the leaf line the search already fetched;
+//   * each level holds only its reachable prefix of nodes, ceil(leaves/b^(d-l))
 //     (the reference allocates b^l; the extra nodes are all-sentinel and never
-//     visited), so level l starts at level_start[l] in a compact array
-//     and child c of node j at level l is node j*b + c of level l+1;
-//   * values are stored at the narrowest width that holds every next hop (u8 for
-//     C0/C1/C3, u16 for C2/C4) instead of u32.
-// Separators, sentinel padding, the leaf fill and the rank-1 ordinal are the
-// reference's.
+//     visited), and child c of node j is node j*b + c of the next level.
+//
+// Separators, sentinel padding, the query clamp and the rank-1 ordinal are the
+// reference's: separator j of internal node n at
+// level l is the first key of child n*b + j + 1, i.e. boundary[(n*b + j + 1) *
+// span_l] with span_l = kL * b^(d-l-1), or the sentinel past the last boundary.
 #pragma once
 
 #include <cstddef>
@@ -24,19 +29,38 @@
 namespace lpm6 {
 
 inline constexpr int kMaxLevels = 9;  // depth <= 8
+inline constexpr u32 kNodeKeys = 16;  // internal keys per 128-byte line
+inline constexpr u32 kLineWords = 16;  // u64 words per line
+
+// Keys per leaf line for a next-hop width (leaf = kL keys + kL values <= 128 B).
+constexpr u32 leaf_keys_for(u32 value_bytes) { return value_bytes == 1 ? 14 : value_bytes == 2 ? 12 : 8; }
 
 struct TreeLayout {
-  u32 k = 16;
-  u32 b = 17;
-  u32 depth = 0;        // internal levels; a lookup visits depth + 1 nodes
+  u32 k = kNodeKeys;    // internal keys per node
+  u32 b = kNodeKeys + 1;
+  u32 depth = 0;        // internal levels; a lookup visits depth + 1 lines
   u32 value_bytes = 1;  // 1, 2 or 4
+  u32 leaf_keys = 14;   // kL
   u64 num_keys = 0;     // m, real boundaries
-  u64 leaf_nodes = 0;   // ceil(m / k)
+  u64 leaf_nodes = 0;   // ceil(m / kL)
   u64 level_nodes[kMaxLevels] = {};  // reachable nodes per level; level depth = leaves
-  u64 level_start[kMaxLevels] = {};  // key offset of each level in the key array
-  u64 total_keys = 0;
+  u64 level_start[kMaxLevels] = {};  // u64-word offset of each level in the line array
+  u64 total_words = 0;               // tree lines (16 words each), then the smem image
+  // Bank-swizzled copy of levels [1, image_levels) that the kernel stages into
+  // shared memory with one TMA bulk copy: key p of node n of those levels sits at
+  // word n*16 + ((p + n) & 15), so threads probing the same key position of
+  // different nodes hit different shared-memory banks. Level l of the image
+  // starts at image word level_start[l] - 16 (the root is not imaged: the
+  // kernel takes it as a launch parameter).
+  u32 image_levels = 0;
+  u64 image_start = 0;
   u32 default_next_hop = 0;
 };
+
+inline constexpr u64 kImageMaxBytes = 200 * 1024;
+
+// Swizzled position of key p of node n in the shared-memory image.
+constexpr u64 image_slot(u64 n, u32 p) { return n * kLineWords + ((p + n) & 15u); }
 
 template <class T, size_t Align>
 struct AlignedAllocator {
@@ -56,15 +80,15 @@ struct AlignedAllocator {
 
 struct Tree {
   TreeLayout g;
-  std::vector<u64, AlignedAllocator<u64, 128>> keys;  // total_keys
-  std::vector<u8, AlignedAllocator<u8, 128>> values;  // leaf_nodes * k * value_bytes
+  std::vector<u64, AlignedAllocator<u64, 128>> lines;  // total_words: the device image
+  std::vector<u32> leaf_values;                         // next hop per leaf slot (inspection only)
 };
 
-// Minimal depth with k * b^depth >= m and the compact level table.
-TreeLayout plan_layout(u64 m, u32 k = 16);
+// Minimal depth with kL * b^depth >= m and the compact level table.
+TreeLayout plan_layout(u64 m, u32 value_bytes);
 
 // value_bytes = 0 picks the narrowest of {1, 2, 4} holding every next hop;
 // an explicit width that cannot hold one throws InvalidArgument.
-Tree build_tree(const IntervalMap& map, u32 k = 16, u32 value_bytes = 0);
+Tree build_tree(const IntervalMap& map, u32 value_bytes = 0);
 
 }  // namespace lpm6

@@ -19,23 +19,29 @@ void check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw Error(Errc::CudaError, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-// Each group of LPL lanes fetches one random line per iteration, lane j taking
-// 16 or 32 bytes of it: the same access shape as the lookup's node loads.
+// Each group of LINE/32 lanes fetches one random line per iteration, lane j
+// taking one 32-byte sector with a 256-bit load that bypasses L1 — the access
+// shape of the lookup's node loads (4 lanes x 32 B per 128-byte node). The line
+// index is a multiply-high range reduction of an LCG, so the probe is bound by the memory
+// system, not by index arithmetic.
 template <int LINE>
 __global__ void __launch_bounds__(256) l2_gather_kernel(const unsigned long long* buf, unsigned long long lines,
                                                         int iters, unsigned long long* sink) {
-  constexpr int LPL = LINE / 16;  // lanes per line, 16 B each
-  const unsigned lane = threadIdx.x & 31u;
+  constexpr int LPL = LINE / 32;  // lanes per line
   const unsigned grp = (blockIdx.x * blockDim.x + threadIdx.x) / LPL;
-  const unsigned j = lane % LPL;
+  const unsigned j = threadIdx.x % LPL;
   unsigned long long acc = 0;
+  unsigned long long h = mix64(grp);
 #pragma unroll 8
   for (int it = 0; it < iters; ++it) {
-    const unsigned long long line = mix64((static_cast<unsigned long long>(grp) << 20) ^ it) % lines;
-    const unsigned long long* p = buf + line * (LINE / 8) + j * 2;
-    unsigned long long a, b;
-    asm volatile("ld.global.nc.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
-    acc ^= a + b;
+    h = h * 6364136223846793005ull + 1442695040888963407ull;  // LCG per group: uniform across its lanes
+    const unsigned long long line = __umul64hi(h, lines);  // uniform in [0, lines)
+    const unsigned long long* p = buf + line * (LINE / 8) + j * 4;
+    unsigned long long a, b, c, d;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+                 : "l"(p));
+    acc ^= a + b + c + d;
   }
   if (acc == 0x123456789ull) sink[0] = acc;
 }
@@ -102,7 +108,7 @@ int lpm6cu_probe_l2_gather(int device, uint64_t buffer_bytes, uint32_t line_byte
       ms = time_ms([&] { l2_gather_kernel<128><<<blocks, 256>>>(buf, lines, iters, sink); });
     else
       ms = time_ms([&] { l2_gather_kernel<32><<<blocks, 256>>>(buf, lines, iters, sink); });
-    const double groups = static_cast<double>(blocks) * 256 / (line_bytes / 16);
+    const double groups = static_cast<double>(blocks) * 256 / (line_bytes / 32);
     *gbps = groups * iters * line_bytes / (ms * 1e-3) / 1e9;
     cudaFree(buf);
     cudaFree(sink);

@@ -158,58 +158,70 @@ class Geometry:
     b: int
     depth: int
     value_bytes: int
+    leaf_keys: int
+    image_levels: int
     num_keys: int
     leaf_nodes: int
-    total_keys: int
+    total_words: int
+    image_start: int
     level_nodes: list[int]
     level_start: list[int]
     default_next_hop: int
 
     @classmethod
     def from_c(cls, g: Geometry_t) -> "Geometry":
-        return cls(g.k, g.b, g.depth, g.value_bytes, g.num_keys, g.leaf_nodes, g.total_keys,
-                   list(g.level_nodes), list(g.level_start), g.default_next_hop)
+        return cls(g.k, g.b, g.depth, g.value_bytes, g.leaf_keys, g.image_levels, g.num_keys, g.leaf_nodes,
+                   g.total_words, g.image_start, list(g.level_nodes), list(g.level_start), g.default_next_hop)
 
     def to_c(self) -> Geometry_t:
         g = Geometry_t()
-        g.k, g.b, g.depth, g.value_bytes = self.k, self.b, self.depth, self.value_bytes
-        g.num_keys, g.leaf_nodes, g.total_keys = self.num_keys, self.leaf_nodes, self.total_keys
+        g.k, g.b, g.depth, g.value_bytes, g.leaf_keys = self.k, self.b, self.depth, self.value_bytes, self.leaf_keys
+        g.image_levels, g.image_start = self.image_levels, self.image_start
+        g.num_keys, g.leaf_nodes, g.total_words = self.num_keys, self.leaf_nodes, self.total_words
         for i in range(len(self.level_nodes)):
             g.level_nodes[i] = self.level_nodes[i]
             g.level_start[i] = self.level_start[i]
         g.default_next_hop = self.default_next_hop
         return g
 
+    @property
+    def tree_bytes(self) -> int:
+        return self.total_words * 8
 
-def plan_layout(m: int, k: int = 16) -> Geometry:
+
+def plan_layout(m: int, value_bytes: int = 1) -> Geometry:
     g = Geometry_t()
-    check(lib().lpm6_plan_layout(m, k, C.byref(g)))
+    check(lib().lpm6_plan_layout(m, value_bytes, C.byref(g)))
     return Geometry.from_c(g)
 
 
 @dataclass
 class Tree:
-    """Host copy of the B200 layout: compact levels of k-key nodes + leaf-aligned values."""
+    """Host copy of the B200 layout: 128-byte lines (internal: 16 separators; leaf:
+    leaf_keys keys + their next hops) and the next hop of every leaf slot."""
     geometry: Geometry
-    keys: np.ndarray    # uint64[total_keys]
-    values: np.ndarray  # uint8/uint16/uint32[leaf_nodes * k]
+    lines: np.ndarray        # uint64[total_words]
+    leaf_values: np.ndarray  # uint32[leaf_nodes * leaf_keys]
+
+    def leaf_keys_array(self) -> np.ndarray:
+        """The leaf boundary keys in slot order (sentinels past m)."""
+        g = self.geometry
+        leaves = self.lines[g.level_start[g.depth]:].reshape(-1, 16)
+        return leaves[:, : g.leaf_keys].reshape(-1)
 
 
-_VDT = {1: np.uint8, 2: np.uint16, 4: np.uint32}
-
-
-def build_tree(imap: IntervalMap, k: int = 16, value_bytes: int = 0) -> Tree:
+def build_tree(imap: IntervalMap, value_bytes: int = 0) -> Tree:
     """Lay out the linearized tree for B200 (csrc/lpm6/layout.cpp; contract S:215-223)."""
     g = Geometry_t()
     b = np.ascontiguousarray(imap.boundaries, np.uint64)
     nh = np.ascontiguousarray(imap.next_hops, np.uint32)
-    check(lib().lpm6_build_tree(b.ctypes.data, nh.ctypes.data, len(b), imap.default_next_hop, k, value_bytes,
+    check(lib().lpm6_build_tree(b.ctypes.data, nh.ctypes.data, len(b), imap.default_next_hop, value_bytes,
                                 C.byref(g), None, None))
-    keys = np.empty(g.total_keys, np.uint64)
-    values = np.empty(g.leaf_nodes * g.k, _VDT[g.value_bytes])
-    check(lib().lpm6_build_tree(b.ctypes.data, nh.ctypes.data, len(b), imap.default_next_hop, k, value_bytes,
-                                C.byref(g), keys.ctypes.data, values.ctypes.data))
-    return Tree(Geometry.from_c(g), keys, values)
+    lines = np.empty(g.total_words, np.uint64)
+    vals = np.empty(g.leaf_nodes * g.leaf_keys, np.uint32)
+    check(lib().lpm6_build_tree(b.ctypes.data, nh.ctypes.data, len(b), imap.default_next_hop, value_bytes,
+                                C.byref(g), lines.ctypes.data, vals.ctypes.data))
+    return Tree(Geometry.from_c(g), lines, vals)
 
 
 # ---- synthetic workloads (BASELINE.json configs) ---------------------------------
@@ -263,5 +275,4 @@ def build_opts(merge_adjacent: bool = True, value_bytes: int = 0) -> BuildOpts_t
     o = BuildOpts_t()
     o.merge_adjacent = int(merge_adjacent)
     o.value_bytes = value_bytes
-    o.k = 16
     return o

@@ -68,17 +68,17 @@ class Fib:
     def from_tree(cls, tree: Tree, device: int = 0) -> "Fib":
         h = C.c_void_p()
         g = tree.geometry.to_c()
-        check(lib().lpm6cu_fib_create(device, C.byref(g), tree.keys.ctypes.data, tree.values.ctypes.data,
-                                      C.byref(h)))
+        lines = np.ascontiguousarray(tree.lines, np.uint64)
+        check(lib().lpm6cu_fib_create(device, C.byref(g), lines.ctypes.data, C.byref(h)))
         return cls(h.value, device)
 
     @classmethod
-    def wrap_device(cls, geometry: Geometry, keys, values, device: int) -> "Fib":
-        """Over device tensors the caller owns (e.g. filled by an NCCL broadcast)."""
+    def wrap_device(cls, geometry: Geometry, lines, device: int) -> "Fib":
+        """Over a device tensor the caller owns (e.g. filled by an NCCL broadcast)."""
         h = C.c_void_p()
         g = geometry.to_c()
-        check(lib().lpm6cu_fib_wrap_device(device, C.byref(g), keys.data_ptr(), values.data_ptr(), C.byref(h)))
-        return cls(h.value, device, keepalive=(keys, values))
+        check(lib().lpm6cu_fib_wrap_device(device, C.byref(g), lines.data_ptr(), C.byref(h)))
+        return cls(h.value, device, keepalive=lines)
 
     def close(self) -> None:
         if self._h and self._h.value:
@@ -98,10 +98,10 @@ class Fib:
         check(lib().lpm6cu_fib_geometry(self._h, C.byref(g)))
         return Geometry.from_c(g)
 
-    def device_arrays(self) -> tuple[int, int]:
-        k, v = C.c_void_p(), C.c_void_p()
-        check(lib().lpm6cu_fib_device_arrays(self._h, C.byref(k), C.byref(v)))
-        return k.value, v.value
+    def device_lines(self) -> int:
+        p = C.c_void_p()
+        check(lib().lpm6cu_fib_device_lines(self._h, C.byref(p)))
+        return p.value
 
     def kernel_config(self) -> dict:
         c = KernelConfig_t()
