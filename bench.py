@@ -272,7 +272,6 @@ def main():
     torch.cuda.set_device(local)
     dev_index = local
     import paper_2604_14650_b200 as lpm
-    from paper_2604_14650_b200.fib import Geometry
 
     info = lpm.workload_info(args.workload)
     fib = lpm.workload_fib(info.fib_kind)
@@ -280,33 +279,19 @@ def main():
     vb = info.value_bytes
 
     # -- FIB: host build on rank 0, NCCL broadcast to the others -----------------------------
+    from paper_2604_14650_b200 import dispatch
     t0 = time.perf_counter()
-    if rank == 0:
-        imap = lpm.build_intervals(fib)
-        tree = lpm.build_tree(imap, vb)
-        geom = tree.geometry
+    tree = dispatch.build_on_root(fib, rank, vb)
     build_ms = (time.perf_counter() - t0) * 1e3
     if dist is not None:
-        obj = [geom if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        geom = obj[0]
-        lines_t = torch.empty(geom.total_words, dtype=torch.int64, device="cuda")
-        if rank == 0:
-            lines_t.copy_(torch.from_numpy(tree.lines.view(np.int64)))
         dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        dist.broadcast(lines_t, 0)
-        e1.record()
-        torch.cuda.synchronize()
-        bcast_ms = e0.elapsed_time(e1)
-        t = torch.tensor([bcast_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        bcast_ms = float(t.item())
-        fdev = lpm.Fib.wrap_device(geom, lines_t, dev_index)
-    else:
-        fdev = lpm.Fib.from_tree(tree, dev_index)
-        bcast_ms = 0.0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    geom, lines_t = dispatch.replicate_tree(tree, dist, torch.device("cuda", dev_index))
+    e1.record()
+    torch.cuda.synchronize()
+    bcast_ms = dispatch.max_over_ranks(e0.elapsed_time(e1), dist, "cuda") if dist is not None else 0.0
+    fdev = lpm.Fib.wrap_device(geom, lines_t, dev_index)
     cfg = fdev.set_kernel_config(lanes_per_query=args.lanes, smem_levels=args.smem_levels,
                                  ctas_per_sm=args.ctas_per_sm)
 
@@ -314,7 +299,8 @@ def main():
     addrs = torch.empty((n, 16), dtype=torch.uint8, device="cuda")
     out = torch.empty(n * vb, dtype=torch.uint8, device="cuda")
     gen = lpm.QueryGen(args.workload, fib, dev_index)
-    gen.run(rank * n, n, addrs)
+    first, _ = dispatch.shard(rank, ws, n)
+    gen.run(first, n, addrs)
     torch.cuda.synchronize()
 
     # -- roofline denominators measured on this device --------------------------------------------
@@ -344,11 +330,7 @@ def main():
     if dist is not None:
         dist.barrier()
     step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
-    total_ms = sum(step_ms)
-    if dist is not None:
-        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = dispatch.max_over_ranks(sum(step_ms), dist, "cuda")
     ms_per_step = total_ms / args.steps
     value = ws * n * args.steps / (total_ms * 1e-3) / 1e9  # aggregate G lookups/s
     lps_gpu = n / (ms_per_step * 1e-3)
@@ -384,11 +366,7 @@ def main():
             fdev.lookup_batch(ha_np, ho_np)
         s1.record(stream)
         torch.cuda.synchronize()
-        e2e_ms = s0.elapsed_time(s1)
-        if dist is not None:
-            t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+        e2e_ms = dispatch.max_over_ranks(s0.elapsed_time(s1), dist, "cuda")
         e2e = {"value": ws * n * k_e2e / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": n * 16,
                "d2h_bytes_per_step": n * vb, "steps": k_e2e,
                "path": "lpm6cu_lookup_batch(host pinned buffers): 8M-address chunks, H2D/kernel/D2H on 3 streams"}

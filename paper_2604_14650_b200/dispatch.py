@@ -1,0 +1,65 @@
+"""Multi-GPU dispatcher: replicate the FIB, partition query batches, reduce timings.
+
+Lookups shard by query batch with no inter-GPU traffic: rank 0
+builds the FIB on the host once, the 128-byte-line tree is broadcast to every
+rank with one collective (NCCL over NVLink on GPUs; gloo in the CPU tests), and
+each rank resolves its own contiguous slice of the query stream. The only other
+collectives are the max-over-ranks reductions of device timings.
+"""
+from __future__ import annotations
+
+from dataclasses import asdict
+
+import numpy as np
+
+from .fib import FibTable, Geometry, build_intervals, build_tree
+
+
+def build_on_root(fib: FibTable, rank: int, value_bytes: int = 0):
+    """Rank 0: FIB -> intervals -> B200 layout on the host. Other ranks: None."""
+    if rank != 0:
+        return None
+    return build_tree(build_intervals(fib), value_bytes)
+
+
+def replicate_tree(tree, dist, device, group=None):
+    """Broadcast the layout from rank 0: geometry as an object, lines as one tensor.
+
+    Returns (Geometry, lines tensor on `device`). With dist None (one rank) the
+    tensor is made from the local tree.
+    """
+    import torch
+    if dist is None:
+        return tree.geometry, torch.from_numpy(tree.lines.view(np.int64)).to(device)
+    rank = dist.get_rank(group)
+    obj = [asdict(tree.geometry) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    geom = Geometry(**obj[0])
+    lines = torch.empty(geom.total_words, dtype=torch.int64, device=device)
+    if rank == 0:
+        lines.copy_(torch.from_numpy(tree.lines.view(np.int64)))
+    dist.broadcast(lines, 0, group=group)
+    return geom, lines
+
+
+def shard(rank: int, world: int, per_rank: int, total: int | None = None) -> tuple[int, int]:
+    """[first, count) of this rank's queries.
+
+    Weak scaling (total None): every rank gets `per_rank` queries, rank r the r-th
+    block. Strong scaling: `total` queries split into near-equal contiguous blocks.
+    """
+    if total is None:
+        return rank * per_rank, per_rank
+    base, extra = divmod(total, world)
+    first = rank * base + min(rank, extra)
+    return first, base + (1 if rank < extra else 0)
+
+
+def max_over_ranks(value: float, dist, device=None) -> float:
+    """Device time of a multi-rank step = the slowest rank's."""
+    if dist is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())

@@ -206,7 +206,8 @@ class Tree:
     def leaf_keys_array(self) -> np.ndarray:
         """The leaf boundary keys in slot order (sentinels past m)."""
         g = self.geometry
-        leaves = self.lines[g.level_start[g.depth]:].reshape(-1, 16)
+        start = g.level_start[g.depth]
+        leaves = self.lines[start: start + g.leaf_nodes * 16].reshape(-1, 16)
         return leaves[:, : g.leaf_keys].reshape(-1)
 
 

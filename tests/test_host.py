@@ -1,0 +1,219 @@
+"""Host-side tests (no GPU): the C ABI library, the B200 layout, the workloads.
+
+The layout is checked by walking it in numpy exactly as the kernel does (test
+code only — the product has no CPU lookup) and comparing with the oracle.
+"""
+import ctypes as C
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from _util import MASK64, addrs_from_keys, boundary_probe_keys, random_fib_rules
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+# ---- the C ABI library -----------------------------------------------------------------------
+
+def header_functions():
+    text = (ROOT / "include" / "lpm6cu.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(lpm6(?:cu)?_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol(lpm):
+    from paper_2604_14650_b200._lib import LIB_PATH, SIGNATURES
+    names = header_functions()
+    assert len(names) == len(SIGNATURES) == 24
+    dll = C.CDLL(str(LIB_PATH))
+    for name in names:
+        assert hasattr(dll, name), f"{name} declared in include/lpm6cu.h but not exported"
+        assert name in SIGNATURES, f"{name} has no ctypes binding"
+
+
+def test_status_names_match_reference_errc(lpm):
+    from paper_2604_14650_b200._lib import ERRC_NAMES, lib
+    for i, name in enumerate(ERRC_NAMES, 1):
+        assert lib().lpm6cu_status_name(i).decode() == name
+    assert b"sm_100a" in lib().lpm6cu_version()
+
+
+def test_no_cpu_fallback_without_gpu(lpm):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    fib = lpm.workload_fib(0)
+    with pytest.raises(lpm.Lpm6Error) as e:
+        lpm.Fib.build(fib)
+    assert e.value.code == "CudaError"
+
+
+# ---- the B200 layout --------------------------------------------------------------------------
+
+def walk_layout(tree, keys):
+    """Numpy restatement of the kernel's descent over the B200 layout (test-only)."""
+    g = tree.geometry
+    lines = tree.lines
+    q = np.minimum(np.asarray(keys, np.uint64), np.uint64(MASK64 - 1))
+    node = np.zeros(len(q), np.int64)
+    for lvl in range(g.depth):
+        base = g.level_start[lvl] + node * 16
+        nd = lines[base[:, None] + np.arange(16)]
+        node = node * 17 + (nd <= q[:, None]).sum(axis=1)
+    base = g.level_start[g.depth] + node * 16
+    lf = lines[base[:, None] + np.arange(g.leaf_keys)]
+    ordinal = (lf <= q[:, None]).sum(axis=1) - 1
+    assert np.all(ordinal >= 0)
+    return tree.leaf_values[node * g.leaf_keys + ordinal]
+
+
+def check_layout(lpm, orc, fib, n_random=20000, seed=0):
+    imap = lpm.build_intervals(fib)
+    tree = lpm.build_tree(imap)
+    g = tree.geometry
+    m = len(imap)
+    # geometry: minimal depth, compact reachable levels
+    assert g.leaf_keys * 17 ** g.depth >= m and (g.depth == 0 or g.leaf_keys * 17 ** (g.depth - 1) < m)
+    assert g.leaf_nodes == -(-m // g.leaf_keys)
+    for lvl in range(g.depth):
+        assert g.level_nodes[lvl] == -(-g.level_nodes[lvl + 1] // 17)
+    assert g.level_nodes[0] == 1
+    # leaves: boundaries then sentinels; values replicate the last one
+    lk = tree.leaf_keys_array()
+    np.testing.assert_array_equal(lk[:m], imap.boundaries)
+    assert np.all(lk[m:] == np.uint64(MASK64))
+    np.testing.assert_array_equal(tree.leaf_values[:m], imap.next_hops)
+    assert np.all(tree.leaf_values[m:] == imap.next_hops[-1])
+    # internal separators = boundary[(n*17 + j + 1) * span]
+    span = g.leaf_keys
+    for lvl in range(g.depth - 1, -1, -1):
+        nodes = g.level_nodes[lvl]
+        idx = (np.arange(nodes)[:, None] * 17 + np.arange(16)[None, :] + 1) * span
+        want = np.where(idx < m, imap.boundaries[np.minimum(idx, m - 1)], np.uint64(MASK64))
+        got = tree.lines[g.level_start[lvl]: g.level_start[lvl] + nodes * 16].reshape(nodes, 16)
+        np.testing.assert_array_equal(got, want)
+        span *= 17
+    # the shared-memory image is the swizzled copy of levels 1..image_levels-1
+    for lvl in range(1, g.image_levels):
+        nodes = g.level_nodes[lvl]
+        src = tree.lines[g.level_start[lvl]: g.level_start[lvl] + nodes * 16].reshape(nodes, 16)
+        off = g.image_start + g.level_start[lvl] - 16
+        img = tree.lines[off: off + nodes * 16].reshape(nodes, 16)
+        rot = (np.arange(16)[None, :] + np.arange(nodes)[:, None]) % 16
+        np.testing.assert_array_equal(np.take_along_axis(img, rot, axis=1), src)
+    # the descent the kernel performs gives the oracle's answer
+    rng = np.random.default_rng(seed)
+    keys = np.concatenate([boundary_probe_keys(imap.boundaries), rng.integers(0, 2**64, n_random, dtype=np.uint64)])
+    want, _ = orc.lookup_batch(0, imap.boundaries, imap.next_hops, addrs_from_keys(keys), threads=8)
+    np.testing.assert_array_equal(walk_layout(tree, keys), want)
+    return tree
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_layout_workload_fibs(lpm, orc, kind):
+    tree = check_layout(lpm, orc, lpm.workload_fib(kind))
+    assert tree.geometry.depth == {0: 2, 1: 4}[kind]
+
+
+@pytest.mark.parametrize("n,dflt", [(0, False), (1, True), (13, False), (14, True), (300, False), (5000, True)])
+def test_layout_random_fibs(lpm, orc, n, dflt):
+    from paper_2604_14650_b200.fib import PREFIX_DTYPE
+    rng = np.random.default_rng(n)
+    rules = random_fib_rules(rng, n, PREFIX_DTYPE, dflt, nest_p=0.4)
+    rules["next_hop"] = rng.integers(1, 250, len(rules))
+    check_layout(lpm, orc, lpm.FibTable(int(rng.integers(0, 9)), rules))
+
+
+@pytest.mark.parametrize("vb,kl", [(1, 14), (2, 12), (4, 8)])
+def test_layout_value_widths(lpm, vb, kl):
+    b = np.arange(1000, dtype=np.uint64) * 977
+    nh = (np.arange(1000) % 200 + 1).astype(np.uint32)
+    imap = lpm.IntervalMap(b, nh, 0)
+    t = lpm.build_tree(imap, vb)
+    g = t.geometry
+    assert g.value_bytes == vb and g.leaf_keys == kl
+    leaves = t.lines[g.level_start[g.depth]: g.level_start[g.depth] + g.leaf_nodes * 16].reshape(-1, 16)
+    raw = leaves.view(np.uint8).reshape(-1, 128)[:, kl * 8: kl * 8 + kl * vb]
+    vals = raw.copy().view({1: np.uint8, 2: np.uint16, 4: np.uint32}[vb]).reshape(-1)
+    np.testing.assert_array_equal(vals[:1000], nh)
+
+
+def test_layout_value_width_errors(lpm):
+    imap = lpm.IntervalMap(np.array([0, 5], np.uint64), np.array([1, 300], np.uint32), 0)
+    assert lpm.build_tree(imap).geometry.value_bytes == 2
+    with pytest.raises(lpm.Lpm6Error) as e:
+        lpm.build_tree(imap, 1)
+    assert e.value.code == "InvalidArgument"
+    with pytest.raises(lpm.Lpm6Error):
+        lpm.build_tree(imap, 3)
+
+
+def test_plan_layout_depths(lpm):
+    for m, d in ((1, 0), (14, 0), (15, 1), (14 * 17, 1), (14 * 17 + 1, 2), (387232, 4)):
+        assert lpm.plan_layout(m, 1).depth == d
+    assert lpm.plan_layout(1893858, 2).depth == 5
+    g = lpm.plan_layout(12 * 17 ** 6 + 1, 2)
+    assert g.depth == 7
+
+
+# ---- workloads ---------------------------------------------------------------------------------
+
+def test_workload_fibs_match_baseline_configs(lpm):
+    f0, f1 = lpm.workload_fib(0), lpm.workload_fib(1)
+    assert len(f0) == 1001 and len(f1) == 200001          # + ::/0
+    for f in (f0, f1):
+        r = f.rules
+        assert np.sum(r["length"] == 0) == 1
+        assert r["next_hop"].min() >= 1 and r["next_hop"].max() <= 255
+    r = f0.rules[f0.rules["length"] > 0]
+    assert r["length"].min() >= 16 and r["length"].max() <= 64
+    r = f1.rules[f1.rules["length"] > 0]
+    agg = r[r["length"] <= 24]
+    assert len(agg) >= 2000
+    assert np.all((agg["value_hi"] >> np.uint64(61)) == 1)  # 2000::/3
+    share48 = np.mean(r["length"] == 48)
+    assert 0.40 < share48 < 0.48
+
+
+def test_workload_c2_fib(lpm):
+    f2 = lpm.workload_fib(2)
+    r = f2.rules
+    assert len(f2) == 1_000_000 and np.sum(r["length"] == 0) == 0
+    assert r["next_hop"].max() > 255 and r["next_hop"].max() <= 65535
+    assert lpm.build_tree(lpm.build_intervals(f2)).geometry.depth == 5
+
+
+def test_query_generator(lpm):
+    fib = lpm.workload_fib(1)
+    a = lpm.workload_queries_host("C1", fib, 0, 200000)
+    b = lpm.workload_queries_host("C1", fib, 100000, 100000)
+    np.testing.assert_array_equal(a[100000:], b)          # counter-based: any slice regenerates exactly
+    hi = a[:, 1]
+    in2000 = (hi >> np.uint64(61)) == 1
+    assert in2000.mean() > 0.95                              # 90% in-prefix (FIB is in 2000::/3) + 10% in 2000::/3
+    u = lpm.workload_queries_host("C3a", fib, 0, 100000)
+    assert 0.08 < ((u[:, 1] >> np.uint64(61)) == 1).mean() < 0.17   # uniform over 128 bits
+    z = lpm.workload_queries_host("C3b", fib, 0, 100000)
+    _, counts = np.unique(z[:, 1] >> np.uint64(16), return_counts=True)
+    assert counts.max() > 1000                               # Zipf(1.1): heavy head
+
+
+def test_ref_oracle_fixture_generator_is_reproducible(ref):
+    """The golden fixtures regenerate bit-identically from the reference."""
+    import subprocess
+    import sys
+    import tempfile
+    src = ROOT / "tests" / "golden" / "make_golden.py"
+    with tempfile.TemporaryDirectory() as d:
+        code = src.read_text().replace('HERE = Path(__file__).resolve().parent', f'HERE = Path({str(src.parent)!r})')
+        code = code.replace('np.savez_compressed(HERE / f"{name}.npz", **out)',
+                            f'np.savez_compressed(Path({d!r}) / f"{{name}}.npz", **out)')
+        p = Path(d) / "gen.py"
+        p.write_text(code)
+        subprocess.run([sys.executable, str(p)], check=True, capture_output=True)
+        for f in (ROOT / "tests" / "golden").glob("*.npz"):
+            a, b = np.load(f), np.load(Path(d) / f.name)
+            for k in a.files:
+                np.testing.assert_array_equal(a[k], b[k])
