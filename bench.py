@@ -45,6 +45,8 @@ def parse_args():
     ap.add_argument("--lanes", type=int, default=0, help="lanes per query (4/8/16), 0 = auto")
     ap.add_argument("--smem-levels", type=int, default=None, help="levels staged in smem, default auto")
     ap.add_argument("--ctas-per-sm", type=int, default=0)
+    ap.add_argument("--queries-per-lane", type=int, default=0, help="32-query tiles per warp iteration (1/2)")
+    ap.add_argument("--min-ctas", type=int, default=0, help="register cap: min CTAs/SM launch bound")
     ap.add_argument("--queries", type=int, default=0, help="override queries per GPU (testing only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -293,7 +295,8 @@ def main():
     bcast_ms = dispatch.max_over_ranks(e0.elapsed_time(e1), dist, "cuda") if dist is not None else 0.0
     fdev = lpm.Fib.wrap_device(geom, lines_t, dev_index)
     cfg = fdev.set_kernel_config(lanes_per_query=args.lanes, smem_levels=args.smem_levels,
-                                 ctas_per_sm=args.ctas_per_sm)
+                                 ctas_per_sm=args.ctas_per_sm, queries_per_lane=args.queries_per_lane,
+                                 min_ctas_per_sm=args.min_ctas)
 
     # -- queries: this rank's slice, generated on the device ------------------------------------
     addrs = torch.empty((n, 16), dtype=torch.uint8, device="cuda")
@@ -378,10 +381,11 @@ def main():
     sweep = None
     if args.sweep and rank == 0:
         sweep = []
-        for g in (4,):
-            for t_lv in range(0, geom.depth + 1):
+        shapes = [(1, 0), (1, 4), (1, 5), (1, 6), (2, 0), (2, 3), (2, 4)]
+        for t_lv in range(max(0, geom.depth - 2), geom.depth + 1):
+            for qpl, minb in shapes:
                 try:
-                    fdev.set_kernel_config(lanes_per_query=g, smem_levels=t_lv)
+                    fdev.set_kernel_config(smem_levels=t_lv, queries_per_lane=qpl, min_ctas_per_sm=minb)
                 except Exception:
                     continue
                 for _ in range(2):
@@ -393,9 +397,11 @@ def main():
                 a1.record(stream)
                 torch.cuda.synchronize()
                 ms = a0.elapsed_time(a1) / 3
-                sweep.append({"lanes": g, "smem_levels": t_lv, "ms": ms, "glps": n / ms / 1e6})
+                sweep.append({"smem_levels": t_lv, "queries_per_lane": qpl, "min_ctas_per_sm": minb,
+                              "ms": ms, "glps": n / ms / 1e6})
         fdev.set_kernel_config(lanes_per_query=args.lanes, smem_levels=args.smem_levels,
-                               ctas_per_sm=args.ctas_per_sm)
+                               ctas_per_sm=args.ctas_per_sm, queries_per_lane=args.queries_per_lane,
+                               min_ctas_per_sm=args.min_ctas)
 
     # -- CPU baseline (rank 0, N = 1) ---------------------------------------------------------------------
     cpu = None

@@ -101,8 +101,10 @@ typedef struct {
   uint32_t lanes_per_query; /* lanes cooperating on one 128-byte line in the L2 levels (4) */
   uint32_t smem_levels;     /* top levels staged in shared memory by TMA and searched one
                                thread per query; 0xFF = auto */
-  uint32_t ctas_per_sm;
-  uint32_t threads_per_cta;
+  uint32_t ctas_per_sm;      /* cap on resident CTAs per SM used for the grid; 0 = occupancy */
+  uint32_t threads_per_cta;  /* 256 */
+  uint32_t queries_per_lane; /* 32-query tiles each warp carries at once: 1 or 2 */
+  uint32_t min_ctas_per_sm;  /* register cap (__launch_bounds__ min blocks): 0, 3, 4, 5, 6 */
 } lpm6cu_kernel_config;
 
 typedef struct lpm6cu_fib lpm6cu_fib;

@@ -123,32 +123,25 @@ struct LookupParams {
   const uint4* addrs;
   unsigned char* out;
   unsigned long long n;
-  unsigned long long root[16];  // level 0, compared from the constant bank
-  const unsigned long long* image;  // bank-swizzled copy of levels 1.. (layout.hpp)
+  const unsigned long long* image;  // bank-swizzled copy of levels 0.. (layout.hpp)
   unsigned int smem_levels;  // phase A levels [0, smem_levels), <= depth
-  unsigned int smem_bytes;   // image bytes staged: (level_start[smem_levels] - 16) * 8
+  unsigned int smem_bytes;   // image bytes staged: level_start[smem_levels] * 8
 };
 
 // Count of the 16 keys of node n of a swizzled shared-memory level that are
-// <= q: branch-free binary search (4 halving probes leave c in [0,15]; the fifth
-// adds key 15). Key p of node n lives at n*16 + ((p + n) & 15) (layout.hpp).
+// <= q: branch-free binary search. The probe positions 7, c|3, c|1, c, c are
+// ORs of the bits found so far, so with the XOR swizzle (key p of node n at
+// n*16 + (p ^ (n & 15)), layout.hpp) each probe address is one LOP3 + LEA and
+// each step one predicated OR. Four halving probes leave c in [0,15]; the fifth
+// adds key 15.
 __device__ __forceinline__ unsigned node_rank_smem(const unsigned long long* lvl, unsigned n, unsigned long long q) {
   const unsigned long long* nd = lvl + n * 16u;
-  const unsigned rot = n & 15u;
-  unsigned c = (nd[(7u + rot) & 15u] <= q) ? 8u : 0u;
-  c += (nd[(c + 3u + rot) & 15u] <= q) ? 4u : 0u;
-  c += (nd[(c + 1u + rot) & 15u] <= q) ? 2u : 0u;
-  c += (nd[(c + rot) & 15u] <= q) ? 1u : 0u;
-  c += (nd[(c + rot) & 15u] <= q) ? 1u : 0u;
-  return c;
-}
-
-// Root rank, one thread per query, against the root keys in the launch
-// parameters (constant bank operands: no load through the LSU at all).
-__device__ __forceinline__ unsigned root_rank(const unsigned long long (&root)[16], unsigned long long q) {
-  unsigned c = 0;
-#pragma unroll
-  for (int p = 0; p < 16; ++p) c += (q >= root[p]) ? 1u : 0u;
+  const unsigned x = n & 15u;
+  unsigned c = (nd[7u ^ x] <= q) ? 8u : 0u;
+  c |= (nd[(c | 3u) ^ x] <= q) ? 4u : 0u;
+  c |= (nd[(c | 1u) ^ x] <= q) ? 2u : 0u;
+  c |= (nd[c ^ x] <= q) ? 1u : 0u;
+  c += (nd[c ^ x] <= q) ? 1u : 0u;
   return c;
 }
 
@@ -179,9 +172,37 @@ __device__ __forceinline__ unsigned leaf_value(const unsigned long long (&w)[4],
                                                               : static_cast<unsigned>(v & 0xFFFFFFFFu);
 }
 
-template <int DEPTH, int VB>
-__global__ void __launch_bounds__(256) lpm6_lookup_kernel(const LookupParams p) {
+template <int VB>
+__device__ __forceinline__ void store_group(const LookupParams& p, unsigned long long q0, const unsigned (&v)[4]) {
+  if (q0 + 3 < p.n) {
+    if constexpr (VB == 1) {
+      const unsigned x = v[0] | (v[1] << 8) | (v[2] << 16) | (v[3] << 24);
+      asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p.out + q0), "r"(x));
+    } else if constexpr (VB == 2) {
+      const unsigned long long x = static_cast<unsigned long long>(v[0] | (v[1] << 16)) |
+                                   (static_cast<unsigned long long>(v[2] | (v[3] << 16)) << 32);
+      asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p.out + 2 * q0), "l"(x));
+    } else {
+      asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p.out + 4 * q0), "r"(v[0]), "r"(v[1]),
+                   "r"(v[2]), "r"(v[3]));
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      if (q0 + s >= p.n) break;
+      if constexpr (VB == 1) p.out[q0 + s] = static_cast<unsigned char>(v[s]);
+      else if constexpr (VB == 2) reinterpret_cast<unsigned short*>(p.out)[q0 + s] = static_cast<unsigned short>(v[s]);
+      else reinterpret_cast<unsigned*>(p.out)[q0 + s] = v[s];
+    }
+  }
+}
+
+// TILES consecutive 32-query tiles per warp iteration (lane L owns query L of
+// each); MINB > 0 caps registers so that MINB CTAs of 256 threads fit an SM.
+template <int DEPTH, int VB, int TILES, int MINB>
+__global__ void __launch_bounds__(256, MINB) lpm6_lookup_kernel(const LookupParams p) {
   using F = LeafFmt<VB>;
+  constexpr int NS = 4 * TILES;  // queries in flight per 4-lane group
   extern __shared__ __align__(128) unsigned long long s_lines[];
   __shared__ __align__(8) uint64_t s_bar;
 
@@ -212,71 +233,64 @@ __global__ void __launch_bounds__(256) lpm6_lookup_kernel(const LookupParams p) 
                               : (F::kL - 4 * static_cast<int>(j)) > 4 ? 4u
                                                                       : static_cast<unsigned>(F::kL - 4 * j);
 
-  for (unsigned long long tile = warp0; tile * 32ull < p.n; tile += nwarps) {
-    const unsigned long long qi = tile * 32ull + lane;
-    unsigned long long key = 0;
-    if (qi < p.n) {
-      const uint4 a = ld_stream_v4(p.addrs + qi, pol_stream);
-      key = (static_cast<unsigned long long>(a.w) << 32) | a.z;  // top 64 bits of the u128
-    }
-    key = key > kMaxQueryKey ? kMaxQueryKey : key;  // types.hpp:25
-
-    // Phase A: this thread's own query through the shared-memory levels.
-    unsigned node = 0;
-    if (DEPTH > 0 && TA > 0) node = root_rank(p.root, key);
+  for (unsigned long long st = warp0; st * (32ull * TILES) < p.n; st += nwarps) {
+    unsigned long long key[TILES];
+    unsigned node[TILES];
 #pragma unroll
-    for (int l = 1; l < DEPTH; ++l)
-      if (static_cast<unsigned>(l) < TA)
-        node = node * 17u + node_rank_smem(s_lines + (p.level_start[l] - 16u), node, key);
-
-    // Phase B: the group's 4 queries, one 128-byte line per query per level.
-    unsigned long long qk[4];
-    unsigned nd[4];
-#pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      qk[s] = __shfl_sync(kFull, key, s, 4);
-      nd[s] = __shfl_sync(kFull, node, s, 4);
+    for (int t = 0; t < TILES; ++t) {
+      const unsigned long long qi = (st * TILES + t) * 32ull + lane;
+      unsigned long long k = 0;
+      if (qi < p.n) {
+        const uint4 a = ld_stream_v4(p.addrs + qi, pol_stream);
+        k = (static_cast<unsigned long long>(a.w) << 32) | a.z;  // top 64 bits of the u128
+      }
+      key[t] = k > kMaxQueryKey ? kMaxQueryKey : k;  // types.hpp:25
+      node[t] = 0;
     }
-    unsigned long long w[4][4];
+
+    // Phase A: this thread's own queries through the shared-memory levels.
+#pragma unroll
+    for (int l = 0; l < DEPTH; ++l)
+      if (static_cast<unsigned>(l) < TA) {
+#pragma unroll
+        for (int t = 0; t < TILES; ++t)
+          node[t] = node[t] * 17u + node_rank_smem(s_lines + p.level_start[l], node[t], key[t]);
+      }
+
+    // Phase B: the group's queries, one 128-byte line per query per level.
+    unsigned long long qk[NS];
+    unsigned nd[NS];
+#pragma unroll
+    for (int t = 0; t < TILES; ++t)
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        qk[4 * t + s] = __shfl_sync(kFull, key[t], s, 4);
+        nd[4 * t + s] = __shfl_sync(kFull, node[t], s, 4);
+      }
+    unsigned long long w[NS][4];
 #pragma unroll
     for (int l = 0; l <= DEPTH; ++l) {
       if (l < DEPTH && static_cast<unsigned>(l) < TA) continue;
-      const unsigned long long* lvl = p.lines + p.level_start[l] + j * 4u;
+      // 32-bit word offsets (the layout keeps the array below 2^32 words): one
+      // IMAD + one IMAD.WIDE per address.
+      const unsigned base_w = static_cast<unsigned>(p.level_start[l]) + j * 4u;
 #pragma unroll
-      for (int s = 0; s < 4; ++s) ld_line_quarter(lvl + nd[s] * 16u, w[s]);
+      for (int s = 0; s < NS; ++s) ld_line_quarter(p.lines + (base_w + nd[s] * 16u), w[s]);
 #pragma unroll
-      for (int s = 0; s < 4; ++s) {
+      for (int s = 0; s < NS; ++s) {
         const unsigned r = group_rank(qk[s], w[s], l < DEPTH ? 4u : leaf_valid, gmask);
         nd[s] = (l < DEPTH) ? nd[s] * 17u + r : r - 1u;  // leaf: ordinal within the line
       }
     }
 
-    // Leaf values: the value lane extracts the group's 4 next hops and stores them.
+    // Leaf values: the value lane extracts the group's next hops and stores them.
     if (j == static_cast<unsigned>(F::kValueLane)) {
-      unsigned v[4];
 #pragma unroll
-      for (int s = 0; s < 4; ++s) v[s] = leaf_value<VB>(w[s], nd[s]);
-      const unsigned long long q0 = tile * 32ull + gbase;
-      if (q0 + 3 < p.n) {
-        if constexpr (VB == 1) {
-          const unsigned x = v[0] | (v[1] << 8) | (v[2] << 16) | (v[3] << 24);
-          asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p.out + q0), "r"(x));
-        } else if constexpr (VB == 2) {
-          const unsigned long long x = static_cast<unsigned long long>(v[0] | (v[1] << 16)) |
-                                       (static_cast<unsigned long long>(v[2] | (v[3] << 16)) << 32);
-          asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p.out + 2 * q0), "l"(x));
-        } else {
-          asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p.out + 4 * q0), "r"(v[0]), "r"(v[1]),
-                       "r"(v[2]), "r"(v[3]));
-        }
-      } else {
+      for (int t = 0; t < TILES; ++t) {
+        unsigned v[4];
 #pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          if (q0 + s >= p.n) break;
-          if constexpr (VB == 1) p.out[q0 + s] = static_cast<unsigned char>(v[s]);
-          else if constexpr (VB == 2) reinterpret_cast<unsigned short*>(p.out)[q0 + s] = static_cast<unsigned short>(v[s]);
-          else reinterpret_cast<unsigned*>(p.out)[q0 + s] = v[s];
-        }
+        for (int s = 0; s < 4; ++s) v[s] = leaf_value<VB>(w[4 * t + s], nd[4 * t + s]);
+        store_group<VB>(p, (st * TILES + t) * 32ull + gbase, v);
       }
     }
   }
@@ -284,28 +298,42 @@ __global__ void __launch_bounds__(256) lpm6_lookup_kernel(const LookupParams p) 
 
 using KernelFn = void (*)(const LookupParams);
 
-template <int VB>
+// Instantiated shapes: (queries per lane, min CTAs per SM) for every depth and
+// value width; the tuning grid below is measured by bench.py --sweep.
+template <int VB, int TILES, int MINB>
 KernelFn pick_depth(int depth) {
   switch (depth) {
-    case 0: return lpm6_lookup_kernel<0, VB>;
-    case 1: return lpm6_lookup_kernel<1, VB>;
-    case 2: return lpm6_lookup_kernel<2, VB>;
-    case 3: return lpm6_lookup_kernel<3, VB>;
-    case 4: return lpm6_lookup_kernel<4, VB>;
-    case 5: return lpm6_lookup_kernel<5, VB>;
-    case 6: return lpm6_lookup_kernel<6, VB>;
-    case 7: return lpm6_lookup_kernel<7, VB>;
+    case 0: return lpm6_lookup_kernel<0, VB, TILES, MINB>;
+    case 1: return lpm6_lookup_kernel<1, VB, TILES, MINB>;
+    case 2: return lpm6_lookup_kernel<2, VB, TILES, MINB>;
+    case 3: return lpm6_lookup_kernel<3, VB, TILES, MINB>;
+    case 4: return lpm6_lookup_kernel<4, VB, TILES, MINB>;
+    case 5: return lpm6_lookup_kernel<5, VB, TILES, MINB>;
+    case 6: return lpm6_lookup_kernel<6, VB, TILES, MINB>;
+    case 7: return lpm6_lookup_kernel<7, VB, TILES, MINB>;
     default: return nullptr;
   }
 }
 
-KernelFn pick_kernel(int vb, int depth) {
+template <int TILES, int MINB>
+KernelFn pick_vb(int vb, int depth) {
   switch (vb) {
-    case 1: return pick_depth<1>(depth);
-    case 2: return pick_depth<2>(depth);
-    case 4: return pick_depth<4>(depth);
+    case 1: return pick_depth<1, TILES, MINB>(depth);
+    case 2: return pick_depth<2, TILES, MINB>(depth);
+    case 4: return pick_depth<4, TILES, MINB>(depth);
     default: return nullptr;
   }
+}
+
+KernelFn pick_kernel(int vb, int depth, int tiles, int minb) {
+  if (tiles == 1 && minb == 0) return pick_vb<1, 0>(vb, depth);
+  if (tiles == 1 && minb == 4) return pick_vb<1, 4>(vb, depth);
+  if (tiles == 1 && minb == 5) return pick_vb<1, 5>(vb, depth);
+  if (tiles == 1 && minb == 6) return pick_vb<1, 6>(vb, depth);
+  if (tiles == 2 && minb == 0) return pick_vb<2, 0>(vb, depth);
+  if (tiles == 2 && minb == 3) return pick_vb<2, 3>(vb, depth);
+  if (tiles == 2 && minb == 4) return pick_vb<2, 4>(vb, depth);
+  return nullptr;
 }
 
 // ---- query generator kernel ----------------------------------------------------
@@ -349,7 +377,6 @@ struct lpm6cu_fib {
   int device = 0;
   lpm6cu_geometry g{};
   unsigned long long* d_lines = nullptr;
-  unsigned long long root[16] = {};  // host copy of level 0 (launch parameter)
   bool owns = true;
   lpm6cu_kernel_config cfg{};  // resolved
   int num_sms = 0;
@@ -401,36 +428,38 @@ void resolve_config(lpm6cu_fib* f, const lpm6cu_kernel_config* req) {
   if (c.lanes_per_query != 4) throw Error(Errc::InvalidArgument, "lanes_per_query must be 4");
   if (c.threads_per_cta == 0) c.threads_per_cta = 256;
   if (c.threads_per_cta != 256) throw Error(Errc::InvalidArgument, "threads_per_cta must be 256");
+  if (c.queries_per_lane == 0) c.queries_per_lane = 1;
+  if (!pick_kernel(1, 0, static_cast<int>(c.queries_per_lane), static_cast<int>(c.min_ctas_per_sm)))
+    throw Error(Errc::InvalidArgument, "no kernel for queries_per_lane=" + std::to_string(c.queries_per_lane) +
+                                           " min_ctas_per_sm=" + std::to_string(c.min_ctas_per_sm));
   const unsigned depth = f->g.depth;
   const size_t budget = std::min<size_t>(f->max_smem_optin, 200 * 1024);
+  const unsigned tmax = std::min<unsigned>(depth, f->g.image_levels);  // phase A: imaged internal levels
   if (req == nullptr || req->smem_levels == 0xFF) {
-    // Auto: the deepest prefix of internal levels that fits 48 KiB (keeps >= 4 CTAs/SM).
+    // Auto: the deepest prefix of internal levels whose image fits 48 KiB (keeps >= 4 CTAs/SM).
     unsigned t = 0;
-    const unsigned tmax = depth == 0 ? 0u : std::min<unsigned>(depth, std::max<unsigned>(1u, f->g.image_levels));
     for (unsigned cand = 1; cand <= tmax; ++cand) {
-      if (cand >= 2 && (f->g.level_start[cand] - 16) * 8ull > 48 * 1024) break;
+      if (f->g.level_start[cand] * 8ull > 48 * 1024) break;
       t = cand;
     }
     c.smem_levels = t;
   }
-  const unsigned tmax = depth == 0 ? 0u : std::min<unsigned>(depth, std::max<unsigned>(1u, f->g.image_levels));
-  if (c.smem_levels > tmax) c.smem_levels = tmax;  // phase A: internal levels held by the image
-  const unsigned long long staged = c.smem_levels >= 2 ? (f->g.level_start[c.smem_levels] - 16) * 8ull : 0ull;
+  if (c.smem_levels > tmax) c.smem_levels = tmax;
+  const unsigned long long staged = f->g.level_start[c.smem_levels] * 8ull;
   if (staged > budget)
     throw Error(Errc::InvalidArgument, "smem_levels=" + std::to_string(c.smem_levels) + " needs " +
                                            std::to_string(staged) + " B of shared memory");
   f->cfg = c;
 }
 
-unsigned long long staged_bytes(const lpm6cu_fib* f) {
-  return f->cfg.smem_levels >= 2 ? (f->g.level_start[f->cfg.smem_levels] - 16) * 8ull : 0ull;
-}
+unsigned long long staged_bytes(const lpm6cu_fib* f) { return f->g.level_start[f->cfg.smem_levels] * 8ull; }
 
 void launch_lookup(const lpm6cu_fib* f, const void* d_addrs, unsigned long long n, void* d_out,
                    cudaStream_t stream) {
   if (n == 0) return;
-  KernelFn fn = pick_kernel(static_cast<int>(f->g.value_bytes), static_cast<int>(f->g.depth));
-  if (!fn) throw Error(Errc::InvalidArgument, "no kernel for depth " + std::to_string(f->g.depth));
+  KernelFn fn = pick_kernel(static_cast<int>(f->g.value_bytes), static_cast<int>(f->g.depth),
+                            static_cast<int>(f->cfg.queries_per_lane), static_cast<int>(f->cfg.min_ctas_per_sm));
+  if (!fn) throw Error(Errc::InvalidArgument, "no kernel instantiated for this configuration");
   LookupParams p{};
   p.lines = f->d_lines;
   for (int l = 0; l < LPM6CU_MAX_LEVELS; ++l) p.level_start[l] = f->g.level_start[l];
@@ -440,7 +469,6 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_addrs, unsigned long long 
   p.smem_bytes = static_cast<unsigned>(staged_bytes(f));
   p.smem_levels = f->cfg.smem_levels;
   p.image = f->d_lines + f->g.image_start;
-  std::memcpy(p.root, f->root, sizeof p.root);
   const int threads = static_cast<int>(f->cfg.threads_per_cta);
   const size_t smem = p.smem_bytes;
   if (smem > 48 * 1024)
@@ -450,7 +478,7 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_addrs, unsigned long long 
   check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem), "occupancy");
   if (per_sm < 1) throw Error(Errc::CudaError, "lookup kernel cannot be resident with this configuration");
   if (f->cfg.ctas_per_sm > 0) per_sm = std::min<int>(per_sm, static_cast<int>(f->cfg.ctas_per_sm));
-  const unsigned long long tiles = (n + 31) / 32;
+  const unsigned long long tiles = (n + 32ull * f->cfg.queries_per_lane - 1) / (32ull * f->cfg.queries_per_lane);
   const unsigned long long warps_per_cta = threads / 32;
   unsigned long long grid = static_cast<unsigned long long>(f->num_sms) * per_sm;
   grid = std::min(grid, (tiles + warps_per_cta - 1) / warps_per_cta);
@@ -530,7 +558,6 @@ int lpm6cu_fib_create(int device, const lpm6cu_geometry* g, const uint64_t* line
     const size_t bytes = g->total_words * 8;
     check_cuda(cudaMalloc(&f->d_lines, bytes), "cudaMalloc lines");
     check_cuda(cudaMemcpy(f->d_lines, lines, bytes, cudaMemcpyHostToDevice), "copy lines");
-    std::memcpy(f->root, lines, sizeof f->root);
     *out = f.release();
   });
 }
@@ -544,7 +571,6 @@ int lpm6cu_fib_wrap_device(int device, const lpm6cu_geometry* g, const void* d_l
     std::unique_ptr<lpm6cu_fib> f(new_fib(device, g));
     f->d_lines = static_cast<unsigned long long*>(const_cast<void*>(d_lines));
     f->owns = false;
-    check_cuda(cudaMemcpy(f->root, d_lines, sizeof f->root, cudaMemcpyDeviceToHost), "copy root");
     *out = f.release();
   });
 }
@@ -560,7 +586,6 @@ int lpm6cu_fib_build(int device, const lpm6cu_prefix* rules, uint64_t n, uint32_
     std::unique_ptr<lpm6cu_fib> f(new_fib(device, &g));
     check_cuda(cudaMalloc(&f->d_lines, t.lines.size() * 8), "cudaMalloc lines");
     check_cuda(cudaMemcpy(f->d_lines, t.lines.data(), t.lines.size() * 8, cudaMemcpyHostToDevice), "copy lines");
-    std::memcpy(f->root, t.lines.data(), sizeof f->root);
     *out = f.release();
   });
 }

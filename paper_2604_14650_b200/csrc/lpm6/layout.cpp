@@ -25,12 +25,14 @@ TreeLayout plan_layout(u64 m, u32 value_bytes) {
     g.level_start[l] = off;
     off += g.level_nodes[l] * kLineWords;
   }
-  // Image of internal levels [1, S) for the largest S whose image fits the budget.
-  u32 s = d >= 1 ? 1 : 0;
-  while (s + 1 <= d && (g.level_start[s + 1] - kLineWords) * 8 <= kImageMaxBytes) ++s;
+  // Image of internal levels [0, S) for the largest S <= depth whose image fits the budget.
+  u32 s = 0;
+  while (s + 1 <= d && g.level_start[s + 1] * 8 <= kImageMaxBytes) ++s;
   g.image_levels = s;
   g.image_start = off;
-  g.total_words = off + (s > 1 ? g.level_start[s] - kLineWords : 0);
+  g.total_words = off + g.level_start[s];
+  if (g.total_words >= (u64(1) << 32))
+    throw Error(Errc::InvalidArgument, "tree larger than 32 GiB (word offsets are 32-bit in the kernel)");
   return g;
 }
 
@@ -90,10 +92,10 @@ Tree build_tree(const IntervalMap& map, u32 value_bytes) {
     std::memcpy(line, bytes, sizeof bytes);
   }
 
-  // Shared-memory image: levels [1, image_levels), keys rotated by node index.
-  for (u32 l = 1; l < g.image_levels; ++l) {
+  // Shared-memory image: internal levels [0, image_levels), keys XOR-swizzled by node index.
+  for (u32 l = 0; l < g.image_levels; ++l) {
     const u64* src = t.lines.data() + g.level_start[l];
-    u64* dst = t.lines.data() + g.image_start + (g.level_start[l] - kLineWords);
+    u64* dst = t.lines.data() + g.image_start + g.level_start[l];
     for (u64 n = 0; n < g.level_nodes[l]; ++n)
       for (u32 p = 0; p < kLineWords; ++p) dst[image_slot(n, p)] = src[n * kLineWords + p];
   }

@@ -46,12 +46,11 @@ struct TreeLayout {
   u64 level_nodes[kMaxLevels] = {};  // reachable nodes per level; level depth = leaves
   u64 level_start[kMaxLevels] = {};  // u64-word offset of each level in the line array
   u64 total_words = 0;               // tree lines (16 words each), then the smem image
-  // Bank-swizzled copy of levels [1, image_levels) that the kernel stages into
-  // shared memory with one TMA bulk copy: key p of node n of those levels sits at
-  // word n*16 + ((p + n) & 15), so threads probing the same key position of
+  // Bank-swizzled copy of internal levels [0, image_levels) that the kernel
+  // stages into shared memory with one TMA bulk copy: key p of node n sits at
+  // word n*16 + (p ^ (n & 15)), so threads probing the same key position of
   // different nodes hit different shared-memory banks. Level l of the image
-  // starts at image word level_start[l] - 16 (the root is not imaged: the
-  // kernel takes it as a launch parameter).
+  // starts at image word level_start[l].
   u32 image_levels = 0;
   u64 image_start = 0;
   u32 default_next_hop = 0;
@@ -60,7 +59,7 @@ struct TreeLayout {
 inline constexpr u64 kImageMaxBytes = 200 * 1024;
 
 // Swizzled position of key p of node n in the shared-memory image.
-constexpr u64 image_slot(u64 n, u32 p) { return n * kLineWords + ((p + n) & 15u); }
+constexpr u64 image_slot(u64 n, u32 p) { return n * kLineWords + (p ^ (n & 15u)); }
 
 template <class T, size_t Align>
 struct AlignedAllocator {

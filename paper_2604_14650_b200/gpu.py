@@ -107,15 +107,19 @@ class Fib:
         c = KernelConfig_t()
         check(lib().lpm6cu_fib_kernel_config(self._h, C.byref(c)))
         return {"lanes_per_query": c.lanes_per_query, "smem_levels": c.smem_levels,
-                "ctas_per_sm": c.ctas_per_sm, "threads_per_cta": c.threads_per_cta}
+                "ctas_per_sm": c.ctas_per_sm, "threads_per_cta": c.threads_per_cta,
+                "queries_per_lane": c.queries_per_lane, "min_ctas_per_sm": c.min_ctas_per_sm}
 
     def set_kernel_config(self, lanes_per_query: int = 0, smem_levels: int | None = None,
-                          ctas_per_sm: int = 0, threads_per_cta: int = 0) -> dict:
+                          ctas_per_sm: int = 0, threads_per_cta: int = 0, queries_per_lane: int = 0,
+                          min_ctas_per_sm: int = 0) -> dict:
         c = KernelConfig_t()
         c.lanes_per_query = lanes_per_query
         c.smem_levels = 0xFF if smem_levels is None else smem_levels
         c.ctas_per_sm = ctas_per_sm
         c.threads_per_cta = threads_per_cta
+        c.queries_per_lane = queries_per_lane
+        c.min_ctas_per_sm = min_ctas_per_sm
         check(lib().lpm6cu_fib_set_kernel_config(self._h, C.byref(c)))
         return self.kernel_config()
 

@@ -95,14 +95,15 @@ def check_layout(lpm, orc, fib, n_random=20000, seed=0):
         got = tree.lines[g.level_start[lvl]: g.level_start[lvl] + nodes * 16].reshape(nodes, 16)
         np.testing.assert_array_equal(got, want)
         span *= 17
-    # the shared-memory image is the swizzled copy of levels 1..image_levels-1
-    for lvl in range(1, g.image_levels):
+    # the shared-memory image is the XOR-swizzled copy of internal levels [0, image_levels)
+    assert g.image_levels <= g.depth
+    for lvl in range(g.image_levels):
         nodes = g.level_nodes[lvl]
         src = tree.lines[g.level_start[lvl]: g.level_start[lvl] + nodes * 16].reshape(nodes, 16)
-        off = g.image_start + g.level_start[lvl] - 16
+        off = g.image_start + g.level_start[lvl]
         img = tree.lines[off: off + nodes * 16].reshape(nodes, 16)
-        rot = (np.arange(16)[None, :] + np.arange(nodes)[:, None]) % 16
-        np.testing.assert_array_equal(np.take_along_axis(img, rot, axis=1), src)
+        pos = np.arange(16)[None, :] ^ (np.arange(nodes)[:, None] % 16)
+        np.testing.assert_array_equal(np.take_along_axis(img, pos, axis=1), src)
     # the descent the kernel performs gives the oracle's answer
     rng = np.random.default_rng(seed)
     keys = np.concatenate([boundary_probe_keys(imap.boundaries), rng.integers(0, 2**64, n_random, dtype=np.uint64)])
