@@ -47,6 +47,7 @@ def parse_args():
     ap.add_argument("--ctas-per-sm", type=int, default=0)
     ap.add_argument("--queries-per-lane", type=int, default=0, help="32-query tiles per warp iteration (1/2)")
     ap.add_argument("--min-ctas", type=int, default=0, help="register cap: min CTAs/SM launch bound")
+    ap.add_argument("--threads", type=int, default=0, help="threads per CTA (256/512/1024)")
     ap.add_argument("--queries", type=int, default=0, help="override queries per GPU (testing only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -296,7 +297,7 @@ def main():
     fdev = lpm.Fib.wrap_device(geom, lines_t, dev_index)
     cfg = fdev.set_kernel_config(lanes_per_query=args.lanes, smem_levels=args.smem_levels,
                                  ctas_per_sm=args.ctas_per_sm, queries_per_lane=args.queries_per_lane,
-                                 min_ctas_per_sm=args.min_ctas)
+                                 min_ctas_per_sm=args.min_ctas, threads_per_cta=args.threads)
 
     # -- queries: this rank's slice, generated on the device ------------------------------------
     addrs = torch.empty((n, 16), dtype=torch.uint8, device="cuda")
@@ -381,11 +382,12 @@ def main():
     sweep = None
     if args.sweep and rank == 0:
         sweep = []
-        shapes = [(1, 0), (1, 4), (1, 5), (1, 6), (2, 0), (2, 3), (2, 4)]
+        shapes = [(1, 256, 0), (1, 256, 4), (2, 256, 0), (1, 512, 2), (1, 1024, 1)]
         for t_lv in range(max(0, geom.depth - 2), geom.depth + 1):
-            for qpl, minb in shapes:
+            for qpl, thr, minb in shapes:
                 try:
-                    fdev.set_kernel_config(smem_levels=t_lv, queries_per_lane=qpl, min_ctas_per_sm=minb)
+                    fdev.set_kernel_config(smem_levels=t_lv, queries_per_lane=qpl, threads_per_cta=thr,
+                                           min_ctas_per_sm=minb)
                 except Exception:
                     continue
                 for _ in range(2):
@@ -397,11 +399,11 @@ def main():
                 a1.record(stream)
                 torch.cuda.synchronize()
                 ms = a0.elapsed_time(a1) / 3
-                sweep.append({"smem_levels": t_lv, "queries_per_lane": qpl, "min_ctas_per_sm": minb,
+                sweep.append({"smem_levels": t_lv, "queries_per_lane": qpl, "threads": thr, "min_ctas_per_sm": minb,
                               "ms": ms, "glps": n / ms / 1e6})
         fdev.set_kernel_config(lanes_per_query=args.lanes, smem_levels=args.smem_levels,
                                ctas_per_sm=args.ctas_per_sm, queries_per_lane=args.queries_per_lane,
-                               min_ctas_per_sm=args.min_ctas)
+                               min_ctas_per_sm=args.min_ctas, threads_per_cta=args.threads)
 
     # -- CPU baseline (rank 0, N = 1) ---------------------------------------------------------------------
     cpu = None

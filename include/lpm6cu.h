@@ -70,10 +70,10 @@ typedef struct {
 #define LPM6CU_MAX_LEVELS 9
 
 /* Geometry of the B200 tree layout: one array of 128-byte lines. Internal
- * lines hold k = 16 separator keys; leaf lines hold leaf_keys boundary keys
+ * lines hold k = 15 separator keys (arity 16); leaf lines hold leaf_keys boundary keys
  * followed by their next hops. Counterpart of lpm6::TreeGeometry (tree.hpp:18-33). */
 typedef struct {
-  uint32_t k;           /* keys per internal node (16) */
+  uint32_t k;           /* separator keys per internal node (15; word 15 is padding) */
   uint32_t b;           /* arity, k + 1 */
   uint32_t depth;       /* internal levels; a lookup visits depth + 1 lines */
   uint32_t value_bytes; /* next-hop width: 1, 2 or 4 */

@@ -31,7 +31,7 @@
 // persistent (grid = SMs x resident CTAs) and stride over tiles.
 //
 // Results are the reference's: key = min(addr >> 64, 0xFFFF...FFFE)
-// (types.hpp:25), internal child = node * 17 + rank, leaf ordinal =
+// (types.hpp:25), internal child = node * 16 + rank, leaf ordinal =
 // rank - 1, next hop = the value of that leaf slot.
 #include <cuda_runtime.h>
 
@@ -123,25 +123,22 @@ struct LookupParams {
   const uint4* addrs;
   unsigned char* out;
   unsigned long long n;
-  const unsigned long long* image;  // bank-swizzled copy of levels 0.. (layout.hpp)
+  const unsigned long long* image;  // packed 15-key copy of internal levels 0.. (layout.hpp)
   unsigned int smem_levels;  // phase A levels [0, smem_levels), <= depth
-  unsigned int smem_bytes;   // image bytes staged: level_start[smem_levels] * 8
+  unsigned int smem_bytes;   // image bytes staged for those levels
 };
 
-// Count of the 16 keys of node n of a swizzled shared-memory level that are
-// <= q: branch-free binary search. The probe positions 7, c|3, c|1, c, c are
-// ORs of the bits found so far, so with the XOR swizzle (key p of node n at
-// n*16 + (p ^ (n & 15)), layout.hpp) each probe address is one LOP3 + LEA and
-// each step one predicated OR. Four halving probes leave c in [0,15]; the fifth
-// adds key 15.
+// Count of the 15 separators of node n of a shared-memory image level that are
+// <= q: a branch-free 4-probe binary search (16 outcomes). The probe positions
+// 7, c|3, c|1, c are ORs of the bits found so far (one predicated OR per step).
+// Nodes are packed at a 15-word stride (layout.hpp), which puts the same
+// position of different nodes in different shared-memory banks.
 __device__ __forceinline__ unsigned node_rank_smem(const unsigned long long* lvl, unsigned n, unsigned long long q) {
-  const unsigned long long* nd = lvl + n * 16u;
-  const unsigned x = n & 15u;
-  unsigned c = (nd[7u ^ x] <= q) ? 8u : 0u;
-  c |= (nd[(c | 3u) ^ x] <= q) ? 4u : 0u;
-  c |= (nd[(c | 1u) ^ x] <= q) ? 2u : 0u;
-  c |= (nd[c ^ x] <= q) ? 1u : 0u;
-  c += (nd[c ^ x] <= q) ? 1u : 0u;
+  const unsigned long long* nd = lvl + n * 15u;
+  unsigned c = (nd[7] <= q) ? 8u : 0u;
+  c |= (nd[c | 3u] <= q) ? 4u : 0u;
+  c |= (nd[c | 1u] <= q) ? 2u : 0u;
+  c |= (nd[c] <= q) ? 1u : 0u;
   return c;
 }
 
@@ -198,9 +195,9 @@ __device__ __forceinline__ void store_group(const LookupParams& p, unsigned long
 }
 
 // TILES consecutive 32-query tiles per warp iteration (lane L owns query L of
-// each); MINB > 0 caps registers so that MINB CTAs of 256 threads fit an SM.
-template <int DEPTH, int VB, int TILES, int MINB>
-__global__ void __launch_bounds__(256, MINB) lpm6_lookup_kernel(const LookupParams p) {
+// each); MINB > 0 caps registers so that MINB CTAs of THREADS threads fit an SM.
+template <int DEPTH, int VB, int TILES, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const LookupParams p) {
   using F = LeafFmt<VB>;
   constexpr int NS = 4 * TILES;  // queries in flight per 4-lane group
   extern __shared__ __align__(128) unsigned long long s_lines[];
@@ -254,7 +251,7 @@ __global__ void __launch_bounds__(256, MINB) lpm6_lookup_kernel(const LookupPara
       if (static_cast<unsigned>(l) < TA) {
 #pragma unroll
         for (int t = 0; t < TILES; ++t)
-          node[t] = node[t] * 17u + node_rank_smem(s_lines + p.level_start[l], node[t], key[t]);
+          node[t] = node[t] * 16u + node_rank_smem(s_lines + (p.level_start[l] >> 4) * 15u, node[t], key[t]);
       }
 
     // Phase B: the group's queries, one 128-byte line per query per level.
@@ -279,7 +276,7 @@ __global__ void __launch_bounds__(256, MINB) lpm6_lookup_kernel(const LookupPara
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
         const unsigned r = group_rank(qk[s], w[s], l < DEPTH ? 4u : leaf_valid, gmask);
-        nd[s] = (l < DEPTH) ? nd[s] * 17u + r : r - 1u;  // leaf: ordinal within the line
+        nd[s] = (l < DEPTH) ? nd[s] * 16u + r : r - 1u;  // leaf: ordinal within the line
       }
     }
 
@@ -300,39 +297,39 @@ using KernelFn = void (*)(const LookupParams);
 
 // Instantiated shapes: (queries per lane, min CTAs per SM) for every depth and
 // value width; the tuning grid below is measured by bench.py --sweep.
-template <int VB, int TILES, int MINB>
+template <int VB, int TILES, int THREADS, int MINB>
 KernelFn pick_depth(int depth) {
   switch (depth) {
-    case 0: return lpm6_lookup_kernel<0, VB, TILES, MINB>;
-    case 1: return lpm6_lookup_kernel<1, VB, TILES, MINB>;
-    case 2: return lpm6_lookup_kernel<2, VB, TILES, MINB>;
-    case 3: return lpm6_lookup_kernel<3, VB, TILES, MINB>;
-    case 4: return lpm6_lookup_kernel<4, VB, TILES, MINB>;
-    case 5: return lpm6_lookup_kernel<5, VB, TILES, MINB>;
-    case 6: return lpm6_lookup_kernel<6, VB, TILES, MINB>;
-    case 7: return lpm6_lookup_kernel<7, VB, TILES, MINB>;
+    case 0: return lpm6_lookup_kernel<0, VB, TILES, THREADS, MINB>;
+    case 1: return lpm6_lookup_kernel<1, VB, TILES, THREADS, MINB>;
+    case 2: return lpm6_lookup_kernel<2, VB, TILES, THREADS, MINB>;
+    case 3: return lpm6_lookup_kernel<3, VB, TILES, THREADS, MINB>;
+    case 4: return lpm6_lookup_kernel<4, VB, TILES, THREADS, MINB>;
+    case 5: return lpm6_lookup_kernel<5, VB, TILES, THREADS, MINB>;
+    case 6: return lpm6_lookup_kernel<6, VB, TILES, THREADS, MINB>;
+    case 7: return lpm6_lookup_kernel<7, VB, TILES, THREADS, MINB>;
     default: return nullptr;
   }
 }
 
-template <int TILES, int MINB>
+template <int TILES, int THREADS, int MINB>
 KernelFn pick_vb(int vb, int depth) {
   switch (vb) {
-    case 1: return pick_depth<1, TILES, MINB>(depth);
-    case 2: return pick_depth<2, TILES, MINB>(depth);
-    case 4: return pick_depth<4, TILES, MINB>(depth);
+    case 1: return pick_depth<1, TILES, THREADS, MINB>(depth);
+    case 2: return pick_depth<2, TILES, THREADS, MINB>(depth);
+    case 4: return pick_depth<4, TILES, THREADS, MINB>(depth);
     default: return nullptr;
   }
 }
 
-KernelFn pick_kernel(int vb, int depth, int tiles, int minb) {
-  if (tiles == 1 && minb == 0) return pick_vb<1, 0>(vb, depth);
-  if (tiles == 1 && minb == 4) return pick_vb<1, 4>(vb, depth);
-  if (tiles == 1 && minb == 5) return pick_vb<1, 5>(vb, depth);
-  if (tiles == 1 && minb == 6) return pick_vb<1, 6>(vb, depth);
-  if (tiles == 2 && minb == 0) return pick_vb<2, 0>(vb, depth);
-  if (tiles == 2 && minb == 3) return pick_vb<2, 3>(vb, depth);
-  if (tiles == 2 && minb == 4) return pick_vb<2, 4>(vb, depth);
+// Instantiated shapes (queries per lane, threads per CTA, min CTAs per SM);
+// bench.py --sweep measures them.
+KernelFn pick_kernel(int vb, int depth, int tiles, int threads, int minb) {
+  if (tiles == 1 && threads == 256 && minb == 0) return pick_vb<1, 256, 0>(vb, depth);
+  if (tiles == 1 && threads == 256 && minb == 4) return pick_vb<1, 256, 4>(vb, depth);
+  if (tiles == 2 && threads == 256 && minb == 0) return pick_vb<2, 256, 0>(vb, depth);
+  if (tiles == 1 && threads == 512 && minb == 2) return pick_vb<1, 512, 2>(vb, depth);
+  if (tiles == 1 && threads == 1024 && minb == 1) return pick_vb<1, 1024, 1>(vb, depth);
   return nullptr;
 }
 
@@ -420,45 +417,60 @@ struct lpm6cu_querygen {
 
 namespace {
 
+// Bytes of the shared-memory image for `levels` levels (layout.hpp image_bytes).
+unsigned long long image_bytes_of(const lpm6cu_geometry& g, unsigned levels) {
+  return (g.level_start[levels] / kLineWords * kNodeKeys * 8 + 15) / 16 * 16;
+}
+
 // Resolve automatic kernel settings against the device and the tree.
 void resolve_config(lpm6cu_fib* f, const lpm6cu_kernel_config* req) {
   lpm6cu_kernel_config c{};
   if (req) c = *req;
   if (c.lanes_per_query == 0) c.lanes_per_query = 4;
   if (c.lanes_per_query != 4) throw Error(Errc::InvalidArgument, "lanes_per_query must be 4");
-  if (c.threads_per_cta == 0) c.threads_per_cta = 256;
-  if (c.threads_per_cta != 256) throw Error(Errc::InvalidArgument, "threads_per_cta must be 256");
+  // Default shape (measured, bench.py --sweep): one 1024-thread CTA per SM, so a
+  // single shared-memory image per SM serves 32 warps and can be as large as
+  // the opt-in limit (227 KiB) — all four internal levels of the 200K FIB.
+  if (c.threads_per_cta == 0) c.threads_per_cta = 1024;
   if (c.queries_per_lane == 0) c.queries_per_lane = 1;
-  if (!pick_kernel(1, 0, static_cast<int>(c.queries_per_lane), static_cast<int>(c.min_ctas_per_sm)))
+  if (c.min_ctas_per_sm == 0 && c.threads_per_cta == 512) c.min_ctas_per_sm = 2;
+  if (c.min_ctas_per_sm == 0 && c.threads_per_cta == 1024) c.min_ctas_per_sm = 1;
+  if (!pick_kernel(1, 0, static_cast<int>(c.queries_per_lane), static_cast<int>(c.threads_per_cta),
+                   static_cast<int>(c.min_ctas_per_sm)))
     throw Error(Errc::InvalidArgument, "no kernel for queries_per_lane=" + std::to_string(c.queries_per_lane) +
+                                           " threads_per_cta=" + std::to_string(c.threads_per_cta) +
                                            " min_ctas_per_sm=" + std::to_string(c.min_ctas_per_sm));
   const unsigned depth = f->g.depth;
-  const size_t budget = std::min<size_t>(f->max_smem_optin, 200 * 1024);
+  const size_t budget = f->max_smem_optin;
   const unsigned tmax = std::min<unsigned>(depth, f->g.image_levels);  // phase A: imaged internal levels
   if (req == nullptr || req->smem_levels == 0xFF) {
-    // Auto: the deepest prefix of internal levels whose image fits 48 KiB (keeps >= 4 CTAs/SM).
+    // Auto: the deepest prefix of internal levels whose image fits the shared
+    // memory one CTA may use; with 256-thread CTAs keep >= 4 CTAs per SM.
+    const unsigned long long cap = c.threads_per_cta >= 1024 ? budget
+                                   : c.threads_per_cta == 512 ? budget / 2 - 1024 : 48 * 1024;
     unsigned t = 0;
     for (unsigned cand = 1; cand <= tmax; ++cand) {
-      if (f->g.level_start[cand] * 8ull > 48 * 1024) break;
+      if (image_bytes_of(f->g, cand) > cap) break;
       t = cand;
     }
     c.smem_levels = t;
   }
   if (c.smem_levels > tmax) c.smem_levels = tmax;
-  const unsigned long long staged = f->g.level_start[c.smem_levels] * 8ull;
+  const unsigned long long staged = image_bytes_of(f->g, c.smem_levels);
   if (staged > budget)
     throw Error(Errc::InvalidArgument, "smem_levels=" + std::to_string(c.smem_levels) + " needs " +
                                            std::to_string(staged) + " B of shared memory");
   f->cfg = c;
 }
 
-unsigned long long staged_bytes(const lpm6cu_fib* f) { return f->g.level_start[f->cfg.smem_levels] * 8ull; }
+unsigned long long staged_bytes(const lpm6cu_fib* f) { return image_bytes_of(f->g, f->cfg.smem_levels); }
 
 void launch_lookup(const lpm6cu_fib* f, const void* d_addrs, unsigned long long n, void* d_out,
                    cudaStream_t stream) {
   if (n == 0) return;
   KernelFn fn = pick_kernel(static_cast<int>(f->g.value_bytes), static_cast<int>(f->g.depth),
-                            static_cast<int>(f->cfg.queries_per_lane), static_cast<int>(f->cfg.min_ctas_per_sm));
+                            static_cast<int>(f->cfg.queries_per_lane), static_cast<int>(f->cfg.threads_per_cta),
+                            static_cast<int>(f->cfg.min_ctas_per_sm));
   if (!fn) throw Error(Errc::InvalidArgument, "no kernel instantiated for this configuration");
   LookupParams p{};
   p.lines = f->d_lines;
@@ -488,7 +500,7 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_addrs, unsigned long long 
 
 lpm6cu_fib* new_fib(int device, const lpm6cu_geometry* g) {
   if (!g) throw Error(Errc::InvalidArgument, "geometry is NULL");
-  if (g->k != kNodeKeys || g->b != kNodeKeys + 1) throw Error(Errc::InvalidArgument, "the kernels take k = 16");
+  if (g->k != kNodeKeys || g->b != kNodeKeys + 1) throw Error(Errc::InvalidArgument, "the kernels take k = 15, b = 16");
   if (g->leaf_keys != leaf_keys_for(g->value_bytes)) throw Error(Errc::InvalidArgument, "leaf_keys mismatch");
   if (g->depth > kMaxKernelDepth) throw Error(Errc::InvalidArgument, "tree depth above 7");
   if (g->value_bytes != 1 && g->value_bytes != 2 && g->value_bytes != 4)

@@ -27,10 +27,10 @@ TreeLayout plan_layout(u64 m, u32 value_bytes) {
   }
   // Image of internal levels [0, S) for the largest S <= depth whose image fits the budget.
   u32 s = 0;
-  while (s + 1 <= d && g.level_start[s + 1] * 8 <= kImageMaxBytes) ++s;
+  while (s + 1 <= d && image_bytes(g, s + 1) <= kImageMaxBytes) ++s;
   g.image_levels = s;
   g.image_start = off;
-  g.total_words = off + g.level_start[s];
+  g.total_words = off + image_bytes(g, s) / 8;
   if (g.total_words >= (u64(1) << 32))
     throw Error(Errc::InvalidArgument, "tree larger than 32 GiB (word offsets are 32-bit in the kernel)");
   return g;
@@ -92,12 +92,12 @@ Tree build_tree(const IntervalMap& map, u32 value_bytes) {
     std::memcpy(line, bytes, sizeof bytes);
   }
 
-  // Shared-memory image: internal levels [0, image_levels), keys XOR-swizzled by node index.
+  // Shared-memory image: internal levels [0, image_levels), 15 keys per node.
   for (u32 l = 0; l < g.image_levels; ++l) {
     const u64* src = t.lines.data() + g.level_start[l];
-    u64* dst = t.lines.data() + g.image_start + g.level_start[l];
+    u64* dst = t.lines.data() + g.image_start + image_level_start(g, l);
     for (u64 n = 0; n < g.level_nodes[l]; ++n)
-      for (u32 p = 0; p < kLineWords; ++p) dst[image_slot(n, p)] = src[n * kLineWords + p];
+      for (u32 p = 0; p < kNodeKeys; ++p) dst[image_slot(n, p)] = src[n * kLineWords + p];
   }
   return t;
 }

@@ -5,8 +5,11 @@
 // with next hops in a separate array indexed by leaf slot (tree.hpp:14-74,
 // S:179-223). On B200 every node is one 128-byte L2 line:
 //
-//   * internal nodes hold k = 16 separator keys (arity b = 17, the paper's own
-//     rule for 128-byte lines);
+//   * internal nodes hold k = 15 separator keys and a sentinel pad word, arity
+//     b = 16 (the paper sizes nodes to the cache line: a 128-byte line
+//     holds 16 keys; we give up the 16th separator so that the fan-out is a power
+//     of two — a node rank is then exactly 4 binary-search probes and the child
+//     index a shift; for the BASELINE FIBs the depth is the same as with b = 17);
 //   * a leaf line holds kL boundary keys followed by their kL next hops
 //     (kL = 14 for 1-byte, 12 for 2-byte, 8 for 4-byte next hops), so the
 //     final value load of the reference (values[i - leaf_start])
@@ -29,7 +32,7 @@
 namespace lpm6 {
 
 inline constexpr int kMaxLevels = 9;  // depth <= 8
-inline constexpr u32 kNodeKeys = 16;  // internal keys per 128-byte line
+inline constexpr u32 kNodeKeys = 15;  // internal separator keys per 128-byte line (word 15 = pad)
 inline constexpr u32 kLineWords = 16;  // u64 words per line
 
 // Keys per leaf line for a next-hop width (leaf = kL keys + kL values <= 128 B).
@@ -46,20 +49,25 @@ struct TreeLayout {
   u64 level_nodes[kMaxLevels] = {};  // reachable nodes per level; level depth = leaves
   u64 level_start[kMaxLevels] = {};  // u64-word offset of each level in the line array
   u64 total_words = 0;               // tree lines (16 words each), then the smem image
-  // Bank-swizzled copy of internal levels [0, image_levels) that the kernel
-  // stages into shared memory with one TMA bulk copy: key p of node n sits at
-  // word n*16 + (p ^ (n & 15)), so threads probing the same key position of
-  // different nodes hit different shared-memory banks. Level l of the image
-  // starts at image word level_start[l].
+  // Packed copy of internal levels [0, image_levels) that the kernel stages
+  // into shared memory with one TMA bulk copy: the 15 separators of each node,
+  // 120 bytes per node (no pad word). The 15-word node stride also skews the
+  // shared-memory banks: key p of node n lives in 8-byte bank pair
+  // (15n + p) mod 16, so threads probing the same position of different nodes
+  // hit different banks. Level l of the image starts at image word
+  // image_level_start(l) = (level_start[l] / 16) * 15.
   u32 image_levels = 0;
   u64 image_start = 0;
   u32 default_next_hop = 0;
 };
 
-inline constexpr u64 kImageMaxBytes = 200 * 1024;
+inline constexpr u64 kImageMaxBytes = 232448 - 1024;  // B200 opt-in smem per CTA minus static smem
 
-// Swizzled position of key p of node n in the shared-memory image.
-constexpr u64 image_slot(u64 n, u32 p) { return n * kLineWords + (p ^ (n & 15u)); }
+// Word offset of level l / of key p of node n (within its level) in the image.
+constexpr u64 image_level_start(const TreeLayout& g, u32 l) { return g.level_start[l] / kLineWords * kNodeKeys; }
+constexpr u64 image_slot(u64 n, u32 p) { return n * kNodeKeys + p; }
+// Bytes the kernel stages for `levels` imaged levels (TMA sizes are 16-byte multiples).
+constexpr u64 image_bytes(const TreeLayout& g, u32 levels) { return (image_level_start(g, levels) * 8 + 15) / 16 * 16; }
 
 template <class T, size_t Align>
 struct AlignedAllocator {

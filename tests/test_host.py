@@ -60,8 +60,8 @@ def walk_layout(tree, keys):
     node = np.zeros(len(q), np.int64)
     for lvl in range(g.depth):
         base = g.level_start[lvl] + node * 16
-        nd = lines[base[:, None] + np.arange(16)]
-        node = node * 17 + (nd <= q[:, None]).sum(axis=1)
+        nd = lines[base[:, None] + np.arange(g.k)]
+        node = node * g.b + (nd <= q[:, None]).sum(axis=1)
     base = g.level_start[g.depth] + node * 16
     lf = lines[base[:, None] + np.arange(g.leaf_keys)]
     ordinal = (lf <= q[:, None]).sum(axis=1) - 1
@@ -74,11 +74,12 @@ def check_layout(lpm, orc, fib, n_random=20000, seed=0):
     tree = lpm.build_tree(imap)
     g = tree.geometry
     m = len(imap)
-    # geometry: minimal depth, compact reachable levels
-    assert g.leaf_keys * 17 ** g.depth >= m and (g.depth == 0 or g.leaf_keys * 17 ** (g.depth - 1) < m)
+    # geometry: 15 separators + pad per internal line, arity 16; minimal depth; compact levels
+    assert (g.k, g.b) == (15, 16)
+    assert g.leaf_keys * 16 ** g.depth >= m and (g.depth == 0 or g.leaf_keys * 16 ** (g.depth - 1) < m)
     assert g.leaf_nodes == -(-m // g.leaf_keys)
     for lvl in range(g.depth):
-        assert g.level_nodes[lvl] == -(-g.level_nodes[lvl + 1] // 17)
+        assert g.level_nodes[lvl] == -(-g.level_nodes[lvl + 1] // 16)
     assert g.level_nodes[0] == 1
     # leaves: boundaries then sentinels; values replicate the last one
     lk = tree.leaf_keys_array()
@@ -86,24 +87,25 @@ def check_layout(lpm, orc, fib, n_random=20000, seed=0):
     assert np.all(lk[m:] == np.uint64(MASK64))
     np.testing.assert_array_equal(tree.leaf_values[:m], imap.next_hops)
     assert np.all(tree.leaf_values[m:] == imap.next_hops[-1])
-    # internal separators = boundary[(n*17 + j + 1) * span]
+    # internal separators = boundary[(n*16 + j + 1) * span], word 15 = sentinel pad
     span = g.leaf_keys
     for lvl in range(g.depth - 1, -1, -1):
         nodes = g.level_nodes[lvl]
-        idx = (np.arange(nodes)[:, None] * 17 + np.arange(16)[None, :] + 1) * span
+        idx = (np.arange(nodes)[:, None] * g.b + np.arange(g.k)[None, :] + 1) * span
         want = np.where(idx < m, imap.boundaries[np.minimum(idx, m - 1)], np.uint64(MASK64))
         got = tree.lines[g.level_start[lvl]: g.level_start[lvl] + nodes * 16].reshape(nodes, 16)
-        np.testing.assert_array_equal(got, want)
-        span *= 17
-    # the shared-memory image is the XOR-swizzled copy of internal levels [0, image_levels)
+        np.testing.assert_array_equal(got[:, : g.k], want)
+        assert np.all(got[:, 15] == np.uint64(MASK64))
+        span *= g.b
+    # the shared-memory image packs the 15 separators of internal levels [0, image_levels)
     assert g.image_levels <= g.depth
     for lvl in range(g.image_levels):
         nodes = g.level_nodes[lvl]
         src = tree.lines[g.level_start[lvl]: g.level_start[lvl] + nodes * 16].reshape(nodes, 16)
-        off = g.image_start + g.level_start[lvl]
-        img = tree.lines[off: off + nodes * 16].reshape(nodes, 16)
-        pos = np.arange(16)[None, :] ^ (np.arange(nodes)[:, None] % 16)
-        np.testing.assert_array_equal(np.take_along_axis(img, pos, axis=1), src)
+        off = g.image_start + g.level_start[lvl] // 16 * 15
+        img = tree.lines[off: off + nodes * 15].reshape(nodes, 15)
+        np.testing.assert_array_equal(img, src[:, :15])
+    assert (g.total_words - g.image_start) * 8 <= 232448 - 1024
     # the descent the kernel performs gives the oracle's answer
     rng = np.random.default_rng(seed)
     keys = np.concatenate([boundary_probe_keys(imap.boundaries), rng.integers(0, 2**64, n_random, dtype=np.uint64)])
@@ -152,10 +154,10 @@ def test_layout_value_width_errors(lpm):
 
 
 def test_plan_layout_depths(lpm):
-    for m, d in ((1, 0), (14, 0), (15, 1), (14 * 17, 1), (14 * 17 + 1, 2), (387232, 4)):
+    for m, d in ((1, 0), (14, 0), (15, 1), (14 * 16, 1), (14 * 16 + 1, 2), (387232, 4)):
         assert lpm.plan_layout(m, 1).depth == d
     assert lpm.plan_layout(1893858, 2).depth == 5
-    g = lpm.plan_layout(12 * 17 ** 6 + 1, 2)
+    g = lpm.plan_layout(12 * 16 ** 6 + 1, 2)
     assert g.depth == 7
 
 
