@@ -142,6 +142,19 @@ def hbm_peak():
     return HBM_FALLBACK_GBS, "B200_PROFILING.md fallback"
 
 
+def measured_traffic(workload, n):
+    """DRAM bytes per lookup launch of n queries, scaled from the committed ncu capture
+    (profiles/r01_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum of one launch)."""
+    p = ROOT / "profiles" / "r01_traffic.json"
+    try:
+        t = json.loads(p.read_text())
+        key = {"C3a": "C1", "C3b": "C1", "C4": "C2"}.get(workload, workload)
+        e = t[key]
+        return (e["dram_read_bytes"] + e["dram_write_bytes"]) / e["queries"] * n
+    except Exception:
+        return None
+
+
 def roofline(geom, w, l2_gbs, smem_gbs, hbm_gbs, smem_cap=232448):
     """roofline_lps = max_T min(HBM/(16+w), SMEM/(128 T), L2/(128 (d+1-T) + w))."""
     d = geom.depth
@@ -262,6 +275,95 @@ def run_reference(args):
     return 0
 
 
+# ---- C4: fixed total, 64M-address chunks partitioned across GPUs ---------------------------------
+
+def run_chunked(args, lpm, dispatch, fdev, fib, info, geom, cfg, ws, rank, dev_index, dist, build_ms, bcast_ms):
+    """C4 (BASELINE configs[4]): info.n_queries addresses in info.chunk-sized chunks, chunk c
+    seeded by its index (any GPU can generate any chunk), chunks split contiguously over the
+    ranks (strong scaling). Each chunk is generated on the device untimed, then looked up
+    between CUDA events; a step = one pass over this rank's chunks; device time = max over
+    ranks of the summed lookup times."""
+    import torch
+    chunk, vb = info.chunk, info.value_bytes
+    total_chunks = info.n_queries // chunk
+    c0, nc = dispatch.shard(rank, ws, 0, total=total_chunks)
+    addrs = torch.empty((chunk, 16), dtype=torch.uint8, device="cuda")
+    out = torch.empty(chunk * vb, dtype=torch.uint8, device="cuda")
+    gen = lpm.QueryGen(args.workload, fib, dev_index)
+    stream = torch.cuda.current_stream()
+    l2_gbs = lpm.probe_l2_gather(dev_index, max(geom.tree_bytes, 1 << 22), 128)
+    smem_gbs = lpm.probe_smem(dev_index)
+    hbm_gbs, hbm_src = hbm_peak()
+
+    def one_pass():
+        evs = []
+        for c in range(c0, c0 + nc):
+            gen.run(c * chunk, chunk, addrs, stream)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fdev.lookup_batch(addrs, out, stream)
+            b.record(stream)
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        return sum(a.elapsed_time(b) for a, b in evs)
+
+    for _ in range(max(args.warmup, 0)):
+        one_pass()
+    if dist is not None:
+        dist.barrier()
+    with ClockSampler(dev_index) as clk:
+        step_ms = [one_pass() for _ in range(args.steps)]
+    total_ms = dispatch.max_over_ranks(sum(step_ms), dist, "cuda")
+    value = info.n_queries * args.steps / (total_ms * 1e-3) / 1e9
+    parity = None
+    if rank == 0:
+        from oracle.oracle import Oracle
+        o = Oracle()
+        gen.run(c0 * chunk, 1 << 20, addrs, stream)
+        fdev.lookup_batch(addrs[: 1 << 20], out[: (1 << 20) * vb], stream)
+        torch.cuda.synchronize()
+        st, b, nh = o.build_intervals(fib.rules, fib.default_next_hop)
+        ha = addrs[: 1 << 20].cpu().numpy().view(np.uint64).reshape(-1, 2)
+        want, _ = o.lookup_batch(0, b, nh, ha, threads=cpu_threads())
+        got = out[: (1 << 20) * vb].cpu().numpy().view({1: np.uint8, 2: np.uint16, 4: np.uint32}[vb])
+        parity = {"checked": 1 << 20, "mismatches": int(np.count_nonzero(got.astype(np.uint32) != want)),
+                  "oracle": "oracle/lpm6_oracle.c interval oracle", "chunk": c0}
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+        return 0
+    lps_gpu = nc * chunk * args.steps / (sum(step_ms) * 1e-3)
+    rl = roofline(geom, vb, l2_gbs, smem_gbs, hbm_gbs)
+    bpq = rl["bytes_per_query"][rl["bound"]]
+    peak = {"hbm": hbm_gbs, "smem": smem_gbs, "l2": l2_gbs}[rl["bound"]]
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "u64",
+        "data": f"synthetic: seeded {info.name} FIB ({len(fib)} prefixes); {info.n_queries} queries in "
+                f"{total_chunks} chunks of {chunk}, chunk c seeded by c, generated on device (untimed)",
+        "config": {"workload": info.name, "fib_prefixes": len(fib), "intervals": geom.num_keys,
+                   "tree_depth": geom.depth, "queries_total": info.n_queries, "chunk": chunk,
+                   "chunks_per_gpu": nc, "value_bytes": vb, "kernel": cfg,
+                   "l2_flush": f"not needed: each chunk streams {chunk * 16 / 1e9:.1f} GB of addresses",
+                   "parallelism": f"dp{ws} (contiguous chunk ranges; FIB replicated by NCCL broadcast)"},
+        "roofline": {"bound": rl["bound"], "achieved": lps_gpu * bpq / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": lps_gpu * bpq / 1e9 / peak, "traffic": measured_traffic(info.name, chunk),
+                     "lps_achieved_per_gpu": lps_gpu / 1e9,
+                     "lps_roofline_per_gpu": rl["lps"] / 1e9, "terms_glps": rl["terms_glps"],
+                     "measured": {"l2_gather_gbs": l2_gbs, "smem_gbs": smem_gbs, "hbm_gbs": hbm_gbs,
+                                  "hbm_source": hbm_src}},
+        "cpu_baseline": None, "e2e": None,
+        "gpu_launches": 2 * nc * args.steps,
+        "clocks": clk.summary(), "parity_sample": parity,
+        "fib_build_ms": build_ms, "fib_broadcast_ms": bcast_ms, "step_ms": step_ms,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+    return 0
+
+
 # ---- our arm ------------------------------------------------------------------------------------
 
 def main():
@@ -298,6 +400,9 @@ def main():
     cfg = fdev.set_kernel_config(lanes_per_query=args.lanes, smem_levels=args.smem_levels,
                                  ctas_per_sm=args.ctas_per_sm, queries_per_lane=args.queries_per_lane,
                                  min_ctas_per_sm=args.min_ctas, threads_per_cta=args.threads)
+    if info.chunk and not args.queries:
+        return run_chunked(args, lpm, dispatch, fdev, fib, info, geom, cfg, ws, rank, dev_index, dist,
+                           build_ms, bcast_ms)
 
     # -- queries: this rank's slice, generated on the device ------------------------------------
     addrs = torch.empty((n, 16), dtype=torch.uint8, device="cuda")
@@ -443,7 +548,7 @@ def main():
                    "l2_flush": f"not needed: each step streams {n * 16 / 1e9:.1f} GB of addresses (> 126 MB L2)",
                    "parallelism": f"dp{ws} (query batches; FIB replicated by NCCL broadcast)"},
         "roofline": {"bound": rl["bound"], "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": measured_traffic(info.name, n),
                      "lps_achieved_per_gpu": lps_gpu / 1e9, "lps_roofline_per_gpu": rl["lps"] / 1e9,
                      "smem_levels_for_roofline": rl["T"], "terms_glps": rl["terms_glps"],
                      "bytes_per_query": rl["bytes_per_query"],
