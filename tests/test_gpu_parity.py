@@ -162,3 +162,15 @@ def test_c1_full_size(lpm, orc, cuda):
         want = oracle_next_hops(orc, imap.boundaries, imap.next_hops, host_addrs)
         mism += int(np.count_nonzero(out.cpu().numpy().astype(np.uint32) != want))
     assert mism == 0
+
+
+def test_reference_dropin(cuda):
+    """The reference's own FibTable -> lpm6::gpu::Fib -> compared with the reference's oracles."""
+    import subprocess
+    from pathlib import Path
+    exe = Path(__file__).resolve().parents[1] / "oracle" / "_ref" / "ref_dropin_demo"
+    if not exe.exists():
+        pytest.skip("drop-in demo not built")
+    r = subprocess.run([str(exe), "50000", "2000000"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert " 0 mismatches" in r.stdout

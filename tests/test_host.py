@@ -220,3 +220,18 @@ def test_ref_oracle_fixture_generator_is_reproducible(ref):
             a, b = np.load(f), np.load(Path(d) / f.name)
             for k in a.files:
                 np.testing.assert_array_equal(a[k], b[k])
+
+
+def test_reference_dropin_without_gpu():
+    """A reference lpm6::FibTable handed to lpm6::gpu::Fib (oracle/ref_dropin_demo.cpp):
+    the host build matches the reference; without a GPU the lookup refuses (no fallback)."""
+    import subprocess
+    import torch
+    exe = ROOT / "oracle" / "_ref" / "ref_dropin_demo"
+    if not exe.exists():
+        pytest.skip("drop-in demo not built (reference sources absent at build time)")
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: covered by test_gpu_parity.py::test_reference_dropin")
+    r = subprocess.run([str(exe), "3000", "20000", "--no-gpu-ok"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "CudaError" in r.stdout
