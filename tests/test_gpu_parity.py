@@ -164,6 +164,46 @@ def test_c1_full_size(lpm, orc, cuda):
     assert mism == 0
 
 
+def _check_chunks(lpm, orc, cuda, workload, chunks, chunk):
+    torch = cuda
+    info = lpm.workload_info(workload)
+    fib = lpm.workload_fib(info.fib_kind)
+    imap = lpm.build_intervals(fib)
+    dev = lpm.Fib.build(fib)
+    gen = lpm.QueryGen(workload, fib)
+    d = torch.empty((chunk, 16), dtype=torch.uint8, device="cuda")
+    vdt = {1: np.uint8, 2: np.uint16, 4: np.uint32}[info.value_bytes]
+    mism = checked = 0
+    for c in chunks:
+        gen.run(c * chunk, chunk, d)
+        out = dev.lookup_batch(d)
+        host_addrs = d.cpu().numpy().view(np.uint64).reshape(-1, 2)
+        want = oracle_next_hops(orc, imap.boundaries, imap.next_hops, host_addrs)
+        got = out.cpu().numpy().view(vdt).astype(np.uint32)
+        mism += int(np.count_nonzero(got != want))
+        checked += chunk
+    return mism, checked
+
+
+def test_c2_full_size(lpm, orc, cuda):
+    """C2 at BASELINE size: 1,073,741,824 queries over the 1M-prefix FIB, every one checked."""
+    mism, checked = _check_chunks(lpm, orc, cuda, "C2", range(16), 1 << 26)
+    assert checked == 1 << 30 and mism == 0
+
+
+@pytest.mark.parametrize("workload", ["C3a", "C3b"])
+def test_c3_full_size(lpm, orc, cuda, workload):
+    """C3a (uniform) / C3b (Zipf 1.1) over the C1 FIB: all 268,435,456 queries."""
+    mism, checked = _check_chunks(lpm, orc, cuda, workload, range(4), 1 << 26)
+    assert checked == 1 << 28 and mism == 0
+
+
+def test_c4_chunks(lpm, orc, cuda):
+    """C4: first, middle and last of the 128 64M-address chunks (each seeded by its index)."""
+    mism, checked = _check_chunks(lpm, orc, cuda, "C4", [0, 63, 127], 1 << 26)
+    assert mism == 0
+
+
 def test_reference_dropin(cuda):
     """The reference's own FibTable -> lpm6::gpu::Fib -> compared with the reference's oracles."""
     import subprocess
