@@ -230,19 +230,29 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
                               : (F::kL - 4 * static_cast<int>(j)) > 4 ? 4u
                                                                       : static_cast<unsigned>(F::kL - 4 * j);
 
+  // Top 64 bits of query address (st, t, lane); the address stream comes from
+  // DRAM, so each warp loads the next tile's addresses one iteration ahead.
+  auto load_key = [&](unsigned long long st_, int t) -> unsigned long long {
+    const unsigned long long qi = (st_ * TILES + t) * 32ull + lane;
+    unsigned long long k = 0;
+    if (qi < p.n) {
+      const uint4 a = ld_stream_v4(p.addrs + qi, pol_stream);
+      k = (static_cast<unsigned long long>(a.w) << 32) | a.z;
+    }
+    return k;
+  };
+  unsigned long long next_key[TILES];
+#pragma unroll
+  for (int t = 0; t < TILES; ++t) next_key[t] = load_key(warp0, t);
+
   for (unsigned long long st = warp0; st * (32ull * TILES) < p.n; st += nwarps) {
     unsigned long long key[TILES];
     unsigned node[TILES];
 #pragma unroll
     for (int t = 0; t < TILES; ++t) {
-      const unsigned long long qi = (st * TILES + t) * 32ull + lane;
-      unsigned long long k = 0;
-      if (qi < p.n) {
-        const uint4 a = ld_stream_v4(p.addrs + qi, pol_stream);
-        k = (static_cast<unsigned long long>(a.w) << 32) | a.z;  // top 64 bits of the u128
-      }
-      key[t] = k > kMaxQueryKey ? kMaxQueryKey : k;  // types.hpp:25
+      key[t] = next_key[t] > kMaxQueryKey ? kMaxQueryKey : next_key[t];  // types.hpp:25
       node[t] = 0;
+      next_key[t] = load_key(st + nwarps, t);  // prefetch; consumed next iteration
     }
 
     // Phase A: this thread's own queries through the shared-memory levels.
