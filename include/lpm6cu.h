@@ -153,6 +153,13 @@ int lpm6cu_fib_set_kernel_config(lpm6cu_fib* fib, const lpm6cu_kernel_config* cf
 int lpm6cu_fib_kernel_config(const lpm6cu_fib* fib, lpm6cu_kernel_config* cfg);
 void lpm6cu_fib_destroy(lpm6cu_fib* fib);
 
+/* Checked mode: lookups run a bounds-checked kernel that never reads outside the
+ * tree and records violations (only a corrupted tree can cause one: bit 0 node
+ * index past a shared-memory level, bit 1 past an L2 level, bit 2 leaf rank 0). */
+int lpm6cu_fib_set_checked(lpm6cu_fib* fib, int on);
+/* OR of the violation bits since the last reset (synchronizes the device). */
+int lpm6cu_fib_violations(lpm6cu_fib* fib, uint32_t* bits, int reset);
+
 /* ---- lookup --------------------------------------------------------------- */
 
 /* n next hops for n addresses. With device pointers: one kernel launch on

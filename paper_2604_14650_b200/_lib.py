@@ -82,6 +82,8 @@ SIGNATURES = {
     "lpm6cu_fib_set_kernel_config": (I32, [P, C.POINTER(KernelConfig_t)]),
     "lpm6cu_fib_kernel_config": (I32, [P, C.POINTER(KernelConfig_t)]),
     "lpm6cu_fib_destroy": (None, [P]),
+    "lpm6cu_fib_set_checked": (I32, [P, I32]),
+    "lpm6cu_fib_violations": (I32, [P, C.POINTER(U32), I32]),
     "lpm6cu_lookup_batch": (I32, [P, P, U64, P, P]),
     "lpm6_workload_info_get": (I32, [I32, C.POINTER(WorkloadInfo_t)]),
     "lpm6_workload_fib": (I32, [I32, P, U64, C.POINTER(U64), C.POINTER(U32)]),

@@ -1,18 +1,17 @@
 // sm_100a batched LPM lookup kernel and the device half of the C ABI.
 //
 // One query = one predecessor search down the B200 tree (layout.hpp): internal
-// 128-byte lines of 16 separators, leaf lines of kL keys + kL next hops. The
-// kernel is the GPU form of the reference's search_batch (S:299-307,
-// P:812-847) over Listing 1's node search, in two phases per
-// 32-query warp tile (lane L owns query L):
+// 128-byte lines of 15 separators (arity 16), leaf lines of kL keys + kL next
+// hops. The kernel is the GPU form of the reference's search_batch
+// over Listing 1's node search, in two
+// phases per 32-query warp tile (lane L owns query L):
 //
-//  Phase A — top `smem_levels` levels, one thread per query. These levels are
-//    staged into shared memory once per CTA by cp.async.bulk (TMA bulk copy)
-//    on an mbarrier. Each thread ranks its own query in a 16-key node with a
-//    branch-free 5-probe binary search (count of keys <= q, i.e. Listing 1's
-//    popcnt(cmpge)). Upper levels are touched by every query, so a
-//    thread-per-query search here costs a fraction of a shared-memory
-//    wavefront per query per level instead of a full 128-byte line.
+//  Phase A — top `smem_levels` levels, one thread per query. A packed image of
+//    these levels is staged into shared memory once per CTA by cp.async.bulk
+//    (TMA bulk copy) on an mbarrier. Each thread ranks its own query in a node
+//    with a branch-free 4-probe binary search (count of keys <= q, i.e.
+//    Listing 1's popcnt(cmpge)), reading 8 bytes per probe instead of a whole
+//    128-byte node.
 //  Phase B — the remaining levels through L1/L2, four lanes per query: lane j of
 //    a 4-lane group loads bytes [32j, 32j+32) of the line with one 256-bit load,
 //    so a warp-wide load fetches exactly one full 128-byte line per query; the
@@ -26,9 +25,10 @@
 //    group's 4 next hops and writes them with one coalesced streaming store.
 //
 // Query addresses are read with coalesced 16-byte-stride loads of the top word
-// (L1::no_allocate, L2 evict_first) — each step streams GBs of addresses
-// through L2 while the tree stays resident (evict_last on tree lines). CTAs are
-// persistent (grid = SMs x resident CTAs) and stride over tiles.
+// (L1::no_allocate, L2 evict_first), one tile ahead of their use — each step
+// streams GBs of addresses through L2 while the tree stays resident
+// (evict_last on tree lines). CTAs are persistent (grid = SMs x resident CTAs,
+// default one 1024-thread CTA per SM) and stride over tiles.
 //
 // Results are the reference's: key = min(addr >> 64, 0xFFFF...FFFE)
 // (types.hpp:25), internal child = node * 16 + rank, leaf ordinal =
@@ -126,6 +126,8 @@ struct LookupParams {
   const unsigned long long* image;  // packed 15-key copy of internal levels 0.. (layout.hpp)
   unsigned int smem_levels;  // phase A levels [0, smem_levels), <= depth
   unsigned int smem_bytes;   // image bytes staged for those levels
+  unsigned long long level_nodes[LPM6CU_MAX_LEVELS];  // checked mode: node-index bounds
+  unsigned int* err;         // checked mode: OR of violation bits (1 smem level, 2 line level, 4 leaf rank)
 };
 
 // Count of the 15 separators of node n of a shared-memory image level that are
@@ -196,9 +198,13 @@ __device__ __forceinline__ void store_group(const LookupParams& p, unsigned long
 
 // TILES consecutive 32-query tiles per warp iteration (lane L owns query L of
 // each); MINB > 0 caps registers so that MINB CTAs of THREADS threads fit an SM.
-template <int DEPTH, int VB, int TILES, int THREADS, int MINB>
+// CHECKED adds bounds checks on every node index and leaf rank: a violation
+// (only possible with a corrupted tree) is clamped, never read out of bounds,
+// and reported through p.err — the fail-loudly mode the tests run.
+template <int DEPTH, int VB, int TILES, int THREADS, int MINB, bool CHECKED>
 __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const LookupParams p) {
   using F = LeafFmt<VB>;
+  unsigned violations = 0;
   constexpr int NS = 4 * TILES;  // queries in flight per 4-lane group
   extern __shared__ __align__(128) unsigned long long s_lines[];
   __shared__ __align__(8) uint64_t s_bar;
@@ -260,8 +266,13 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
     for (int l = 0; l < DEPTH; ++l)
       if (static_cast<unsigned>(l) < TA) {
 #pragma unroll
-        for (int t = 0; t < TILES; ++t)
+        for (int t = 0; t < TILES; ++t) {
           node[t] = node[t] * 16u + node_rank_smem(s_lines + (p.level_start[l] >> 4) * 15u, node[t], key[t]);
+          if (CHECKED && node[t] >= p.level_nodes[l + 1]) {
+            violations |= 1u;
+            node[t] = 0;
+          }
+        }
       }
 
     // Phase B: the group's queries, one 128-byte line per query per level.
@@ -281,12 +292,21 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
       // 32-bit word offsets (the layout keeps the array below 2^32 words): one
       // IMAD + one IMAD.WIDE per address.
       const unsigned base_w = static_cast<unsigned>(p.level_start[l]) + j * 4u;
+      if (CHECKED) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+          if (nd[s] >= p.level_nodes[l]) {
+            violations |= 2u;
+            nd[s] = 0;
+          }
+      }
 #pragma unroll
       for (int s = 0; s < NS; ++s) ld_line_quarter(p.lines + (base_w + nd[s] * 16u), w[s]);
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
         const unsigned r = group_rank(qk[s], w[s], l < DEPTH ? 4u : leaf_valid, gmask);
-        nd[s] = (l < DEPTH) ? nd[s] * 16u + r : r - 1u;  // leaf: ordinal within the line
+        if (CHECKED && l == DEPTH && r == 0) violations |= 4u;
+        nd[s] = (l < DEPTH) ? nd[s] * 16u + r : (CHECKED && r == 0 ? 0u : r - 1u);  // leaf: ordinal in line
       }
     }
 
@@ -301,40 +321,42 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
       }
     }
   }
+  if (CHECKED && violations) atomicOr(p.err, violations);
 }
 
 using KernelFn = void (*)(const LookupParams);
 
 // Instantiated shapes: (queries per lane, min CTAs per SM) for every depth and
 // value width; the tuning grid below is measured by bench.py --sweep.
-template <int VB, int TILES, int THREADS, int MINB>
+template <int VB, int TILES, int THREADS, int MINB, bool CHECKED>
 KernelFn pick_depth(int depth) {
   switch (depth) {
-    case 0: return lpm6_lookup_kernel<0, VB, TILES, THREADS, MINB>;
-    case 1: return lpm6_lookup_kernel<1, VB, TILES, THREADS, MINB>;
-    case 2: return lpm6_lookup_kernel<2, VB, TILES, THREADS, MINB>;
-    case 3: return lpm6_lookup_kernel<3, VB, TILES, THREADS, MINB>;
-    case 4: return lpm6_lookup_kernel<4, VB, TILES, THREADS, MINB>;
-    case 5: return lpm6_lookup_kernel<5, VB, TILES, THREADS, MINB>;
-    case 6: return lpm6_lookup_kernel<6, VB, TILES, THREADS, MINB>;
-    case 7: return lpm6_lookup_kernel<7, VB, TILES, THREADS, MINB>;
+    case 0: return lpm6_lookup_kernel<0, VB, TILES, THREADS, MINB, CHECKED>;
+    case 1: return lpm6_lookup_kernel<1, VB, TILES, THREADS, MINB, CHECKED>;
+    case 2: return lpm6_lookup_kernel<2, VB, TILES, THREADS, MINB, CHECKED>;
+    case 3: return lpm6_lookup_kernel<3, VB, TILES, THREADS, MINB, CHECKED>;
+    case 4: return lpm6_lookup_kernel<4, VB, TILES, THREADS, MINB, CHECKED>;
+    case 5: return lpm6_lookup_kernel<5, VB, TILES, THREADS, MINB, CHECKED>;
+    case 6: return lpm6_lookup_kernel<6, VB, TILES, THREADS, MINB, CHECKED>;
+    case 7: return lpm6_lookup_kernel<7, VB, TILES, THREADS, MINB, CHECKED>;
     default: return nullptr;
   }
 }
 
-template <int TILES, int THREADS, int MINB>
+template <int TILES, int THREADS, int MINB, bool CHECKED = false>
 KernelFn pick_vb(int vb, int depth) {
   switch (vb) {
-    case 1: return pick_depth<1, TILES, THREADS, MINB>(depth);
-    case 2: return pick_depth<2, TILES, THREADS, MINB>(depth);
-    case 4: return pick_depth<4, TILES, THREADS, MINB>(depth);
+    case 1: return pick_depth<1, TILES, THREADS, MINB, CHECKED>(depth);
+    case 2: return pick_depth<2, TILES, THREADS, MINB, CHECKED>(depth);
+    case 4: return pick_depth<4, TILES, THREADS, MINB, CHECKED>(depth);
     default: return nullptr;
   }
 }
 
 // Instantiated shapes (queries per lane, threads per CTA, min CTAs per SM);
-// bench.py --sweep measures them.
-KernelFn pick_kernel(int vb, int depth, int tiles, int threads, int minb) {
+// bench.py --sweep measures them. The checked variant exists for the default shape.
+KernelFn pick_kernel(int vb, int depth, int tiles, int threads, int minb, bool checked = false) {
+  if (checked) return (tiles == 1 && threads == 1024 && minb == 1) ? pick_vb<1, 1024, 1, true>(vb, depth) : nullptr;
   if (tiles == 1 && threads == 256 && minb == 0) return pick_vb<1, 256, 0>(vb, depth);
   if (tiles == 1 && threads == 256 && minb == 4) return pick_vb<1, 256, 4>(vb, depth);
   if (tiles == 2 && threads == 256 && minb == 0) return pick_vb<2, 256, 0>(vb, depth);
@@ -384,6 +406,7 @@ struct lpm6cu_fib {
   int device = 0;
   lpm6cu_geometry g{};
   unsigned long long* d_lines = nullptr;
+  unsigned int* d_err = nullptr;  // non-null: checked mode (bounds-checked kernel)
   bool owns = true;
   lpm6cu_kernel_config cfg{};  // resolved
   int num_sms = 0;
@@ -404,6 +427,7 @@ struct lpm6cu_fib {
       if (pipe->start) cudaEventDestroy(pipe->start);
     }
     if (owns && d_lines) cudaFree(d_lines);
+    if (d_err) cudaFree(d_err);
     if (prev >= 0) cudaSetDevice(prev);
   }
 };
@@ -480,7 +504,7 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_addrs, unsigned long long 
   if (n == 0) return;
   KernelFn fn = pick_kernel(static_cast<int>(f->g.value_bytes), static_cast<int>(f->g.depth),
                             static_cast<int>(f->cfg.queries_per_lane), static_cast<int>(f->cfg.threads_per_cta),
-                            static_cast<int>(f->cfg.min_ctas_per_sm));
+                            static_cast<int>(f->cfg.min_ctas_per_sm), f->d_err != nullptr);
   if (!fn) throw Error(Errc::InvalidArgument, "no kernel instantiated for this configuration");
   LookupParams p{};
   p.lines = f->d_lines;
@@ -491,6 +515,8 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_addrs, unsigned long long 
   p.smem_bytes = static_cast<unsigned>(staged_bytes(f));
   p.smem_levels = f->cfg.smem_levels;
   p.image = f->d_lines + f->g.image_start;
+  for (int l = 0; l < LPM6CU_MAX_LEVELS; ++l) p.level_nodes[l] = f->g.level_nodes[l];
+  p.err = f->d_err;
   const int threads = static_cast<int>(f->cfg.threads_per_cta);
   const size_t smem = p.smem_bytes;
   if (smem > 48 * 1024)
@@ -641,6 +667,33 @@ int lpm6cu_fib_kernel_config(const lpm6cu_fib* f, lpm6cu_kernel_config* cfg) {
 }
 
 void lpm6cu_fib_destroy(lpm6cu_fib* f) { delete f; }
+
+int lpm6cu_fib_set_checked(lpm6cu_fib* f, int on) {
+  return guard([&] {
+    if (!f) throw Error(Errc::InvalidArgument, "NULL fib");
+    DeviceGuard dg(f->device);
+    if (on && !f->d_err) {
+      check_cuda(cudaMalloc(&f->d_err, sizeof(unsigned)), "cudaMalloc err");
+      check_cuda(cudaMemset(f->d_err, 0, sizeof(unsigned)), "memset err");
+    } else if (!on && f->d_err) {
+      check_cuda(cudaFree(f->d_err), "cudaFree err");
+      f->d_err = nullptr;
+    }
+  });
+}
+
+int lpm6cu_fib_violations(lpm6cu_fib* f, uint32_t* bits, int reset) {
+  return guard([&] {
+    if (!f || !bits) throw Error(Errc::InvalidArgument, "NULL argument");
+    *bits = 0;
+    if (!f->d_err) return;
+    DeviceGuard dg(f->device);
+    unsigned v = 0;
+    check_cuda(cudaMemcpy(&v, f->d_err, sizeof v, cudaMemcpyDeviceToHost), "read err");  // syncs the device
+    *bits = v;
+    if (reset) check_cuda(cudaMemset(f->d_err, 0, sizeof(unsigned)), "reset err");
+  });
+}
 
 int lpm6cu_lookup_batch(const lpm6cu_fib* fib, const void* addrs, uint64_t n, void* out, void* stream) {
   return guard([&] {

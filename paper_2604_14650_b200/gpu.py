@@ -123,6 +123,16 @@ class Fib:
         check(lib().lpm6cu_fib_set_kernel_config(self._h, C.byref(c)))
         return self.kernel_config()
 
+    def set_checked(self, on: bool = True) -> None:
+        """Bounds-checked kernel: never reads outside the tree, records violations."""
+        check(lib().lpm6cu_fib_set_checked(self._h, int(on)))
+
+    def violations(self, reset: bool = True) -> int:
+        """OR of violation bits since the last reset (1 smem level, 2 L2 level, 4 leaf rank)."""
+        v = C.c_uint32(0)
+        check(lib().lpm6cu_fib_violations(self._h, C.byref(v), int(reset)))
+        return v.value
+
     # -- lookup ---------------------------------------------------------------
     def lookup_batch(self, addrs, out=None, stream=None):
         """Next hops of n 16-byte little-endian u128 addresses.

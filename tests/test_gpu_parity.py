@@ -40,10 +40,15 @@ def check_fib(lpm, orc, cuda, fib, addrs, lanes=LANES, smem_levels=(None, 0, 1, 
             if t is not None and t > dev.geometry.depth:
                 continue
             dev.set_kernel_config(lanes_per_query=g, smem_levels=t)
-            got = run_lookup(cuda, dev, addrs).astype(np.uint32)
-            bad = np.nonzero(got != want)[0]
-            assert len(bad) == 0, (f"G={g} T={t}: {len(bad)} mismatches, first key "
-                                   f"{int(addrs[bad[0], 1]):#x} want {want[bad[0]]} got {got[bad[0]]}")
+            for checked in (False, True):
+                dev.set_checked(checked)
+                got = run_lookup(cuda, dev, addrs).astype(np.uint32)
+                bad = np.nonzero(got != want)[0]
+                assert len(bad) == 0, (f"G={g} T={t} checked={checked}: {len(bad)} mismatches, first key "
+                                       f"{int(addrs[bad[0], 1]):#x} want {want[bad[0]]} got {got[bad[0]]}")
+                if checked:
+                    assert dev.violations() == 0
+    dev.set_checked(False)
     return dev, want
 
 
@@ -142,6 +147,29 @@ def test_corrupted_device_fib_is_detected(lpm, orc, cuda):
     assert got[0] != want[0]
     ok = lpm.Fib.from_tree(tree)
     assert run_lookup(cuda, ok, probe).astype(np.uint32)[0] == want[0]
+
+
+def test_checked_mode_flags_corrupted_tree(lpm, orc, cuda):
+    """A tree whose root routes past the end of level 1 is caught (no out-of-bounds read)."""
+    torch = cuda
+    fib = lpm.workload_fib(1)
+    tree = lpm.build_tree(lpm.build_intervals(fib))
+    g = tree.geometry
+    lines = tree.lines.copy()
+    lines[0:15] = 0                                   # every root separator <= every query: rank 15
+    img = g.image_start                               # and its shared-memory copy
+    lines[img: img + 15] = 0
+    dev = lpm.Fib.wrap_device(g, torch.from_numpy(lines.view(np.int64)).cuda(), 0)
+    dev.set_checked(True)
+    addrs = addrs_from_keys(np.arange(1, 4097, dtype=np.uint64) << np.uint64(50))
+    for t in (None, 0):                               # shared-memory and L2 descents
+        dev.set_kernel_config(smem_levels=t)
+        run_lookup(cuda, dev, addrs)
+        assert dev.violations() & 3
+    good = lpm.Fib.from_tree(tree)
+    good.set_checked(True)
+    run_lookup(cuda, good, addrs)
+    assert good.violations() == 0
 
 
 def test_c1_full_size(lpm, orc, cuda):
