@@ -142,6 +142,20 @@ def hbm_peak():
     return HBM_FALLBACK_GBS, "B200_PROFILING.md fallback"
 
 
+def device_build_ms(lpm, fib, device, vb, reps=3):
+    """Wall time of the GPU FIB build (rules on the host -> ready device FIB), best of reps."""
+    import torch
+    lpm.Fib.build_device(fib, device, value_bytes=vb).close()  # warm-up (module load, allocator)
+    best = float("inf")
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        lpm.Fib.build_device(fib, device, value_bytes=vb).close()
+        torch.cuda.synchronize()
+        best = min(best, (time.perf_counter() - t0) * 1e3)
+    return best
+
+
 def measured_traffic(workload, n):
     """DRAM bytes per lookup launch of n queries, scaled from the committed ncu capture
     (profiles/r01_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum of one launch)."""
@@ -356,7 +370,8 @@ def run_chunked(args, lpm, dispatch, fdev, fib, info, geom, cfg, ws, rank, dev_i
         "cpu_baseline": None, "e2e": None,
         "gpu_launches": 2 * nc * args.steps,
         "clocks": clk.summary(), "parity_sample": parity,
-        "fib_build_ms": build_ms, "fib_broadcast_ms": bcast_ms, "step_ms": step_ms,
+        "fib_build_ms": build_ms, "fib_build_device_ms": device_build_ms(lpm, fib, dev_index, vb),
+        "fib_broadcast_ms": bcast_ms, "step_ms": step_ms,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
@@ -561,6 +576,7 @@ def main():
         "clocks": clk.summary(),
         "parity_sample": parity,
         "fib_build_ms": build_ms,
+        "fib_build_device_ms": device_build_ms(lpm, fib, dev_index, vb),
         "fib_broadcast_ms": bcast_ms,
         "step_ms": step_ms,
     }

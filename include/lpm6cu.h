@@ -140,6 +140,18 @@ int lpm6_parse_prefix(const char* text, lpm6cu_prefix* out, int* host_bits_maske
 int lpm6cu_fib_build(int device, const lpm6cu_prefix* rules, uint64_t n, uint32_t default_next_hop,
                      const lpm6cu_build_opts* opts, lpm6cu_fib** out);
 
+/* The same build done entirely on the GPU: rules (host or device
+ * memory) -> intervals -> layout, bit-identical to lpm6cu_fib_build. Stream-ordered
+ * on `stream`; returns when the FIB is ready. */
+int lpm6cu_fib_build_device(int device, const lpm6cu_prefix* rules, uint64_t n, uint32_t default_next_hop,
+                            const lpm6cu_build_opts* opts, void* stream, lpm6cu_fib** out);
+
+/* Device-built intervals copied to host arrays (capacity >= 2n+1), for checking
+ * against lpm6_build_intervals and the reference. */
+int lpm6cu_build_intervals_device(int device, const lpm6cu_prefix* rules, uint64_t n, uint32_t default_next_hop,
+                                  int merge_adjacent, uint64_t* boundaries, uint32_t* next_hops,
+                                  uint64_t capacity, uint64_t* m_out);
+
 /* From a host layout (lpm6_build_tree output); copies into device memory it owns. */
 int lpm6cu_fib_create(int device, const lpm6cu_geometry* g, const uint64_t* lines, lpm6cu_fib** out);
 
@@ -149,6 +161,8 @@ int lpm6cu_fib_wrap_device(int device, const lpm6cu_geometry* g, const void* d_l
 
 int lpm6cu_fib_geometry(const lpm6cu_fib* fib, lpm6cu_geometry* g);
 int lpm6cu_fib_device_lines(const lpm6cu_fib* fib, const void** d_lines);
+/* Copy the device line array (g.total_words u64 words) to host memory. */
+int lpm6cu_fib_copy_lines(const lpm6cu_fib* fib, uint64_t* host_lines, uint64_t words);
 int lpm6cu_fib_set_kernel_config(lpm6cu_fib* fib, const lpm6cu_kernel_config* cfg);
 int lpm6cu_fib_kernel_config(const lpm6cu_fib* fib, lpm6cu_kernel_config* cfg);
 void lpm6cu_fib_destroy(lpm6cu_fib* fib);

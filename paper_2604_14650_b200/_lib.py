@@ -75,10 +75,13 @@ SIGNATURES = {
     "lpm6_build_tree": (I32, [P, P, U64, U32, U32, C.POINTER(Geometry_t), P, P]),
     "lpm6_parse_prefix": (I32, [C.c_char_p, C.POINTER(Prefix_t), C.POINTER(I32)]),
     "lpm6cu_fib_build": (I32, [I32, P, U64, U32, C.POINTER(BuildOpts_t), C.POINTER(P)]),
+    "lpm6cu_fib_build_device": (I32, [I32, P, U64, U32, C.POINTER(BuildOpts_t), P, C.POINTER(P)]),
+    "lpm6cu_build_intervals_device": (I32, [I32, P, U64, U32, I32, P, P, U64, C.POINTER(U64)]),
     "lpm6cu_fib_create": (I32, [I32, C.POINTER(Geometry_t), P, C.POINTER(P)]),
     "lpm6cu_fib_wrap_device": (I32, [I32, C.POINTER(Geometry_t), P, C.POINTER(P)]),
     "lpm6cu_fib_geometry": (I32, [P, C.POINTER(Geometry_t)]),
     "lpm6cu_fib_device_lines": (I32, [P, C.POINTER(P)]),
+    "lpm6cu_fib_copy_lines": (I32, [P, P, U64]),
     "lpm6cu_fib_set_kernel_config": (I32, [P, C.POINTER(KernelConfig_t)]),
     "lpm6cu_fib_kernel_config": (I32, [P, C.POINTER(KernelConfig_t)]),
     "lpm6cu_fib_destroy": (None, [P]),

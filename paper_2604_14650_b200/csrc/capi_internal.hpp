@@ -3,6 +3,8 @@
 
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "capi_util.hpp"
 #include "lpm6/fib.hpp"
 #include "lpm6/layout.hpp"
@@ -14,5 +16,9 @@ std::vector<Prefix> to_prefixes(const lpm6cu_prefix* rules, uint64_t n);
 void export_geometry(const TreeLayout& t, lpm6cu_geometry* g);
 Tree build_device_tree(const lpm6cu_prefix* rules, uint64_t n, uint32_t default_nh,
                        const lpm6cu_build_opts* opts);
+
+// Device-side build (build.cu): returns a cudaMalloc'ed line array and its geometry.
+void* device_build_tree(const lpm6cu_prefix* rules, uint64_t n, uint32_t default_nh, const lpm6cu_build_opts* opts,
+                        cudaStream_t s, lpm6cu_geometry* geom);
 
 }  // namespace lpm6::capi

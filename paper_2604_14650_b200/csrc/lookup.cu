@@ -638,6 +638,35 @@ int lpm6cu_fib_build(int device, const lpm6cu_prefix* rules, uint64_t n, uint32_
   });
 }
 
+int lpm6cu_fib_copy_lines(const lpm6cu_fib* f, uint64_t* host_lines, uint64_t words) {
+  return guard([&] {
+    if (!f || !host_lines) throw Error(Errc::InvalidArgument, "NULL argument");
+    if (words != f->g.total_words) throw Error(Errc::InvalidArgument, "words must equal geometry.total_words");
+    DeviceGuard dg(f->device);
+    check_cuda(cudaMemcpy(host_lines, f->d_lines, words * 8, cudaMemcpyDeviceToHost), "copy lines");
+  });
+}
+
+int lpm6cu_fib_build_device(int device, const lpm6cu_prefix* rules, uint64_t n, uint32_t default_nh,
+                            const lpm6cu_build_opts* opts, void* stream, lpm6cu_fib** out) {
+  return guard([&] {
+    if (n > 0 && !rules) throw Error(Errc::InvalidArgument, "rules is NULL");
+    if (!out) throw Error(Errc::InvalidArgument, "NULL out");
+    DeviceGuard dg(device);
+    lpm6cu_geometry g;
+    void* lines = capi::device_build_tree(rules, n, default_nh, opts, static_cast<cudaStream_t>(stream), &g);
+    std::unique_ptr<lpm6cu_fib> f;
+    try {
+      f.reset(new_fib(device, &g));
+    } catch (...) {
+      cudaFree(lines);
+      throw;
+    }
+    f->d_lines = static_cast<unsigned long long*>(lines);
+    *out = f.release();
+  });
+}
+
 int lpm6cu_fib_geometry(const lpm6cu_fib* f, lpm6cu_geometry* g) {
   return guard([&] {
     if (!f || !g) throw Error(Errc::InvalidArgument, "NULL argument");

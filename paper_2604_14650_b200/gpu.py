@@ -65,6 +65,18 @@ class Fib:
         return cls(h.value, device)
 
     @classmethod
+    def build_device(cls, fib: FibTable, device: int = 0, merge_adjacent: bool = True, value_bytes: int = 0,
+                     stream=None) -> "Fib":
+        """The same build done on the GPU (csrc/build.cu); bit-identical layout."""
+        h = C.c_void_p()
+        opts = build_opts(merge_adjacent, value_bytes)
+        rules = fib.rules
+        s = _stream_handle(stream)
+        check(lib().lpm6cu_fib_build_device(device, _rules_ptr(rules), len(rules), fib.default_next_hop,
+                                            C.byref(opts), s, C.byref(h)))
+        return cls(h.value, device)
+
+    @classmethod
     def from_tree(cls, tree: Tree, device: int = 0) -> "Fib":
         h = C.c_void_p()
         g = tree.geometry.to_c()
@@ -192,6 +204,27 @@ class QueryGen:
             self.close()
         except Exception:
             pass
+
+
+def build_intervals_device(fib: FibTable, device: int = 0, merge_adjacent: bool = True):
+    """Elementary intervals computed on the GPU (csrc/build.cu), returned as an IntervalMap."""
+    from .fib import IntervalMap
+    rules = fib.rules
+    cap = 2 * len(rules) + 1
+    b = np.empty(cap, np.uint64)
+    nh = np.empty(cap, np.uint32)
+    m = C.c_uint64(0)
+    check(lib().lpm6cu_build_intervals_device(device, _rules_ptr(rules), len(rules), fib.default_next_hop,
+                                              int(merge_adjacent), b.ctypes.data, nh.ctypes.data, cap, C.byref(m)))
+    return IntervalMap(b[: m.value].copy(), nh[: m.value].copy(), fib.default_next_hop)
+
+
+def device_lines(fib_dev: "Fib") -> np.ndarray:
+    """Host copy of a device FIB's line array (for bit-exact layout comparisons)."""
+    g = fib_dev.geometry
+    out = np.empty(g.total_words, np.uint64)
+    check(lib().lpm6cu_fib_copy_lines(fib_dev._h, out.ctypes.data, g.total_words))
+    return out
 
 
 def probe_l2_gather(device: int, buffer_bytes: int, line_bytes: int = 128) -> float:
