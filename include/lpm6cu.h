@@ -184,6 +184,86 @@ int lpm6cu_fib_violations(lpm6cu_fib* fib, uint32_t* bits, int reset);
 int lpm6cu_lookup_batch(const lpm6cu_fib* fib, const void* addrs, uint64_t n, void* out,
                         void* stream);
 
+/* ---- rebuild-and-swap FIB store (SPEC update-engine) ---
+ *
+ * Replaces the reference's FibStore: route changes are staged,
+ * commit rebuilds the whole FIB on the GPU (lpm6cu_fib_build_device, off the
+ * lookup streams) and publishes it with one pointer swap; readers pin a snapshot
+ * with acquire/release and never wait for a commit. Release is stream-ordered:
+ * it records an event on the reader's stream, and a retired snapshot's device
+ * memory is freed only after its last release AND every lookup queued before
+ * those releases has finished on the device. */
+
+enum {
+  LPM6_UPDATE_INSERT = 0,   /* must not exist (DuplicatePrefix) */
+  LPM6_UPDATE_DELETE = 1,   /* must exist (UnknownPrefix); next_hop ignored */
+  LPM6_UPDATE_MODIFY = 2,   /* must exist (UnknownPrefix) */
+  LPM6_UPDATE_ANNOUNCE = 3, /* insert-or-modify: the trace's "A" line */
+};
+
+/* lpm6::UpdateOp; 48 bytes. */
+typedef struct {
+  uint32_t kind;
+  uint32_t reserved0;
+  uint64_t reserved1;
+  lpm6cu_prefix prefix;
+} lpm6_update_op;
+
+typedef struct {
+  uint64_t epoch;         /* active snapshot's epoch: 1 after create, +1 per effective commit */
+  uint64_t pending_ops;   /* staged, not yet committed */
+  uint64_t active_rules;  /* rules in the active snapshot */
+  uint64_t retired;       /* snapshots replaced but not yet reclaimed */
+  uint64_t reclaimed;     /* snapshots whose device memory was freed */
+  uint64_t commits;       /* effective commits */
+  double last_build_ms;   /* wall time of the last device rebuild */
+  double last_publish_us; /* time the active-pointer swap was held */
+} lpm6cu_store_stats;
+
+typedef struct lpm6cu_store lpm6cu_store;
+typedef struct lpm6cu_snapshot lpm6cu_snapshot;
+
+/* Parse one update-trace line "A <ipv6>/<len> <next_hop>" | "W <ipv6>/<len> [next_hop]". */
+int lpm6_parse_update(const char* line, lpm6_update_op* op);
+
+/* The store's staging rule on host arrays (no GPU): apply ops in order to the rule
+ * set `rules` (n entries); op_status[i] (optional) receives 0 or the status of op i,
+ * invalid ops are skipped. The resulting rules go to out (capacity cap; order is
+ * the store's, not sorted) and *out_n; *staged counts the applied ops. */
+int lpm6_apply_updates(const lpm6cu_prefix* rules, uint64_t n, const lpm6_update_op* ops, uint64_t n_ops,
+                       lpm6cu_prefix* out, uint64_t cap, uint64_t* out_n, uint64_t* staged, int32_t* op_status);
+
+/* Epoch 1 = rules built on `device`. opts as lpm6cu_fib_build (value_bytes 0 =
+ * re-derived at every commit). */
+int lpm6cu_store_create(int device, const lpm6cu_prefix* rules, uint64_t n, uint32_t default_next_hop,
+                        const lpm6cu_build_opts* opts, lpm6cu_store** out);
+/* Waits for every outstanding release fence; fails (InvalidArgument) while a
+ * snapshot is still acquired. */
+int lpm6cu_store_destroy(lpm6cu_store* store);
+/* Validate and append ops (any thread). Invalid ops are skipped and reported in
+ * op_status (optional, n entries: 0 or a status); *staged = ops appended. */
+int lpm6cu_store_stage(lpm6cu_store* store, const lpm6_update_op* ops, uint64_t n, uint64_t* staged,
+                       int32_t* op_status);
+/* Rebuild from the staged view and publish (one committer at a time). Empty
+ * pending: no-op. On failure (e.g. SentinelCollision) the old snapshot stays
+ * active and the pending ops stay staged. *epoch (optional) = active epoch. */
+int lpm6cu_store_commit(lpm6cu_store* store, uint64_t* epoch);
+/* Pin the current snapshot. */
+int lpm6cu_store_acquire(lpm6cu_store* store, lpm6cu_snapshot** snap);
+/* Unpin. Work already queued on `stream` (cudaStream_t, NULL = legacy default)
+ * that uses the snapshot keeps it alive until it finishes on the device. */
+int lpm6cu_store_release(lpm6cu_snapshot* snap, void* stream);
+/* The snapshot's epoch, device FIB (for lpm6cu_lookup_batch) and rule count. */
+int lpm6cu_snapshot_info(const lpm6cu_snapshot* snap, uint64_t* epoch, const lpm6cu_fib** fib, uint64_t* n_rules);
+/* Copy the snapshot's rules (n_rules entries, store order). */
+int lpm6cu_snapshot_rules(const lpm6cu_snapshot* snap, lpm6cu_prefix* out, uint64_t cap);
+/* acquire -> lpm6cu_lookup_batch -> release(stream) in one call. */
+int lpm6cu_store_lookup_batch(lpm6cu_store* store, const void* addrs, uint64_t n, void* out, void* stream,
+                              uint64_t* epoch);
+/* Free retired snapshots whose fences have completed (non-blocking). */
+int lpm6cu_store_reclaim(lpm6cu_store* store);
+int lpm6cu_store_stats_get(lpm6cu_store* store, lpm6cu_store_stats* stats);
+
 /* ---- synthetic workloads C0..C4 (BASELINE.json configs) ---------------------- */
 
 typedef struct {

@@ -8,9 +8,11 @@ from ._lib import Lpm6Error
 from .fib import (FibTable, Geometry, IntervalMap, Prefix, Tree, WORKLOADS, build_intervals, build_tree, load_fib,
                   parse_prefix, plan_layout, workload_fib, workload_info, workload_queries_host)
 from .gpu import Fib, QueryGen, probe_l2_gather, probe_smem
+from .store import FibStore, Snapshot, UpdateOp, apply_updates, load_update_trace, parse_update
 
 __all__ = [
     "Lpm6Error", "FibTable", "Geometry", "IntervalMap", "Prefix", "Tree", "WORKLOADS", "build_intervals",
     "build_tree", "load_fib", "parse_prefix", "plan_layout", "workload_fib", "workload_info",
-    "workload_queries_host", "Fib", "QueryGen", "probe_l2_gather", "probe_smem",
+    "workload_queries_host", "Fib", "QueryGen", "probe_l2_gather", "probe_smem", "FibStore", "Snapshot",
+    "UpdateOp", "apply_updates", "load_update_trace", "parse_update",
 ]

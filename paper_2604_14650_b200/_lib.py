@@ -60,6 +60,16 @@ class WorkloadInfo_t(C.Structure):
                 ("value_bytes", C.c_uint32), ("reserved", C.c_uint32), ("name", C.c_char * 8)]
 
 
+class UpdateOp_t(C.Structure):
+    _fields_ = [("kind", C.c_uint32), ("reserved0", C.c_uint32), ("reserved1", C.c_uint64), ("prefix", Prefix_t)]
+
+
+class StoreStats_t(C.Structure):
+    _fields_ = [("epoch", C.c_uint64), ("pending_ops", C.c_uint64), ("active_rules", C.c_uint64),
+                ("retired", C.c_uint64), ("reclaimed", C.c_uint64), ("commits", C.c_uint64),
+                ("last_build_ms", C.c_double), ("last_publish_us", C.c_double)]
+
+
 P = C.c_void_p
 U64 = C.c_uint64
 U32 = C.c_uint32
@@ -96,6 +106,19 @@ SIGNATURES = {
     "lpm6cu_querygen_destroy": (None, [P]),
     "lpm6cu_probe_l2_gather": (I32, [I32, U64, U32, C.POINTER(C.c_double)]),
     "lpm6cu_probe_smem": (I32, [I32, C.POINTER(C.c_double)]),
+    "lpm6_parse_update": (I32, [C.c_char_p, C.POINTER(UpdateOp_t)]),
+    "lpm6_apply_updates": (I32, [P, U64, P, U64, P, U64, C.POINTER(U64), C.POINTER(U64), P]),
+    "lpm6cu_store_create": (I32, [I32, P, U64, U32, C.POINTER(BuildOpts_t), C.POINTER(P)]),
+    "lpm6cu_store_destroy": (I32, [P]),
+    "lpm6cu_store_stage": (I32, [P, P, U64, C.POINTER(U64), P]),
+    "lpm6cu_store_commit": (I32, [P, C.POINTER(U64)]),
+    "lpm6cu_store_acquire": (I32, [P, C.POINTER(P)]),
+    "lpm6cu_store_release": (I32, [P, P]),
+    "lpm6cu_snapshot_info": (I32, [P, C.POINTER(U64), C.POINTER(P), C.POINTER(U64)]),
+    "lpm6cu_snapshot_rules": (I32, [P, P, U64]),
+    "lpm6cu_store_lookup_batch": (I32, [P, P, U64, P, P, C.POINTER(U64)]),
+    "lpm6cu_store_reclaim": (I32, [P]),
+    "lpm6cu_store_stats_get": (I32, [P, C.POINTER(StoreStats_t)]),
 }
 
 _lib = None

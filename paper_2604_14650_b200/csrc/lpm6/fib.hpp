@@ -64,7 +64,9 @@ class FibTable {
   void insert(const Prefix& p);             // throws DuplicatePrefix / ReservedNextHop
   bool insert_or_replace(const Prefix& p);  // true when an existing rule was overwritten
   void erase(u128 value, int length);       // throws UnknownPrefix
+  void modify(u128 value, int length, u32 next_hop);  // throws ReservedNextHop / UnknownPrefix
   const Prefix* find(u128 value, int length) const;
+  bool contains(u128 value, int length) const { return find(value, length) != nullptr; }
 
  private:
   struct KeyHash {

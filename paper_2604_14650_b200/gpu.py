@@ -49,10 +49,11 @@ def _ptr_len(buf, item: int) -> tuple[int, int, bool]:
 class Fib:
     """An immutable FIB resident in one GPU's HBM (lpm6cu_fib)."""
 
-    def __init__(self, handle: int, device: int, keepalive=None):
+    def __init__(self, handle: int, device: int, keepalive=None, owned: bool = True):
         self._h = C.c_void_p(handle)
         self.device = device
         self._keepalive = keepalive
+        self._owned = owned  # False: a store snapshot's FIB, freed by the store
 
     # -- construction ---------------------------------------------------------
     @classmethod
@@ -94,7 +95,8 @@ class Fib:
 
     def close(self) -> None:
         if self._h and self._h.value:
-            lib().lpm6cu_fib_destroy(self._h)
+            if self._owned:
+                lib().lpm6cu_fib_destroy(self._h)
             self._h = C.c_void_p()
 
     def __del__(self):

@@ -1,0 +1,300 @@
+"""Rebuild-and-swap FIB store on the GPU (csrc/store.cpp; SPEC update-engine S:341-404).
+
+Every post-commit lookup is compared bit-exactly with the CPU oracle of the
+FIB the host staging oracle (oracle/update_oracle.py) predicts for that epoch.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+from _util import addrs_from_keys, boundary_probe_keys, random_fib_rules
+
+pytestmark = pytest.mark.gpu
+
+MASK64 = (1 << 64) - 1
+
+
+def expected(lpm, orc, fib, addrs):
+    st, b, nh = orc.build_intervals(fib.rules, fib.default_next_hop)
+    assert st == 0
+    out, _ = orc.lookup_batch(0, b, nh, addrs, threads=8)
+    return out
+
+
+def probe_addrs(lpm, fib, rng, n_random=4096):
+    imap = lpm.build_intervals(fib)
+    keys = np.concatenate([boundary_probe_keys(imap.boundaries), rng.integers(0, 2**64, n_random, dtype=np.uint64)])
+    return addrs_from_keys(keys, rng)
+
+
+def lookup(cuda, snap_or_store, addrs):
+    torch = cuda
+    a = torch.from_numpy(addrs.view(np.uint8).reshape(-1, 16)).cuda()
+    out = snap_or_store.lookup_batch(a)
+    if isinstance(out, tuple):
+        out = out[0]
+    torch.cuda.synchronize()
+    return out.cpu().numpy().view({1: np.uint8, 2: np.uint16, 4: np.uint32}[out.element_size()]).astype(np.uint32)
+
+
+def random_ops(st, rng, fib, n, new_p=0.4):
+    from paper_2604_14650_b200.fib import Prefix
+    existing = [(int(r["value_hi"]) << 64, int(r["length"])) for r in fib.rules]
+    ops = []
+    for _ in range(n):
+        if existing and rng.random() > new_p:
+            v, ln = existing[int(rng.integers(0, len(existing)))]
+            kind = int(rng.choice([st.DELETE, st.MODIFY, st.ANNOUNCE]))
+        else:
+            ln = int(rng.integers(16, 65))
+            top = int(rng.integers(0, 2**63)) << 1
+            top &= (MASK64 << (64 - ln)) & MASK64
+            if top == 0 or top + (1 << (64 - ln)) >= MASK64:
+                continue
+            v, kind = top << 64, int(rng.choice([st.INSERT, st.ANNOUNCE]))
+        ops.append(st.UpdateOp(kind, Prefix(v, ln, int(rng.integers(1, 256)))))
+    return ops
+
+
+@pytest.fixture(scope="module")
+def st():
+    from paper_2604_14650_b200 import store
+    return store
+
+
+def test_store_epochs_and_lookups(lpm, orc, cuda, st):
+    rng = np.random.default_rng(1)
+    fib = lpm.workload_fib(0)
+    store = st.FibStore(fib)
+    assert store.epoch == 1 and store.stats.active_rules == len(fib)
+    addrs = probe_addrs(lpm, fib, rng)
+    np.testing.assert_array_equal(lookup(cuda, store, addrs), expected(lpm, orc, fib, addrs))
+    assert store.commit() == 1  # empty pending: same epoch, same handle
+    view = fib
+    for epoch in range(2, 7):
+        ops = random_ops(st, rng, view, 200)
+        staged, errs = store.stage(ops)
+        view, want_staged, want_errs = st.apply_updates(view, ops)
+        assert (staged, errs) == (want_staged, want_errs)
+        assert store.stats.pending_ops == staged
+        assert store.commit() == epoch
+        assert store.stats.pending_ops == 0
+        with store.acquire() as snap:
+            assert snap.epoch == epoch and snap.num_rules == len(view)
+            got_rules = sorted(map(tuple, snap.rules()[["value_hi", "length", "next_hop"]].tolist()))
+            assert got_rules == sorted(map(tuple, view.rules[["value_hi", "length", "next_hop"]].tolist()))
+        addrs = probe_addrs(lpm, view, rng)
+        np.testing.assert_array_equal(lookup(cuda, store, addrs), expected(lpm, orc, view, addrs))
+    s = store.stats
+    assert s.commits == 5 and s.retired == 0 and s.reclaimed == 5 and s.last_build_ms > 0
+    store.close()
+
+
+def test_commit_failure_keeps_old_snapshot_and_pending(lpm, orc, cuda, st):
+    """Rebuild failure (sentinel collision) leaves the old snapshot active and pending intact."""
+    from paper_2604_14650_b200.fib import Prefix
+    rng = np.random.default_rng(2)
+    fib = lpm.workload_fib(0)
+    store = st.FibStore(fib)
+    bad = st.UpdateOp(st.INSERT, Prefix(MASK64 << 64, 64, 7))  # starts at the sentinel key
+    ok = st.UpdateOp(st.ANNOUNCE, Prefix(0x2001 << 112, 16, 9))
+    assert store.stage([ok, bad]) == (2, [None, None])
+    with pytest.raises(lpm.Lpm6Error) as e:
+        store.commit()
+    assert e.value.code == "SentinelCollision"
+    assert store.epoch == 1 and store.stats.pending_ops == 2
+    addrs = probe_addrs(lpm, fib, rng)
+    np.testing.assert_array_equal(lookup(cuda, store, addrs), expected(lpm, orc, fib, addrs))
+    assert store.stage([st.UpdateOp(st.DELETE, bad.prefix)]) == (1, [None])
+    assert store.commit() == 2
+    view, _, _ = st.apply_updates(fib, [ok])
+    addrs = probe_addrs(lpm, view, rng)
+    np.testing.assert_array_equal(lookup(cuda, store, addrs), expected(lpm, orc, view, addrs))
+    store.close()
+
+
+def test_pinned_snapshot_survives_commits(lpm, orc, cuda, st):
+    """A reader's pinned snapshot keeps answering with its epoch's FIB; reclamation waits for release."""
+    from paper_2604_14650_b200.fib import Prefix
+    rng = np.random.default_rng(3)
+    fib = lpm.workload_fib(0)
+    store = st.FibStore(fib)
+    addrs = probe_addrs(lpm, fib, rng)
+    want1 = expected(lpm, orc, fib, addrs)
+    old = store.acquire()
+    ops = [st.UpdateOp(st.ANNOUNCE, Prefix(0, 0, 77))]  # change the default route's next hop
+    store.stage(ops)
+    assert store.commit() == 2
+    view, _, _ = st.apply_updates(fib, ops)
+    want2 = expected(lpm, orc, view, addrs)
+    assert np.any(want1 != want2)
+    assert store.stats.retired == 1  # held by `old`
+    np.testing.assert_array_equal(lookup(cuda, old, addrs), want1)
+    np.testing.assert_array_equal(lookup(cuda, store, addrs), want2)
+    with pytest.raises(lpm.Lpm6Error):
+        store.close()  # a snapshot is still acquired
+    old.release()
+    cuda.cuda.synchronize()
+    store.reclaim()
+    assert store.stats.retired == 0 and store.stats.reclaimed == 1
+    store.close()
+
+
+def test_release_is_stream_ordered(lpm, orc, cuda, st):
+    """Lookups queued before release keep the retired snapshot alive on the device."""
+    from paper_2604_14650_b200.fib import Prefix
+    torch = cuda
+    rng = np.random.default_rng(4)
+    fib = lpm.workload_fib(0)
+    store = st.FibStore(fib)
+    addrs = probe_addrs(lpm, fib, rng, n_random=1 << 20)
+    want = expected(lpm, orc, fib, addrs)
+    a = torch.from_numpy(addrs.view(np.uint8).reshape(-1, 16)).cuda()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        snap = store.acquire()
+        torch.cuda._sleep(1_000_000_000)  # ~0.5 s of device time ahead of the lookup
+        out = snap.lookup_batch(a, stream=s)
+        snap.release(s)
+    store.stage([st.UpdateOp(st.ANNOUNCE, Prefix(0, 0, 99))])
+    assert store.commit() == 2
+    store.reclaim()
+    assert store.stats.retired == 1, "freed while a queued lookup still uses it"
+    s.synchronize()
+    store.reclaim()
+    assert store.stats.retired == 0
+    got = out.cpu().numpy().astype(np.uint32)
+    np.testing.assert_array_equal(got, want)
+    store.close()
+
+
+def test_value_width_follows_commits(lpm, orc, cuda, st):
+    """A commit whose next hops outgrow the byte width rebuilds at 2 bytes (value_bytes = 0)."""
+    from paper_2604_14650_b200.fib import Prefix
+    rng = np.random.default_rng(5)
+    fib = lpm.workload_fib(0)
+    store = st.FibStore(fib)
+    with store.acquire() as snap:
+        assert snap.fib.geometry.value_bytes == 1
+    ops = [st.UpdateOp(st.ANNOUNCE, Prefix(0x2001 << 112, 16, 4000))]
+    store.stage(ops)
+    store.commit()
+    view, _, _ = st.apply_updates(fib, ops)
+    with store.acquire() as snap:
+        assert snap.fib.geometry.value_bytes == 2
+        addrs = probe_addrs(lpm, view, rng)
+        np.testing.assert_array_equal(lookup(cuda, snap, addrs), expected(lpm, orc, view, addrs))
+    store.close()
+
+
+def test_epoch_monotonic_over_1000_commits(lpm, cuda, st):
+    """Epoch monotonicity across >= 10^3 commits; memory is reclaimed as it goes."""
+    from paper_2604_14650_b200.fib import PREFIX_DTYPE, Prefix
+    rng = np.random.default_rng(6)
+    fib = lpm.FibTable(0, random_fib_rules(rng, 64, PREFIX_DTYPE, True))
+    store = st.FibStore(fib)
+    last = store.epoch
+    for i in range(1000):
+        store.stage([st.UpdateOp(st.ANNOUNCE, Prefix(0, 0, 1 + i % 200))])
+        e = store.commit()
+        assert e == last + 1
+        last = e
+    s = store.stats
+    assert s.epoch == 1001 and s.commits == 1000 and s.retired <= 1
+    store.close()
+
+
+def test_concurrent_readers_see_whole_snapshots(lpm, orc, cuda, st):
+    """Readers loop acquire -> lookups -> release while a writer commits: every
+    window's results equal the oracle of exactly one epoch's FIB."""
+    torch = cuda
+    rng = np.random.default_rng(7)
+    fib = lpm.workload_fib(0)
+    store = st.FibStore(fib)
+    addrs = probe_addrs(lpm, fib, rng, n_random=1 << 16)
+    a = torch.from_numpy(addrs.view(np.uint8).reshape(-1, 16)).cuda()
+    views = {1: fib}
+    stop = threading.Event()
+    seen: dict[int, list[np.ndarray]] = {}
+    errors: list[BaseException] = []
+    lock = threading.Lock()
+
+    def reader():
+        try:
+            s = torch.cuda.Stream()
+            while not stop.is_set():
+                with torch.cuda.stream(s):
+                    snap = store.acquire()
+                    o1 = snap.lookup_batch(a, stream=s)
+                    o2 = snap.lookup_batch(a, stream=s)
+                    snap.release(s)
+                s.synchronize()
+                r1 = o1.cpu().numpy().view(np.uint8 if o1.element_size() == 1 else np.uint16).astype(np.uint32)
+                r2 = o2.cpu().numpy().view(np.uint8 if o2.element_size() == 1 else np.uint16).astype(np.uint32)
+                assert np.array_equal(r1, r2), "torn window"
+                with lock:
+                    got = seen.setdefault(snap.epoch, [])
+                    if len(got) < 4:
+                        got.append(r1)
+        except BaseException as e:  # noqa: BLE001
+            errors.append(e)
+
+    threads = [threading.Thread(target=reader) for _ in range(3)]
+    for t in threads:
+        t.start()
+    view = fib
+    for _ in range(20):
+        ops = random_ops(st, rng, view, 50)
+        store.stage(ops)
+        view, _, _ = st.apply_updates(view, ops)
+        views[store.commit()] = view
+    stop.set()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    assert len(seen) >= 2
+    for e, rs in seen.items():
+        want = expected(lpm, orc, views[e], addrs)
+        for r in rs:
+            np.testing.assert_array_equal(r, want)
+    torch.cuda.synchronize()
+    store.reclaim()
+    assert store.stats.retired == 0
+    store.close()
+
+
+def test_update_trace_replay_c1(lpm, orc, cuda, st):
+    """An A/W update trace over the 200K FIB replayed in batches; after every commit
+    1,000 random addresses (+ boundary probes of the changed prefixes) match the
+    oracle of the updated FIB (cmd_update_bench's verification)."""
+    import ipaddress
+    rng = np.random.default_rng(8)
+    fib = lpm.workload_fib(1)
+    store = st.FibStore(fib)
+    rules = fib.rules
+    lines = []
+    for _ in range(3000):
+        if rng.random() < 0.5:
+            r = rules[int(rng.integers(0, len(rules)))]
+            v = int(r["value_hi"]) << 64
+            text = f"{ipaddress.IPv6Address(v)}/{int(r['length'])}"
+            lines.append(f"A {text} {int(rng.integers(1, 256))}" if rng.random() < 0.5 else f"W {text}")
+        else:
+            ln = int(rng.integers(32, 65))
+            top = (0x2000 << 48 | int(rng.integers(0, 2**61))) & ((MASK64 << (64 - ln)) & MASK64)
+            lines.append(f"A {ipaddress.IPv6Address(top << 64)}/{ln} {int(rng.integers(1, 256))}")
+    ops, bad = st.load_update_trace("\n".join(lines))
+    assert bad == 0
+    view = fib
+    for i in range(0, len(ops), 500):
+        batch = ops[i:i + 500]
+        store.stage(batch)
+        view, _, _ = st.apply_updates(view, batch)
+        store.commit()
+        keys = np.concatenate([rng.integers(0, 2**64, 1000, dtype=np.uint64),
+                               np.array([o.prefix.value >> 64 for o in batch], np.uint64)])
+        addrs = addrs_from_keys(keys, rng)
+        np.testing.assert_array_equal(lookup(cuda, store, addrs), expected(lpm, orc, view, addrs))
+    assert store.epoch == 7
+    store.close()
