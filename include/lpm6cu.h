@@ -184,6 +184,46 @@ int lpm6cu_fib_violations(lpm6cu_fib* fib, uint32_t* bits, int reset);
 int lpm6cu_lookup_batch(const lpm6cu_fib* fib, const void* addrs, uint64_t n, void* out,
                         void* stream);
 
+/* 8-byte keys instead of 16-byte addresses — the input of the reference's
+ * search_batch(t, keys[B]) and of its PBTR traces. Device buffers
+ * only; one kernel launch on `stream`. Keys are clamped like address keys. */
+int lpm6cu_lookup_keys(const lpm6cu_fib* fib, const uint64_t* keys, uint64_t n, void* out, void* stream);
+
+/* The layout step alone on the GPU, from host intervals (an IntervalMap:
+ * boundaries[0] = 0, strictly increasing, no sentinel, no reserved next hop) —
+ * the device counterpart of build_tree(map) (tree.hpp:74). merge_adjacent in
+ * opts is ignored (the map is final). */
+int lpm6cu_fib_build_from_intervals(int device, const uint64_t* boundaries, const uint32_t* next_hops, uint64_t m,
+                                    uint32_t default_next_hop, const lpm6cu_build_opts* opts, void* stream,
+                                    lpm6cu_fib** out);
+
+/* ---- reference file formats ---------------------------------------
+ * PBT1 snapshot (tree.hpp:90-96): "PBT1", u16 version 1, u16 k, u16 depth,
+ * u64 m, u64 allocated_leaf_nodes (26 header bytes), the reference LinearizedTree's
+ * keys (u64 LE) and values (u32 LE). PBTR trace: "PBTR", u16 version 1,
+ * u16 reserved, u64 count, count u64 LE keys. Errors: BadSnapshotFile /
+ * BadTraceFile / Io. */
+
+/* Interval map -> PBT1 bytes in the reference layout at k keys per node (8 = the
+ * reference default). buf NULL: *size only. */
+int lpm6_snapshot_encode(const uint64_t* boundaries, const uint32_t* next_hops, uint64_t m, uint32_t k, void* buf,
+                         uint64_t cap, uint64_t* size);
+int lpm6_snapshot_save(const uint64_t* boundaries, const uint32_t* next_hops, uint64_t m, uint32_t k,
+                       const char* path);
+/* Validate a PBT1 image and extract its interval map (arrays NULL: *m, *k only). */
+int lpm6_snapshot_decode(const void* buf, uint64_t size, uint64_t* boundaries, uint32_t* next_hops, uint64_t cap,
+                         uint64_t* m, uint32_t* k);
+/* PBT1 file -> device FIB without an interval sweep (load_snapshot_file, tree.hpp:96). */
+int lpm6cu_fib_load_snapshot(int device, const char* path, uint32_t default_next_hop, const lpm6cu_build_opts* opts,
+                             void* stream, lpm6cu_fib** out);
+int lpm6_trace_save(const uint64_t* keys, uint64_t n, const char* path);
+/* Validate a PBTR image in memory; *n = key count. */
+int lpm6_trace_count(const void* buf, uint64_t size, uint64_t* n);
+/* PBTR file -> d_keys (device, capacity cap keys) through pinned double-buffered
+ * staging, ordered on `stream`; returns when the keys are resident. d_keys NULL:
+ * validate and count only. */
+int lpm6cu_trace_load(int device, const char* path, uint64_t* d_keys, uint64_t cap, uint64_t* count, void* stream);
+
 /* ---- rebuild-and-swap FIB store (SPEC update-engine) ---
  *
  * Replaces the reference's FibStore: route changes are staged,

@@ -106,6 +106,15 @@ SIGNATURES = {
     "lpm6cu_querygen_destroy": (None, [P]),
     "lpm6cu_probe_l2_gather": (I32, [I32, U64, U32, C.POINTER(C.c_double)]),
     "lpm6cu_probe_smem": (I32, [I32, C.POINTER(C.c_double)]),
+    "lpm6cu_lookup_keys": (I32, [P, P, U64, P, P]),
+    "lpm6cu_fib_build_from_intervals": (I32, [I32, P, P, U64, U32, C.POINTER(BuildOpts_t), P, C.POINTER(P)]),
+    "lpm6_snapshot_encode": (I32, [P, P, U64, U32, P, U64, C.POINTER(U64)]),
+    "lpm6_snapshot_save": (I32, [P, P, U64, U32, C.c_char_p]),
+    "lpm6_snapshot_decode": (I32, [P, U64, P, P, U64, C.POINTER(U64), C.POINTER(U32)]),
+    "lpm6cu_fib_load_snapshot": (I32, [I32, C.c_char_p, U32, C.POINTER(BuildOpts_t), P, C.POINTER(P)]),
+    "lpm6_trace_save": (I32, [P, U64, C.c_char_p]),
+    "lpm6_trace_count": (I32, [P, U64, C.POINTER(U64)]),
+    "lpm6cu_trace_load": (I32, [I32, C.c_char_p, P, U64, C.POINTER(U64), P]),
     "lpm6_parse_update": (I32, [C.c_char_p, C.POINTER(UpdateOp_t)]),
     "lpm6_apply_updates": (I32, [P, U64, P, U64, P, U64, C.POINTER(U64), C.POINTER(U64), P]),
     "lpm6cu_store_create": (I32, [I32, P, U64, U32, C.POINTER(BuildOpts_t), C.POINTER(P)]),

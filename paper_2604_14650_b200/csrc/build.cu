@@ -370,18 +370,10 @@ DeviceIntervals device_intervals(const lpm6cu_prefix* rules, u64d n, unsigned de
 
 namespace lpm6::capi {
 
-// Steps 1-6: a device-resident line array (caller frees with cudaFree) + its geometry.
-void* device_build_tree(const lpm6cu_prefix* rules, uint64_t n, uint32_t default_nh, const lpm6cu_build_opts* opts,
-                        cudaStream_t s, lpm6cu_geometry* geom) {
-  const bool merge = opts ? opts->merge_adjacent != 0 : true;
-  u32 vb = opts ? opts->value_bytes : 0;
-  DeviceIntervals iv = device_intervals(rules, n, default_nh, merge, s);
-  const u32 need = iv.max_nh <= 0xFFu ? 1 : (iv.max_nh <= 0xFFFFu ? 2 : 4);
-  if (vb == 0) vb = need;
-  if (vb != 1 && vb != 2 && vb != 4) throw Error(Errc::InvalidArgument, "value_bytes must be 1, 2 or 4");
-  if (vb < need)
-    throw Error(Errc::InvalidArgument, "next hop " + std::to_string(iv.max_nh) + " does not fit in " +
-                                           std::to_string(vb) + " byte(s)");
+namespace {
+
+// Step 6: lay out m device-resident intervals; returns the cudaMalloc'ed line array.
+void* device_layout(const DeviceIntervals& iv, u32 vb, uint32_t default_nh, cudaStream_t s, lpm6cu_geometry* geom) {
   TreeLayout t = plan_layout(iv.m, vb);
   t.default_next_hop = default_nh;
   Geo g{};
@@ -421,6 +413,42 @@ void* device_build_tree(const lpm6cu_prefix* rules, uint64_t n, uint32_t default
   void* result = lines.p;
   lines.p = nullptr;
   return result;
+}
+
+u32 value_bytes_for(const lpm6cu_build_opts* opts, unsigned max_nh) {
+  u32 vb = opts ? opts->value_bytes : 0;
+  const u32 need = max_nh <= 0xFFu ? 1 : (max_nh <= 0xFFFFu ? 2 : 4);
+  if (vb == 0) vb = need;
+  if (vb != 1 && vb != 2 && vb != 4) throw Error(Errc::InvalidArgument, "value_bytes must be 1, 2 or 4");
+  if (vb < need)
+    throw Error(Errc::InvalidArgument, "next hop " + std::to_string(max_nh) + " does not fit in " +
+                                           std::to_string(vb) + " byte(s)");
+  return vb;
+}
+
+}  // namespace
+
+// Steps 1-6: a device-resident line array (caller frees with cudaFree) + its geometry.
+void* device_build_tree(const lpm6cu_prefix* rules, uint64_t n, uint32_t default_nh, const lpm6cu_build_opts* opts,
+                        cudaStream_t s, lpm6cu_geometry* geom) {
+  const bool merge = opts ? opts->merge_adjacent != 0 : true;
+  DeviceIntervals iv = device_intervals(rules, n, default_nh, merge, s);
+  return device_layout(iv, value_bytes_for(opts, iv.max_nh), default_nh, s, geom);
+}
+
+// Step 6 only, from host intervals already validated by the caller (a loaded
+// snapshot): one host->device copy of the boundaries and next hops.
+void* device_build_tree_from_intervals(const uint64_t* boundaries, const uint32_t* next_hops, uint64_t m,
+                                       uint32_t default_nh, const lpm6cu_build_opts* opts, cudaStream_t s,
+                                       lpm6cu_geometry* geom) {
+  DeviceIntervals iv;
+  iv.m = m;
+  iv.bnd = DBuf(m * 8, s);
+  iv.nh = DBuf(m * 4, s);
+  for (uint64_t i = 0; i < m; ++i) iv.max_nh = std::max(iv.max_nh, next_hops[i]);
+  ck(cudaMemcpyAsync(iv.bnd.p, boundaries, m * 8, cudaMemcpyHostToDevice, s), "H2D boundaries");
+  ck(cudaMemcpyAsync(iv.nh.p, next_hops, m * 4, cudaMemcpyHostToDevice, s), "H2D next hops");
+  return device_layout(iv, value_bytes_for(opts, iv.max_nh), default_nh, s, geom);
 }
 
 }  // namespace lpm6::capi

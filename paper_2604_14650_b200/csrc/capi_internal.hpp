@@ -20,5 +20,9 @@ Tree build_device_tree(const lpm6cu_prefix* rules, uint64_t n, uint32_t default_
 // Device-side build (build.cu): returns a cudaMalloc'ed line array and its geometry.
 void* device_build_tree(const lpm6cu_prefix* rules, uint64_t n, uint32_t default_nh, const lpm6cu_build_opts* opts,
                         cudaStream_t s, lpm6cu_geometry* geom);
+// Layout only, from validated host intervals (build.cu).
+void* device_build_tree_from_intervals(const uint64_t* boundaries, const uint32_t* next_hops, uint64_t m,
+                                       uint32_t default_nh, const lpm6cu_build_opts* opts, cudaStream_t s,
+                                       lpm6cu_geometry* geom);
 
 }  // namespace lpm6::capi

@@ -78,6 +78,12 @@ __device__ __forceinline__ uint4 ld_stream_v4(const uint4* p, uint64_t pol) {
   return r;
 }
 
+__device__ __forceinline__ unsigned long long ld_stream_u64(const unsigned long long* p, uint64_t pol) {
+  unsigned long long r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(pol));
+  return r;
+}
+
 __device__ __forceinline__ void ld_line_quarter(const unsigned long long* p, unsigned long long (&w)[4]) {
   asm volatile("ld.global.nc.L2::evict_last.v4.u64 {%0,%1,%2,%3}, [%4];"
                : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
@@ -120,7 +126,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 struct LookupParams {
   const unsigned long long* lines;                     // the tree, 16 u64 words per line
   unsigned long long level_start[LPM6CU_MAX_LEVELS];  // word offset of each level
-  const uint4* addrs;
+  const uint4* addrs;               // 16-byte addresses (lookup_batch), or
+  const unsigned long long* keys;   // 8-byte keys (lookup_keys: search_batch's input)
   unsigned char* out;
   unsigned long long n;
   const unsigned long long* image;  // packed 15-key copy of internal levels 0.. (layout.hpp)
@@ -201,7 +208,7 @@ __device__ __forceinline__ void store_group(const LookupParams& p, unsigned long
 // CHECKED adds bounds checks on every node index and leaf rank: a violation
 // (only possible with a corrupted tree) is clamped, never read out of bounds,
 // and reported through p.err — the fail-loudly mode the tests run.
-template <int DEPTH, int VB, int TILES, int THREADS, int MINB, bool CHECKED>
+template <int DEPTH, int VB, int TILES, int THREADS, int MINB, bool CHECKED, bool KEYS = false>
 __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const LookupParams p) {
   using F = LeafFmt<VB>;
   unsigned violations = 0;
@@ -242,8 +249,12 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
     const unsigned long long qi = (st_ * TILES + t) * 32ull + lane;
     unsigned long long k = 0;
     if (qi < p.n) {
-      const uint4 a = ld_stream_v4(p.addrs + qi, pol_stream);
-      k = (static_cast<unsigned long long>(a.w) << 32) | a.z;
+      if constexpr (KEYS) {
+        k = ld_stream_u64(p.keys + qi, pol_stream);
+      } else {
+        const uint4 a = ld_stream_v4(p.addrs + qi, pol_stream);
+        k = (static_cast<unsigned long long>(a.w) << 32) | a.z;
+      }
     }
     return k;
   };
@@ -328,34 +339,39 @@ using KernelFn = void (*)(const LookupParams);
 
 // Instantiated shapes: (queries per lane, min CTAs per SM) for every depth and
 // value width; the tuning grid below is measured by bench.py --sweep.
-template <int VB, int TILES, int THREADS, int MINB, bool CHECKED>
+template <int VB, int TILES, int THREADS, int MINB, bool CHECKED, bool KEYS>
 KernelFn pick_depth(int depth) {
   switch (depth) {
-    case 0: return lpm6_lookup_kernel<0, VB, TILES, THREADS, MINB, CHECKED>;
-    case 1: return lpm6_lookup_kernel<1, VB, TILES, THREADS, MINB, CHECKED>;
-    case 2: return lpm6_lookup_kernel<2, VB, TILES, THREADS, MINB, CHECKED>;
-    case 3: return lpm6_lookup_kernel<3, VB, TILES, THREADS, MINB, CHECKED>;
-    case 4: return lpm6_lookup_kernel<4, VB, TILES, THREADS, MINB, CHECKED>;
-    case 5: return lpm6_lookup_kernel<5, VB, TILES, THREADS, MINB, CHECKED>;
-    case 6: return lpm6_lookup_kernel<6, VB, TILES, THREADS, MINB, CHECKED>;
-    case 7: return lpm6_lookup_kernel<7, VB, TILES, THREADS, MINB, CHECKED>;
+    case 0: return lpm6_lookup_kernel<0, VB, TILES, THREADS, MINB, CHECKED, KEYS>;
+    case 1: return lpm6_lookup_kernel<1, VB, TILES, THREADS, MINB, CHECKED, KEYS>;
+    case 2: return lpm6_lookup_kernel<2, VB, TILES, THREADS, MINB, CHECKED, KEYS>;
+    case 3: return lpm6_lookup_kernel<3, VB, TILES, THREADS, MINB, CHECKED, KEYS>;
+    case 4: return lpm6_lookup_kernel<4, VB, TILES, THREADS, MINB, CHECKED, KEYS>;
+    case 5: return lpm6_lookup_kernel<5, VB, TILES, THREADS, MINB, CHECKED, KEYS>;
+    case 6: return lpm6_lookup_kernel<6, VB, TILES, THREADS, MINB, CHECKED, KEYS>;
+    case 7: return lpm6_lookup_kernel<7, VB, TILES, THREADS, MINB, CHECKED, KEYS>;
     default: return nullptr;
   }
 }
 
-template <int TILES, int THREADS, int MINB, bool CHECKED = false>
+template <int TILES, int THREADS, int MINB, bool CHECKED = false, bool KEYS = false>
 KernelFn pick_vb(int vb, int depth) {
   switch (vb) {
-    case 1: return pick_depth<1, TILES, THREADS, MINB, CHECKED>(depth);
-    case 2: return pick_depth<2, TILES, THREADS, MINB, CHECKED>(depth);
-    case 4: return pick_depth<4, TILES, THREADS, MINB, CHECKED>(depth);
+    case 1: return pick_depth<1, TILES, THREADS, MINB, CHECKED, KEYS>(depth);
+    case 2: return pick_depth<2, TILES, THREADS, MINB, CHECKED, KEYS>(depth);
+    case 4: return pick_depth<4, TILES, THREADS, MINB, CHECKED, KEYS>(depth);
     default: return nullptr;
   }
 }
 
 // Instantiated shapes (queries per lane, threads per CTA, min CTAs per SM);
 // bench.py --sweep measures them. The checked variant exists for the default shape.
-KernelFn pick_kernel(int vb, int depth, int tiles, int threads, int minb, bool checked = false) {
+KernelFn pick_kernel(int vb, int depth, int tiles, int threads, int minb, bool checked = false,
+                     bool keys = false) {
+  if (keys)  // 8-byte key input: the default shape, unchecked and checked
+    return (tiles == 1 && threads == 1024 && minb == 1)
+               ? (checked ? pick_vb<1, 1024, 1, true, true>(vb, depth) : pick_vb<1, 1024, 1, false, true>(vb, depth))
+               : nullptr;
   if (checked) return (tiles == 1 && threads == 1024 && minb == 1) ? pick_vb<1, 1024, 1, true>(vb, depth) : nullptr;
   if (tiles == 1 && threads == 256 && minb == 0) return pick_vb<1, 256, 0>(vb, depth);
   if (tiles == 1 && threads == 256 && minb == 4) return pick_vb<1, 256, 4>(vb, depth);
@@ -499,17 +515,23 @@ void resolve_config(lpm6cu_fib* f, const lpm6cu_kernel_config* req) {
 
 unsigned long long staged_bytes(const lpm6cu_fib* f) { return image_bytes_of(f->g, f->cfg.smem_levels); }
 
-void launch_lookup(const lpm6cu_fib* f, const void* d_addrs, unsigned long long n, void* d_out,
-                   cudaStream_t stream) {
+// keys = false: d_in holds 16-byte addresses; true: 8-byte keys (default kernel shape).
+void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, void* d_out, cudaStream_t stream,
+                   bool keys = false) {
   if (n == 0) return;
-  KernelFn fn = pick_kernel(static_cast<int>(f->g.value_bytes), static_cast<int>(f->g.depth),
-                            static_cast<int>(f->cfg.queries_per_lane), static_cast<int>(f->cfg.threads_per_cta),
-                            static_cast<int>(f->cfg.min_ctas_per_sm), f->d_err != nullptr);
+  const unsigned tiles = keys ? 1 : f->cfg.queries_per_lane;
+  const unsigned threads_cta = keys ? 1024 : f->cfg.threads_per_cta;
+  const unsigned minb = keys ? 1 : f->cfg.min_ctas_per_sm;
+  KernelFn fn = pick_kernel(static_cast<int>(f->g.value_bytes), static_cast<int>(f->g.depth), static_cast<int>(tiles),
+                            static_cast<int>(threads_cta), static_cast<int>(minb), f->d_err != nullptr, keys);
   if (!fn) throw Error(Errc::InvalidArgument, "no kernel instantiated for this configuration");
   LookupParams p{};
   p.lines = f->d_lines;
   for (int l = 0; l < LPM6CU_MAX_LEVELS; ++l) p.level_start[l] = f->g.level_start[l];
-  p.addrs = static_cast<const uint4*>(d_addrs);
+  if (keys)
+    p.keys = static_cast<const unsigned long long*>(d_in);
+  else
+    p.addrs = static_cast<const uint4*>(d_in);
   p.out = static_cast<unsigned char*>(d_out);
   p.n = n;
   p.smem_bytes = static_cast<unsigned>(staged_bytes(f));
@@ -517,7 +539,7 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_addrs, unsigned long long 
   p.image = f->d_lines + f->g.image_start;
   for (int l = 0; l < LPM6CU_MAX_LEVELS; ++l) p.level_nodes[l] = f->g.level_nodes[l];
   p.err = f->d_err;
-  const int threads = static_cast<int>(f->cfg.threads_per_cta);
+  const int threads = static_cast<int>(threads_cta);
   const size_t smem = p.smem_bytes;
   if (smem > 48 * 1024)
     check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
@@ -526,10 +548,10 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_addrs, unsigned long long 
   check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem), "occupancy");
   if (per_sm < 1) throw Error(Errc::CudaError, "lookup kernel cannot be resident with this configuration");
   if (f->cfg.ctas_per_sm > 0) per_sm = std::min<int>(per_sm, static_cast<int>(f->cfg.ctas_per_sm));
-  const unsigned long long tiles = (n + 32ull * f->cfg.queries_per_lane - 1) / (32ull * f->cfg.queries_per_lane);
+  const unsigned long long ntiles = (n + 32ull * tiles - 1) / (32ull * tiles);
   const unsigned long long warps_per_cta = threads / 32;
   unsigned long long grid = static_cast<unsigned long long>(f->num_sms) * per_sm;
-  grid = std::min(grid, (tiles + warps_per_cta - 1) / warps_per_cta);
+  grid = std::min(grid, (ntiles + warps_per_cta - 1) / warps_per_cta);
   fn<<<static_cast<unsigned>(grid), threads, smem, stream>>>(p);
   check_cuda(cudaGetLastError(), "lookup launch");
 }
@@ -739,6 +761,49 @@ int lpm6cu_lookup_batch(const lpm6cu_fib* fib, const void* addrs, uint64_t n, vo
       launch_lookup(fib, addrs, n, out, static_cast<cudaStream_t>(stream));
     else
       lookup_host(const_cast<lpm6cu_fib*>(fib), addrs, n, out, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int lpm6cu_lookup_keys(const lpm6cu_fib* fib, const uint64_t* keys, uint64_t n, void* out, void* stream) {
+  return guard([&] {
+    if (!fib) throw Error(Errc::InvalidArgument, "NULL fib");
+    if (n == 0) return;
+    if (!keys || !out) throw Error(Errc::InvalidArgument, "NULL buffer");
+    DeviceGuard dg(fib->device);
+    if (!is_device_ptr(keys) || !is_device_ptr(out))
+      throw Error(Errc::InvalidArgument, "lpm6cu_lookup_keys takes device buffers");
+    if (reinterpret_cast<uintptr_t>(keys) % 8 != 0) throw Error(Errc::InvalidArgument, "keys must be 8-byte aligned");
+    launch_lookup(fib, keys, n, out, static_cast<cudaStream_t>(stream), true);
+  });
+}
+
+int lpm6cu_fib_build_from_intervals(int device, const uint64_t* boundaries, const uint32_t* next_hops, uint64_t m,
+                                    uint32_t default_nh, const lpm6cu_build_opts* opts, void* stream,
+                                    lpm6cu_fib** out) {
+  return guard([&] {
+    if (!boundaries || !next_hops || !out) throw Error(Errc::InvalidArgument, "NULL argument");
+    // The IntervalMap contract (intervals.hpp:18-24).
+    if (m == 0) throw Error(Errc::InvalidArgument, "an interval map has at least one boundary");
+    if (boundaries[0] != 0) throw Error(Errc::InvalidArgument, "boundaries[0] must be 0");
+    for (uint64_t i = 0; i < m; ++i) {
+      if (i && boundaries[i] <= boundaries[i - 1])
+        throw Error(Errc::InvalidArgument, "boundaries must be strictly increasing");
+      if (next_hops[i] == kUnresolved) throw Error(Errc::ReservedNextHop, "next hop 4294967295 is reserved");
+    }
+    if (boundaries[m - 1] == kSentinelKey) throw Error(Errc::SentinelCollision, "boundary equals the sentinel key");
+    DeviceGuard dg(device);
+    lpm6cu_geometry g;
+    void* lines = capi::device_build_tree_from_intervals(boundaries, next_hops, m, default_nh, opts,
+                                                         static_cast<cudaStream_t>(stream), &g);
+    std::unique_ptr<lpm6cu_fib> f;
+    try {
+      f.reset(new_fib(device, &g));
+    } catch (...) {
+      cudaFree(lines);
+      throw;
+    }
+    f->d_lines = static_cast<unsigned long long*>(lines);
+    *out = f.release();
   });
 }
 

@@ -225,6 +225,52 @@ def build_tree(imap: IntervalMap, value_bytes: int = 0) -> Tree:
     return Tree(Geometry.from_c(g), lines, vals)
 
 
+# ---- reference file formats: PBT1 snapshots, PBTR traces (csrc/lpm6/snapshot.cpp) --
+
+def encode_snapshot(imap: IntervalMap, k: int = 8) -> bytes:
+    """PBT1 bytes of ``imap`` in the reference's layout (tree.hpp:90-96)."""
+    b = np.ascontiguousarray(imap.boundaries, np.uint64)
+    nh = np.ascontiguousarray(imap.next_hops, np.uint32)
+    size = C.c_uint64(0)
+    check(lib().lpm6_snapshot_encode(b.ctypes.data, nh.ctypes.data, len(b), k, None, 0, C.byref(size)))
+    buf = np.empty(size.value, np.uint8)
+    check(lib().lpm6_snapshot_encode(b.ctypes.data, nh.ctypes.data, len(b), k, buf.ctypes.data, size.value,
+                                     C.byref(size)))
+    return buf.tobytes()
+
+
+def save_snapshot(imap: IntervalMap, path: str, k: int = 8) -> None:
+    b = np.ascontiguousarray(imap.boundaries, np.uint64)
+    nh = np.ascontiguousarray(imap.next_hops, np.uint32)
+    check(lib().lpm6_snapshot_save(b.ctypes.data, nh.ctypes.data, len(b), k, str(path).encode()))
+
+
+def decode_snapshot(data: bytes, default_next_hop: int = 0) -> tuple[IntervalMap, int]:
+    """Validate a PBT1 image; returns (its interval map, k)."""
+    raw = np.frombuffer(data, np.uint8)
+    m, k = C.c_uint64(0), C.c_uint32(0)
+    ptr = raw.ctypes.data if len(raw) else None
+    check(lib().lpm6_snapshot_decode(ptr, len(raw), None, None, 0, C.byref(m), C.byref(k)))
+    b = np.empty(m.value, np.uint64)
+    nh = np.empty(m.value, np.uint32)
+    check(lib().lpm6_snapshot_decode(ptr, len(raw), b.ctypes.data, nh.ctypes.data, m.value, C.byref(m),
+                                     C.byref(k)))
+    return IntervalMap(b, nh, default_next_hop), k.value
+
+
+def save_trace(keys: np.ndarray, path: str) -> None:
+    """PBTR key trace."""
+    k = np.ascontiguousarray(keys, np.uint64)
+    check(lib().lpm6_trace_save(k.ctypes.data if len(k) else None, len(k), str(path).encode()))
+
+
+def trace_count(data: bytes) -> int:
+    raw = np.frombuffer(data, np.uint8)
+    n = C.c_uint64(0)
+    check(lib().lpm6_trace_count(raw.ctypes.data if len(raw) else None, len(raw), C.byref(n)))
+    return n.value
+
+
 # ---- synthetic workloads (BASELINE.json configs) ---------------------------------
 
 WORKLOADS = {"C0": 0, "C1": 1, "C2": 2, "C3a": 3, "C3b": 4, "C4": 5}

@@ -78,6 +78,28 @@ class Fib:
         return cls(h.value, device)
 
     @classmethod
+    def from_intervals(cls, imap, device: int = 0, value_bytes: int = 0, stream=None) -> "Fib":
+        """Layout-only device build from an IntervalMap (build_tree(map), tree.hpp:74)."""
+        h = C.c_void_p()
+        opts = build_opts(True, value_bytes)
+        b = np.ascontiguousarray(imap.boundaries, np.uint64)
+        nh = np.ascontiguousarray(imap.next_hops, np.uint32)
+        check(lib().lpm6cu_fib_build_from_intervals(device, b.ctypes.data, nh.ctypes.data, len(b),
+                                                    imap.default_next_hop, C.byref(opts), _stream_handle(stream),
+                                                    C.byref(h)))
+        return cls(h.value, device)
+
+    @classmethod
+    def load_snapshot(cls, path: str, device: int = 0, value_bytes: int = 0, default_next_hop: int = 0,
+                      stream=None) -> "Fib":
+        """PBT1 snapshot file -> device FIB, no interval sweep (load_snapshot_file, tree.hpp:96)."""
+        h = C.c_void_p()
+        opts = build_opts(True, value_bytes)
+        check(lib().lpm6cu_fib_load_snapshot(device, str(path).encode(), default_next_hop, C.byref(opts),
+                                             _stream_handle(stream), C.byref(h)))
+        return cls(h.value, device)
+
+    @classmethod
     def from_tree(cls, tree: Tree, device: int = 0) -> "Fib":
         h = C.c_void_p()
         g = tree.geometry.to_c()
@@ -175,6 +197,33 @@ class Fib:
         s = _stream_handle(stream) if adev else None
         check(lib().lpm6cu_lookup_batch(self._h, aptr, n, optr, s))
         return out
+
+
+    def lookup_keys(self, keys, out=None, stream=None):
+        """Next hops of n 8-byte keys (search_batch's input): device buffers,
+        one asynchronous kernel launch on ``stream``."""
+        vb = self.geometry.value_bytes
+        kptr, n, kdev = _ptr_len(keys, 8)
+        if out is None:
+            torch = _torch()
+            dt = {1: torch.uint8, 2: torch.int16, 4: torch.int32}[vb]
+            out = torch.empty(n, dtype=dt, device=keys.device if kdev else "cuda")
+        optr, nout, odev = _ptr_len(out, vb)
+        if nout < n:
+            raise Lpm6Error(9, f"out holds {nout} next hops, need {n}")
+        check(lib().lpm6cu_lookup_keys(self._h, kptr, n, optr, _stream_handle(stream)))
+        return out
+
+
+def load_trace(path: str, device: int = 0, stream=None):
+    """PBTR trace file -> torch uint64-as-int64 device tensor of its keys."""
+    torch = _torch()
+    n = C.c_uint64(0)
+    check(lib().lpm6cu_trace_load(device, str(path).encode(), None, 0, C.byref(n), None))
+    keys = torch.empty(max(n.value, 1), dtype=torch.int64, device=f"cuda:{device}")
+    check(lib().lpm6cu_trace_load(device, str(path).encode(), keys.data_ptr(), n.value, C.byref(n),
+                                  _stream_handle(stream)))
+    return keys[: n.value]
 
 
 class QueryGen:
