@@ -78,11 +78,12 @@ typedef struct {
   uint32_t depth;       /* internal levels; a lookup visits depth + 1 lines */
   uint32_t value_bytes; /* next-hop width: 1, 2 or 4 */
   uint32_t leaf_keys;   /* keys per leaf line: 14, 12 or 8 for 1-, 2-, 4-byte next hops */
-  uint32_t image_levels;/* the shared-memory image covers levels [1, image_levels) */
+  uint32_t image_levels;/* internal levels [0, image_levels) have a shared-memory image */
   uint64_t num_keys;    /* m, real interval boundaries */
   uint64_t leaf_nodes;  /* ceil(m / leaf_keys) */
   uint64_t total_words; /* length of the array in u64 words: tree lines, then the image */
-  uint64_t image_start; /* word offset of the bank-swizzled copy of levels 1.. staged by TMA */
+  uint64_t image_start; /* word offset of that image: the 15 keys of each node at a 120-byte
+                           stride (bank skew), staged into shared memory by one TMA copy */
   uint64_t level_nodes[LPM6CU_MAX_LEVELS]; /* reachable nodes per level (level depth = leaves) */
   uint64_t level_start[LPM6CU_MAX_LEVELS]; /* u64-word offset of each level */
   uint32_t default_next_hop;
@@ -102,9 +103,10 @@ typedef struct {
   uint32_t smem_levels;     /* top levels staged in shared memory by TMA and searched one
                                thread per query; 0xFF = auto */
   uint32_t ctas_per_sm;      /* cap on resident CTAs per SM used for the grid; 0 = occupancy */
-  uint32_t threads_per_cta;  /* 256 */
-  uint32_t queries_per_lane; /* 32-query tiles each warp carries at once: 1 or 2 */
-  uint32_t min_ctas_per_sm;  /* register cap (__launch_bounds__ min blocks): 0, 3, 4, 5, 6 */
+  uint32_t threads_per_cta;  /* 1024 (default), 512 or 256 */
+  uint32_t queries_per_lane; /* 32-query tiles each warp carries at once: 1, or 2 at 256 threads */
+  uint32_t min_ctas_per_sm;  /* register cap (__launch_bounds__ min blocks): 1 at 1024 threads,
+                                2 at 512, 0 or 4 at 256 */
 } lpm6cu_kernel_config;
 
 typedef struct lpm6cu_fib lpm6cu_fib;
@@ -188,6 +190,14 @@ int lpm6cu_lookup_batch(const lpm6cu_fib* fib, const void* addrs, uint64_t n, vo
  * search_batch(t, keys[B]) and of its PBTR traces. Device buffers
  * only; one kernel launch on `stream`. Keys are clamped like address keys. */
 int lpm6cu_lookup_keys(const lpm6cu_fib* fib, const uint64_t* keys, uint64_t n, void* out, void* stream);
+
+/* Packet-path ingest: n frames `stride` bytes apart in device memory
+ * (e.g. a NIC RX ring written by GPUDirect), the IPv6 destination address at byte
+ * `dst_offset` of each frame in network byte order (38 for Ethernet + IPv6). The
+ * kernel reads the destination's first 8 bytes straight from the frame — no
+ * separate extraction pass — and writes one next hop per frame. */
+int lpm6cu_lookup_packets(const lpm6cu_fib* fib, const void* frames, uint64_t n, uint64_t stride, uint32_t dst_offset,
+                          void* out, void* stream);
 
 /* The layout step alone on the GPU, from host intervals (an IntervalMap:
  * boundaries[0] = 0, strictly increasing, no sentinel, no reserved next hop) —

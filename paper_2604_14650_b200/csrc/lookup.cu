@@ -84,6 +84,56 @@ __device__ __forceinline__ unsigned long long ld_stream_u64(const unsigned long 
   return r;
 }
 
+// Input formats of the lookup kernel.
+enum : int { kInAddr = 0, kInKey = 1, kInPacket = 2 };
+
+template <class T>
+__device__ __forceinline__ T ld_stream(const void* p, uint64_t pol);
+template <>
+__device__ __forceinline__ unsigned long long ld_stream<unsigned long long>(const void* p, uint64_t pol) {
+  unsigned long long r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(pol));
+  return r;
+}
+template <>
+__device__ __forceinline__ unsigned ld_stream<unsigned>(const void* p, uint64_t pol) {
+  unsigned r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
+template <>
+__device__ __forceinline__ unsigned short ld_stream<unsigned short>(const void* p, uint64_t pol) {
+  unsigned short r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(r) : "l"(p), "l"(pol));
+  return r;
+}
+
+__device__ __forceinline__ unsigned long long bswap64(unsigned long long v) {
+  const unsigned lo = static_cast<unsigned>(v), hi = static_cast<unsigned>(v >> 32);
+  return (static_cast<unsigned long long>(__byte_perm(lo, 0, 0x0123)) << 32) | __byte_perm(hi, 0, 0x0123);
+}
+
+// Top 64 bits of an IPv6 address stored in network byte order (the first 8
+// bytes of the destination field) at an address aligned to `align` bytes.
+__device__ __forceinline__ unsigned long long load_dst_key(const unsigned char* a, unsigned align, uint64_t pol) {
+  unsigned long long le;  // the 8 bytes as a little-endian integer
+  if (align >= 8) {
+    le = ld_stream<unsigned long long>(a, pol);
+  } else if (align >= 4) {
+    le = ld_stream<unsigned>(a, pol) | (static_cast<unsigned long long>(ld_stream<unsigned>(a + 4, pol)) << 32);
+  } else if (align >= 2) {
+    le = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      le |= static_cast<unsigned long long>(ld_stream<unsigned short>(a + 2 * i, pol)) << (16 * i);
+  } else {
+    le = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) le |= static_cast<unsigned long long>(__ldg(a + i)) << (8 * i);
+  }
+  return bswap64(le);  // network order: first byte is the most significant
+}
+
 __device__ __forceinline__ void ld_line_quarter(const unsigned long long* p, unsigned long long (&w)[4]) {
   asm volatile("ld.global.nc.L2::evict_last.v4.u64 {%0,%1,%2,%3}, [%4];"
                : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
@@ -126,8 +176,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 struct LookupParams {
   const unsigned long long* lines;                     // the tree, 16 u64 words per line
   unsigned long long level_start[LPM6CU_MAX_LEVELS];  // word offset of each level
-  const uint4* addrs;               // 16-byte addresses (lookup_batch), or
-  const unsigned long long* keys;   // 8-byte keys (lookup_keys: search_batch's input)
+  const uint4* addrs;               // kInAddr: 16-byte addresses (lookup_batch), or
+  const unsigned long long* keys;   // kInKey: 8-byte keys (lookup_keys: search_batch's input), or
+  const unsigned char* pkts;        // kInPacket: frames, destination address at pkt_off of each
+  unsigned long long pkt_stride;    //   bytes between frames
+  unsigned int pkt_off;             //   byte offset of the IPv6 destination address in a frame
+  unsigned int pkt_align;           //   8, 4, 2 or 1: alignment of every destination address
   unsigned char* out;
   unsigned long long n;
   const unsigned long long* image;  // packed 15-key copy of internal levels 0.. (layout.hpp)
@@ -208,7 +262,7 @@ __device__ __forceinline__ void store_group(const LookupParams& p, unsigned long
 // CHECKED adds bounds checks on every node index and leaf rank: a violation
 // (only possible with a corrupted tree) is clamped, never read out of bounds,
 // and reported through p.err — the fail-loudly mode the tests run.
-template <int DEPTH, int VB, int TILES, int THREADS, int MINB, bool CHECKED, bool KEYS = false>
+template <int DEPTH, int VB, int TILES, int THREADS, int MINB, bool CHECKED, int INPUT = kInAddr>
 __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const LookupParams p) {
   using F = LeafFmt<VB>;
   unsigned violations = 0;
@@ -249,8 +303,10 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
     const unsigned long long qi = (st_ * TILES + t) * 32ull + lane;
     unsigned long long k = 0;
     if (qi < p.n) {
-      if constexpr (KEYS) {
+      if constexpr (INPUT == kInKey) {
         k = ld_stream_u64(p.keys + qi, pol_stream);
+      } else if constexpr (INPUT == kInPacket) {
+        k = load_dst_key(p.pkts + qi * p.pkt_stride + p.pkt_off, p.pkt_align, pol_stream);
       } else {
         const uint4 a = ld_stream_v4(p.addrs + qi, pol_stream);
         k = (static_cast<unsigned long long>(a.w) << 32) | a.z;
@@ -339,27 +395,27 @@ using KernelFn = void (*)(const LookupParams);
 
 // Instantiated shapes: (queries per lane, min CTAs per SM) for every depth and
 // value width; the tuning grid below is measured by bench.py --sweep.
-template <int VB, int TILES, int THREADS, int MINB, bool CHECKED, bool KEYS>
+template <int VB, int TILES, int THREADS, int MINB, bool CHECKED, int INPUT>
 KernelFn pick_depth(int depth) {
   switch (depth) {
-    case 0: return lpm6_lookup_kernel<0, VB, TILES, THREADS, MINB, CHECKED, KEYS>;
-    case 1: return lpm6_lookup_kernel<1, VB, TILES, THREADS, MINB, CHECKED, KEYS>;
-    case 2: return lpm6_lookup_kernel<2, VB, TILES, THREADS, MINB, CHECKED, KEYS>;
-    case 3: return lpm6_lookup_kernel<3, VB, TILES, THREADS, MINB, CHECKED, KEYS>;
-    case 4: return lpm6_lookup_kernel<4, VB, TILES, THREADS, MINB, CHECKED, KEYS>;
-    case 5: return lpm6_lookup_kernel<5, VB, TILES, THREADS, MINB, CHECKED, KEYS>;
-    case 6: return lpm6_lookup_kernel<6, VB, TILES, THREADS, MINB, CHECKED, KEYS>;
-    case 7: return lpm6_lookup_kernel<7, VB, TILES, THREADS, MINB, CHECKED, KEYS>;
+    case 0: return lpm6_lookup_kernel<0, VB, TILES, THREADS, MINB, CHECKED, INPUT>;
+    case 1: return lpm6_lookup_kernel<1, VB, TILES, THREADS, MINB, CHECKED, INPUT>;
+    case 2: return lpm6_lookup_kernel<2, VB, TILES, THREADS, MINB, CHECKED, INPUT>;
+    case 3: return lpm6_lookup_kernel<3, VB, TILES, THREADS, MINB, CHECKED, INPUT>;
+    case 4: return lpm6_lookup_kernel<4, VB, TILES, THREADS, MINB, CHECKED, INPUT>;
+    case 5: return lpm6_lookup_kernel<5, VB, TILES, THREADS, MINB, CHECKED, INPUT>;
+    case 6: return lpm6_lookup_kernel<6, VB, TILES, THREADS, MINB, CHECKED, INPUT>;
+    case 7: return lpm6_lookup_kernel<7, VB, TILES, THREADS, MINB, CHECKED, INPUT>;
     default: return nullptr;
   }
 }
 
-template <int TILES, int THREADS, int MINB, bool CHECKED = false, bool KEYS = false>
+template <int TILES, int THREADS, int MINB, bool CHECKED = false, int INPUT = kInAddr>
 KernelFn pick_vb(int vb, int depth) {
   switch (vb) {
-    case 1: return pick_depth<1, TILES, THREADS, MINB, CHECKED, KEYS>(depth);
-    case 2: return pick_depth<2, TILES, THREADS, MINB, CHECKED, KEYS>(depth);
-    case 4: return pick_depth<4, TILES, THREADS, MINB, CHECKED, KEYS>(depth);
+    case 1: return pick_depth<1, TILES, THREADS, MINB, CHECKED, INPUT>(depth);
+    case 2: return pick_depth<2, TILES, THREADS, MINB, CHECKED, INPUT>(depth);
+    case 4: return pick_depth<4, TILES, THREADS, MINB, CHECKED, INPUT>(depth);
     default: return nullptr;
   }
 }
@@ -367,11 +423,16 @@ KernelFn pick_vb(int vb, int depth) {
 // Instantiated shapes (queries per lane, threads per CTA, min CTAs per SM);
 // bench.py --sweep measures them. The checked variant exists for the default shape.
 KernelFn pick_kernel(int vb, int depth, int tiles, int threads, int minb, bool checked = false,
-                     bool keys = false) {
-  if (keys)  // 8-byte key input: the default shape, unchecked and checked
-    return (tiles == 1 && threads == 1024 && minb == 1)
-               ? (checked ? pick_vb<1, 1024, 1, true, true>(vb, depth) : pick_vb<1, 1024, 1, false, true>(vb, depth))
-               : nullptr;
+                     int input = kInAddr) {
+  if (input != kInAddr) {  // key / packet input: the default shape, unchecked and checked
+    if (tiles != 1 || threads != 1024 || minb != 1) return nullptr;
+    if (input == kInKey)
+      return checked ? pick_vb<1, 1024, 1, true, kInKey>(vb, depth) : pick_vb<1, 1024, 1, false, kInKey>(vb, depth);
+    if (input == kInPacket)
+      return checked ? pick_vb<1, 1024, 1, true, kInPacket>(vb, depth)
+                     : pick_vb<1, 1024, 1, false, kInPacket>(vb, depth);
+    return nullptr;
+  }
   if (checked) return (tiles == 1 && threads == 1024 && minb == 1) ? pick_vb<1, 1024, 1, true>(vb, depth) : nullptr;
   if (tiles == 1 && threads == 256 && minb == 0) return pick_vb<1, 256, 0>(vb, depth);
   if (tiles == 1 && threads == 256 && minb == 4) return pick_vb<1, 256, 4>(vb, depth);
@@ -515,23 +576,36 @@ void resolve_config(lpm6cu_fib* f, const lpm6cu_kernel_config* req) {
 
 unsigned long long staged_bytes(const lpm6cu_fib* f) { return image_bytes_of(f->g, f->cfg.smem_levels); }
 
-// keys = false: d_in holds 16-byte addresses; true: 8-byte keys (default kernel shape).
+struct PacketInput {
+  unsigned long long stride = 0;
+  unsigned off = 0, align = 8;
+};
+
+// input: kInAddr (d_in = 16-byte addresses, configured shape), kInKey (8-byte
+// keys) or kInPacket (frames described by pk); the last two use the default shape.
 void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, void* d_out, cudaStream_t stream,
-                   bool keys = false) {
+                   int input = kInAddr, const PacketInput* pk = nullptr) {
   if (n == 0) return;
-  const unsigned tiles = keys ? 1 : f->cfg.queries_per_lane;
-  const unsigned threads_cta = keys ? 1024 : f->cfg.threads_per_cta;
-  const unsigned minb = keys ? 1 : f->cfg.min_ctas_per_sm;
+  const bool dflt = input != kInAddr;
+  const unsigned tiles = dflt ? 1 : f->cfg.queries_per_lane;
+  const unsigned threads_cta = dflt ? 1024 : f->cfg.threads_per_cta;
+  const unsigned minb = dflt ? 1 : f->cfg.min_ctas_per_sm;
   KernelFn fn = pick_kernel(static_cast<int>(f->g.value_bytes), static_cast<int>(f->g.depth), static_cast<int>(tiles),
-                            static_cast<int>(threads_cta), static_cast<int>(minb), f->d_err != nullptr, keys);
+                            static_cast<int>(threads_cta), static_cast<int>(minb), f->d_err != nullptr, input);
   if (!fn) throw Error(Errc::InvalidArgument, "no kernel instantiated for this configuration");
   LookupParams p{};
   p.lines = f->d_lines;
   for (int l = 0; l < LPM6CU_MAX_LEVELS; ++l) p.level_start[l] = f->g.level_start[l];
-  if (keys)
+  if (input == kInKey) {
     p.keys = static_cast<const unsigned long long*>(d_in);
-  else
+  } else if (input == kInPacket) {
+    p.pkts = static_cast<const unsigned char*>(d_in);
+    p.pkt_stride = pk->stride;
+    p.pkt_off = pk->off;
+    p.pkt_align = pk->align;
+  } else {
     p.addrs = static_cast<const uint4*>(d_in);
+  }
   p.out = static_cast<unsigned char*>(d_out);
   p.n = n;
   p.smem_bytes = static_cast<unsigned>(staged_bytes(f));
@@ -773,7 +847,26 @@ int lpm6cu_lookup_keys(const lpm6cu_fib* fib, const uint64_t* keys, uint64_t n, 
     if (!is_device_ptr(keys) || !is_device_ptr(out))
       throw Error(Errc::InvalidArgument, "lpm6cu_lookup_keys takes device buffers");
     if (reinterpret_cast<uintptr_t>(keys) % 8 != 0) throw Error(Errc::InvalidArgument, "keys must be 8-byte aligned");
-    launch_lookup(fib, keys, n, out, static_cast<cudaStream_t>(stream), true);
+    launch_lookup(fib, keys, n, out, static_cast<cudaStream_t>(stream), kInKey);
+  });
+}
+
+int lpm6cu_lookup_packets(const lpm6cu_fib* fib, const void* frames, uint64_t n, uint64_t stride, uint32_t dst_offset,
+                          void* out, void* stream) {
+  return guard([&] {
+    if (!fib) throw Error(Errc::InvalidArgument, "NULL fib");
+    if (n == 0) return;
+    if (!frames || !out) throw Error(Errc::InvalidArgument, "NULL buffer");
+    if (stride < dst_offset + 16ull) throw Error(Errc::InvalidArgument, "stride must cover dst_offset + 16 bytes");
+    DeviceGuard dg(fib->device);
+    if (!is_device_ptr(frames) || !is_device_ptr(out))
+      throw Error(Errc::InvalidArgument, "lpm6cu_lookup_packets takes device buffers");
+    PacketInput pk;
+    pk.stride = stride;
+    pk.off = dst_offset;
+    const unsigned long long bits = (reinterpret_cast<uintptr_t>(frames) + dst_offset) | stride;
+    pk.align = (bits & 7) == 0 ? 8 : (bits & 3) == 0 ? 4 : (bits & 1) == 0 ? 2 : 1;
+    launch_lookup(fib, frames, n, out, static_cast<cudaStream_t>(stream), kInPacket, &pk);
   });
 }
 

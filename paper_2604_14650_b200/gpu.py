@@ -214,6 +214,23 @@ class Fib:
         check(lib().lpm6cu_lookup_keys(self._h, kptr, n, optr, _stream_handle(stream)))
         return out
 
+    def lookup_packets(self, frames, n: int, stride: int, dst_offset: int = 38, out=None, stream=None):
+        """Next hops of n frames ``stride`` bytes apart in a device buffer, the IPv6
+        destination at ``dst_offset`` (network order; 38 = Ethernet + IPv6)."""
+        vb = self.geometry.value_bytes
+        fptr, nbytes, fdev = _ptr_len(frames, 1)
+        if n and (n - 1) * stride + dst_offset + 16 > nbytes:
+            raise Lpm6Error(9, "frame buffer too small for n frames")
+        if out is None:
+            torch = _torch()
+            dt = {1: torch.uint8, 2: torch.int16, 4: torch.int32}[vb]
+            out = torch.empty(n, dtype=dt, device=frames.device if fdev else "cuda")
+        optr, nout, _ = _ptr_len(out, vb)
+        if nout < n:
+            raise Lpm6Error(9, f"out holds {nout} next hops, need {n}")
+        check(lib().lpm6cu_lookup_packets(self._h, fptr, n, stride, dst_offset, optr, _stream_handle(stream)))
+        return out
+
 
 def load_trace(path: str, device: int = 0, stream=None):
     """PBTR trace file -> torch uint64-as-int64 device tensor of its keys."""

@@ -104,3 +104,39 @@ def test_trace_to_device_and_lookup(lpm, orc, cuda, tmp_path):
     with pytest.raises(lpm.Lpm6Error) as e:
         lpm.load_trace(tmp_path / "bad.pbtr")
     assert e.value.code == "BadTraceFile"
+
+
+def make_frames(addrs: np.ndarray, stride: int, dst_offset: int, rng) -> np.ndarray:
+    """Frames with random bytes everywhere but the IPv6 destination field, written
+    in network byte order (first hextet first) at dst_offset."""
+    n = len(addrs)
+    frames = rng.integers(0, 256, n * stride, dtype=np.uint8).reshape(n, stride)
+    be = np.empty((n, 16), np.uint8)
+    hi = addrs[:, 1].astype(">u8").view(np.uint8).reshape(n, 8)
+    lo = addrs[:, 0].astype(">u8").view(np.uint8).reshape(n, 8)
+    be[:, :8], be[:, 8:] = hi, lo
+    frames[:, dst_offset:dst_offset + 16] = be
+    return frames.reshape(-1)
+
+
+@pytest.mark.parametrize("stride,off", [(64, 38), (80, 40), (72, 36), (66, 38), (65, 38), (128, 22)])
+def test_lookup_packets_matches_oracle(lpm, orc, cuda, stride, off):
+    """Packet ingest: the destination read straight from frames at every alignment
+    (8/4/2/1) gives the oracle's next hops (Ethernet + IPv6: offset 38)."""
+    torch = cuda
+    fib = lpm.workload_fib(1)
+    imap = lpm.build_intervals(fib)
+    rng = np.random.default_rng(stride * 100 + off)
+    keys = np.concatenate([boundary_probe_keys(imap.boundaries)[:20000],
+                           rng.integers(0, 2**64, 50000, dtype=np.uint64)])
+    addrs = addrs_from_keys(keys, rng)
+    want, _ = orc.lookup_batch(0, imap.boundaries, imap.next_hops, addrs, threads=8)
+    frames = torch.from_numpy(make_frames(addrs, stride, off, rng)).cuda()
+    dev = lpm.Fib.build(fib)
+    for checked in (False, True):
+        dev.set_checked(checked)
+        out = dev.lookup_packets(frames, len(addrs), stride, off)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(out.cpu().numpy().astype(np.uint32), want)
+    with pytest.raises(lpm.Lpm6Error):
+        dev.lookup_packets(frames, len(addrs) + 1, stride, off)  # past the buffer
