@@ -64,13 +64,32 @@ class Fib {
     static_assert(sizeof(*fib.entries().data()) == sizeof(lpm6cu_prefix), "Prefix layout mismatch");
   }
 
+  // PBT1 snapshot file (the reference's save_snapshot_file output) -> device FIB.
+  static Fib load_snapshot(int device, const std::string& path, uint32_t value_bytes = 0, void* stream = nullptr) {
+    lpm6cu_build_opts o{};
+    o.merge_adjacent = 1;
+    o.value_bytes = value_bytes;
+    Fib f;
+    lpm6cu::check(lpm6cu_fib_load_snapshot(device, path.c_str(), 0, &o, stream, &f.h_));
+    return f;
+  }
+
+  // Borrow a handle (a store snapshot's FIB): not destroyed by this object.
+  static Fib borrow(const lpm6cu_fib* h) {
+    Fib f;
+    f.h_ = const_cast<lpm6cu_fib*>(h);
+    f.owned_ = false;
+    return f;
+  }
+
   Fib(const Fib&) = delete;
   Fib& operator=(const Fib&) = delete;
-  Fib(Fib&& o) noexcept : h_(std::exchange(o.h_, nullptr)) {}
+  Fib(Fib&& o) noexcept : h_(std::exchange(o.h_, nullptr)), owned_(o.owned_) {}
   Fib& operator=(Fib&& o) noexcept {
     if (this != &o) {
       reset();
       h_ = std::exchange(o.h_, nullptr);
+      owned_ = o.owned_;
     }
     return *this;
   }
@@ -89,14 +108,93 @@ class Fib {
     lpm6cu::check(lpm6cu_lookup_batch(h_, addrs, n, out_next_hops, stream));
   }
 
+  // 8-byte keys (search_batch's input); device buffers.
+  void lookup_keys(const uint64_t* d_keys, uint64_t n, void* d_out, void* stream = nullptr) const {
+    lpm6cu::check(lpm6cu_lookup_keys(h_, d_keys, n, d_out, stream));
+  }
+
+  // Frames `stride` bytes apart, IPv6 destination at `dst_offset` (38 = Ethernet + IPv6); device buffers.
+  void lookup_packets(const void* d_frames, uint64_t n, uint64_t stride, uint32_t dst_offset, void* d_out,
+                      void* stream = nullptr) const {
+    lpm6cu::check(lpm6cu_lookup_packets(h_, d_frames, n, stride, dst_offset, d_out, stream));
+  }
+
   lpm6cu_fib* handle() const { return h_; }
 
  private:
+  Fib() = default;
   void reset() {
-    if (h_) lpm6cu_fib_destroy(h_);
+    if (h_ && owned_) lpm6cu_fib_destroy(h_);
     h_ = nullptr;
   }
   lpm6cu_fib* h_ = nullptr;
+  bool owned_ = true;
+};
+
+// The reference's FibStore on the GPU: stage / commit / acquire / release.
+class FibStore {
+ public:
+  template <class FibTable, class = decltype(std::declval<const FibTable&>().entries().data())>
+  FibStore(int device, const FibTable& fib, uint32_t value_bytes = 0) {
+    lpm6cu_build_opts o{};
+    o.merge_adjacent = 1;
+    o.value_bytes = value_bytes;
+    lpm6cu::check(lpm6cu_store_create(device, reinterpret_cast<const lpm6cu_prefix*>(fib.entries().data()),
+                                      fib.entries().size(), fib.default_next_hop(), &o, &h_));
+  }
+  FibStore(const FibStore&) = delete;
+  FibStore& operator=(const FibStore&) = delete;
+  ~FibStore() {
+    if (h_) lpm6cu_store_destroy(h_);
+  }
+
+  // RAII pin: lookups through fib() see one epoch; the destructor releases on the
+  // stream the snapshot was used on (set with use_on()).
+  class Snapshot {
+   public:
+    explicit Snapshot(lpm6cu_store* st) { lpm6cu::check(lpm6cu_store_acquire(st, &s_)); }
+    Snapshot(const Snapshot&) = delete;
+    Snapshot& operator=(const Snapshot&) = delete;
+    ~Snapshot() {
+      if (s_) lpm6cu_store_release(s_, stream_);
+    }
+    uint64_t epoch() const {
+      uint64_t e = 0;
+      lpm6cu::check(lpm6cu_snapshot_info(s_, &e, nullptr, nullptr));
+      return e;
+    }
+    Fib fib() const {
+      const lpm6cu_fib* f = nullptr;
+      lpm6cu::check(lpm6cu_snapshot_info(s_, nullptr, &f, nullptr));
+      return Fib::borrow(f);
+    }
+    void use_on(void* stream) { stream_ = stream; }
+
+   private:
+    lpm6cu_snapshot* s_ = nullptr;
+    void* stream_ = nullptr;
+  };
+
+  Snapshot acquire() const { return Snapshot(h_); }
+  // Returns the ops staged; op_status (optional, n entries) gets 0 or a status per op.
+  uint64_t stage(const lpm6_update_op* ops, uint64_t n, int32_t* op_status = nullptr) {
+    uint64_t staged = 0;
+    lpm6cu::check(lpm6cu_store_stage(h_, ops, n, &staged, op_status));
+    return staged;
+  }
+  uint64_t commit() {
+    uint64_t e = 0;
+    lpm6cu::check(lpm6cu_store_commit(h_, &e));
+    return e;
+  }
+  lpm6cu_store_stats stats() const {
+    lpm6cu_store_stats s{};
+    lpm6cu::check(lpm6cu_store_stats_get(h_, &s));
+    return s;
+  }
+
+ private:
+  lpm6cu_store* h_ = nullptr;
 };
 
 }  // namespace lpm6::gpu

@@ -4,6 +4,12 @@
 // results compared with the reference's own lookup_interval_oracle and
 // lookup_linear_oracle (intervals.cpp:95-145).
 //
+// Then the same for the update engine: random route changes are applied to the
+// reference FibTable with its own insert / erase / modify / insert_or_replace
+// (fib.cpp:120-161) and staged into lpm6::gpu::FibStore; per-op outcomes must
+// agree, and after each commit every lookup through the store's snapshot must
+// equal lookup_interval_oracle(build_intervals(updated reference FibTable)).
+//
 //   oracle/_ref/ref_dropin_demo [n_rules] [n_queries] [--no-gpu-ok]
 // exit 0 = every query matched (or, with --no-gpu-ok and no GPU, the library
 // refused with CudaError); 3 = a mismatch (the reference CLI's verify code).
@@ -72,7 +78,67 @@ int main(int argc, char** argv) {
     }
     std::printf("dropin: %zu rules, %zu intervals, %zu queries, %lu mismatches\n", fib.size(), ref_map.size(),
                 addrs.size(), static_cast<unsigned long>(bad));
-    return bad ? 3 : 0;
+    if (bad) return 3;
+
+    // ---- update engine against the reference FibTable mutators ----
+    lpm6::gpu::FibStore store(0, fib);
+    lpm6::FibTable ref = fib;
+    for (int round = 0; round < 3; ++round) {
+      std::vector<lpm6_update_op> ops;
+      std::vector<int> want_status;
+      for (int i = 0; i < 2000; ++i) {
+        lpm6_update_op op{};
+        const auto& cur = ref.entries();
+        lpm6::Prefix p;
+        if (!cur.empty() && rng() % 3 != 0) {
+          p = cur[rng() % cur.size()];
+        } else {
+          p.length = 16 + static_cast<int>(rng() % 49);
+          const lpm6::u128 mask = ~lpm6::u128(0) << (128 - p.length);
+          p.value = ((lpm6::u128(rng() | (1ull << 61)) << 64)) & mask;  // inside 2000::/3-ish, canonical
+        }
+        p.next_hop = 1 + static_cast<uint32_t>(rng() % 250);
+        op.kind = static_cast<uint32_t>(rng() % 4);
+        std::memcpy(&op.prefix, &p, sizeof p);
+        int st = 0;
+        try {
+          switch (op.kind) {
+            case LPM6_UPDATE_INSERT: ref.insert(p); break;
+            case LPM6_UPDATE_DELETE: ref.erase(p.value, p.length); break;
+            case LPM6_UPDATE_MODIFY: ref.modify(p.value, p.length, p.next_hop); break;
+            default: ref.insert_or_replace(p); break;
+          }
+        } catch (const lpm6::Error& err) {
+          st = static_cast<int>(err.code()) + 1;
+        }
+        ops.push_back(op);
+        want_status.push_back(st);
+      }
+      std::vector<int32_t> got_status(ops.size());
+      store.stage(ops.data(), ops.size(), got_status.data());
+      for (size_t i = 0; i < ops.size(); ++i)
+        if (got_status[i] != want_status[i]) {
+          std::printf("store: op %zu status %d, reference %d\n", i, got_status[i], want_status[i]);
+          return 3;
+        }
+      const uint64_t epoch = store.commit();
+      const lpm6::IntervalMap map = lpm6::build_intervals(ref);
+      auto snap = store.acquire();
+      const lpm6::gpu::Fib sf = snap.fib();
+      std::vector<uint8_t> o(addrs.size() * sf.value_bytes());
+      sf.lookup_batch(addrs.data(), addrs.size(), o.data());
+      uint64_t sbad = 0;
+      for (size_t i = 0; i < addrs.size(); ++i) {
+        uint32_t got = 0;
+        std::memcpy(&got, o.data() + i * sf.value_bytes(), sf.value_bytes());
+        if (got != lpm6::lookup_interval_oracle(map, static_cast<uint64_t>(addrs[i] >> 64)) && sbad++ < 5)
+          std::printf("store mismatch at %zu\n", i);
+      }
+      std::printf("store: epoch %lu, %zu rules, %zu intervals, %lu mismatches\n", static_cast<unsigned long>(epoch),
+                  ref.size(), map.size(), static_cast<unsigned long>(sbad));
+      if (sbad || epoch != static_cast<uint64_t>(round) + 2) return 3;
+    }
+    return 0;
   } catch (const lpm6cu::Error& err) {
     std::printf("dropin: %s\n", err.what());
     return (no_gpu_ok && err.status() == LPM6CU_E_CUDA) ? 0 : 1;

@@ -242,3 +242,5 @@ def test_reference_dropin(cuda):
     r = subprocess.run([str(exe), "50000", "2000000"], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert " 0 mismatches" in r.stdout
+    # the store phase: per-op outcomes equal the reference FibTable mutators', 3 commits
+    assert r.stdout.count("store: epoch") == 3 and "store: epoch 4" in r.stdout
