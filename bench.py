@@ -52,6 +52,7 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also time every kernel shape (extra key)")
+    ap.add_argument("--no-extras", action="store_true", help="skip the key/packet-input and store timings")
     return ap.parse_args()
 
 
@@ -154,6 +155,64 @@ def device_build_ms(lpm, fib, device, vb, reps=3):
         torch.cuda.synchronize()
         best = min(best, (time.perf_counter() - t0) * 1e3)
     return best
+
+
+def _time_ms(torch, fn, stream, reps=3):
+    fn()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record(stream)
+    for _ in range(reps):
+        fn()
+    a1.record(stream)
+    torch.cuda.synchronize()
+    return a0.elapsed_time(a1) / reps
+
+
+def time_extras(lpm, torch, fdev, fib, addrs, n, vb, stream, device):
+    """The same workload through the other inputs (8-byte keys; 64-byte Ethernet+IPv6
+    frames) and the update store's commit latency. Each result is checked against
+    the address path's output."""
+    out = {}
+    ref = fdev.lookup_batch(addrs, None, stream)
+    keys = addrs[:, 8:16].contiguous().view(torch.int64).reshape(-1)
+    ko = torch.empty_like(ref)
+    ms = _time_ms(torch, lambda: fdev.lookup_keys(keys, ko, stream), stream)
+    out["keys8"] = {"value": n / ms / 1e6, "unit": UNIT, "ms": ms, "dram_bytes_per_query": 8 + vb,
+                    "matches_address_path": bool(torch.equal(ko, ref))}
+    del keys, ko
+    m = min(n, 1 << 26)
+    frames = torch.zeros((m, 64), dtype=torch.uint8, device=addrs.device)
+    frames[:, 12] = 0x86  # EtherType 0x86DD
+    frames[:, 13] = 0xDD
+    frames[:, 14] = 0x60  # IPv6 version
+    frames[:, 38:54] = torch.flip(addrs[:m], dims=[1])  # destination, network byte order
+    frames = frames.reshape(-1)
+    po = torch.empty(m * vb, dtype=torch.uint8, device=addrs.device)
+    ms = _time_ms(torch, lambda: fdev.lookup_packets(frames, m, 64, 38, po, stream), stream)
+    out["packets64"] = {"value": m / ms / 1e6, "unit": UNIT, "frames": m, "stride": 64, "dst_offset": 38, "ms": ms,
+                        "matches_address_path": bool(torch.equal(po, ref.view(torch.uint8)[: m * vb]))}
+    del frames, po
+    # store: create (device build) + commits of 1,000 announces each
+    from paper_2604_14650_b200.fib import Prefix
+    st = lpm.FibStore(fib, device, value_bytes=vb)
+    rng = np.random.default_rng(1)
+    rules = fib.rules
+    commits = []
+    for _ in range(3):
+        idx = rng.integers(0, len(rules), 1000)
+        ops = [lpm.UpdateOp(3, Prefix(int(rules[i]["value_hi"]) << 64, int(rules[i]["length"]),
+                                      int(rng.integers(1, 255)))) for i in idx]
+        st.stage(ops)
+        t0 = time.perf_counter()
+        st.commit()
+        commits.append((time.perf_counter() - t0) * 1e3)
+    s = st.stats
+    out["store_commit"] = {"ops_per_commit": 1000, "commit_ms": commits, "device_build_ms": s.last_build_ms,
+                           "publish_us": s.last_publish_us, "epoch": s.epoch,
+                           "note": "stage 1,000 announces, rebuild the whole FIB on the GPU, publish; "
+                                   "paper quotes 850 ms for a 1M-prefix rebuild (P:1334-1335)"}
+    st.close()
+    return out
 
 
 def measured_traffic(workload, n):
@@ -525,6 +584,11 @@ def main():
                                ctas_per_sm=args.ctas_per_sm, queries_per_lane=args.queries_per_lane,
                                min_ctas_per_sm=args.min_ctas, threads_per_cta=args.threads)
 
+    # -- other inputs and the update store (rank 0; extra keys, not the headline) ---------------------
+    extras = None
+    if rank == 0 and not args.no_extras:
+        extras = time_extras(lpm, torch, fdev, fib, addrs, n, vb, stream, dev_index)
+
     # -- CPU baseline (rank 0, N = 1) ---------------------------------------------------------------------
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -582,6 +646,8 @@ def main():
     }
     if sweep is not None:
         line["sweep"] = sweep
+    if extras is not None:
+        line["extras"] = extras
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()

@@ -113,20 +113,56 @@ __device__ __forceinline__ unsigned long long bswap64(unsigned long long v) {
   return (static_cast<unsigned long long>(__byte_perm(lo, 0, 0x0123)) << 32) | __byte_perm(hi, 0, 0x0123);
 }
 
+__device__ __forceinline__ uint4 ld_stream_v4u(const void* p, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+
+// Bytes [sh, sh + 8) of the little-endian pair (w0, w1), sh in 0..8.
+__device__ __forceinline__ unsigned long long extract8(unsigned long long w0, unsigned long long w1, unsigned sh) {
+  return sh == 0 ? w0 : sh >= 8 ? w1 : (w0 >> (8 * sh)) | (w1 << (64 - 8 * sh));
+}
+
 // Top 64 bits of an IPv6 address stored in network byte order (the first 8
-// bytes of the destination field) at an address aligned to `align` bytes.
-__device__ __forceinline__ unsigned long long load_dst_key(const unsigned char* a, unsigned align, uint64_t pol) {
+// bytes of the destination field) at frame + off, where every frame start is
+// aligned to `align` bytes (16, 8, 4, 2 or 1; uniform across the launch). The
+// 8 key bytes are fetched with as few aligned loads as cover them — one 16-byte
+// load when they sit inside one aligned 16-byte chunk — because every load
+// instruction of a warp costs one L1 wavefront per distinct line it touches.
+__device__ __forceinline__ unsigned long long load_dst_key(const unsigned char* frame, unsigned off, unsigned align,
+                                                           uint64_t pol) {
   unsigned long long le;  // the 8 bytes as a little-endian integer
-  if (align >= 8) {
-    le = ld_stream<unsigned long long>(a, pol);
-  } else if (align >= 4) {
+  if (align >= 16) {
+    const unsigned sh = off & 15u;
+    const unsigned char* c = frame + (off - sh);
+    const uint4 v = ld_stream_v4u(c, pol);
+    const unsigned long long w0 = v.x | (static_cast<unsigned long long>(v.y) << 32);
+    const unsigned long long w1 = v.z | (static_cast<unsigned long long>(v.w) << 32);
+    if (sh <= 8) {
+      le = extract8(w0, w1, sh);
+    } else {
+      const unsigned long long w2 = ld_stream<unsigned long long>(c + 16, pol);
+      le = extract8(w1, w2, sh - 8);
+    }
+  } else if (align >= 8) {
+    const unsigned sh = off & 7u;
+    const unsigned char* c = frame + (off - sh);
+    const unsigned long long w0 = ld_stream<unsigned long long>(c, pol);
+    le = sh ? extract8(w0, ld_stream<unsigned long long>(c + 8, pol), sh) : w0;
+  } else if (align >= 4 && (off & 3u) == 0) {
+    const unsigned char* a = frame + off;
     le = ld_stream<unsigned>(a, pol) | (static_cast<unsigned long long>(ld_stream<unsigned>(a + 4, pol)) << 32);
-  } else if (align >= 2) {
+  } else if (align >= 2 && (off & 1u) == 0) {
+    const unsigned char* a = frame + off;
     le = 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
       le |= static_cast<unsigned long long>(ld_stream<unsigned short>(a + 2 * i, pol)) << (16 * i);
   } else {
+    const unsigned char* a = frame + off;
     le = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) le |= static_cast<unsigned long long>(__ldg(a + i)) << (8 * i);
@@ -181,7 +217,7 @@ struct LookupParams {
   const unsigned char* pkts;        // kInPacket: frames, destination address at pkt_off of each
   unsigned long long pkt_stride;    //   bytes between frames
   unsigned int pkt_off;             //   byte offset of the IPv6 destination address in a frame
-  unsigned int pkt_align;           //   8, 4, 2 or 1: alignment of every destination address
+  unsigned int pkt_align;           //   16, 8, 4, 2 or 1: alignment of every frame start
   unsigned char* out;
   unsigned long long n;
   const unsigned long long* image;  // packed 15-key copy of internal levels 0.. (layout.hpp)
@@ -306,7 +342,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
       if constexpr (INPUT == kInKey) {
         k = ld_stream_u64(p.keys + qi, pol_stream);
       } else if constexpr (INPUT == kInPacket) {
-        k = load_dst_key(p.pkts + qi * p.pkt_stride + p.pkt_off, p.pkt_align, pol_stream);
+        k = load_dst_key(p.pkts + qi * p.pkt_stride, p.pkt_off, p.pkt_align, pol_stream);
       } else {
         const uint4 a = ld_stream_v4(p.addrs + qi, pol_stream);
         k = (static_cast<unsigned long long>(a.w) << 32) | a.z;
@@ -864,8 +900,8 @@ int lpm6cu_lookup_packets(const lpm6cu_fib* fib, const void* frames, uint64_t n,
     PacketInput pk;
     pk.stride = stride;
     pk.off = dst_offset;
-    const unsigned long long bits = (reinterpret_cast<uintptr_t>(frames) + dst_offset) | stride;
-    pk.align = (bits & 7) == 0 ? 8 : (bits & 3) == 0 ? 4 : (bits & 1) == 0 ? 2 : 1;
+    const unsigned long long bits = reinterpret_cast<uintptr_t>(frames) | stride;  // frame-start alignment
+    pk.align = (bits & 15) == 0 ? 16 : (bits & 7) == 0 ? 8 : (bits & 3) == 0 ? 4 : (bits & 1) == 0 ? 2 : 1;
     launch_lookup(fib, frames, n, out, static_cast<cudaStream_t>(stream), kInPacket, &pk);
   });
 }

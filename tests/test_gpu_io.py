@@ -119,7 +119,7 @@ def make_frames(addrs: np.ndarray, stride: int, dst_offset: int, rng) -> np.ndar
     return frames.reshape(-1)
 
 
-@pytest.mark.parametrize("stride,off", [(64, 38), (80, 40), (72, 36), (66, 38), (65, 38), (128, 22)])
+@pytest.mark.parametrize("stride,off", [(64, 38), (80, 40), (72, 36), (66, 38), (65, 38), (128, 22), (64, 44), (48, 30), (72, 38), (68, 36)])
 def test_lookup_packets_matches_oracle(lpm, orc, cuda, stride, off):
     """Packet ingest: the destination read straight from frames at every alignment
     (8/4/2/1) gives the oracle's next hops (Ethernet + IPv6: offset 38)."""
