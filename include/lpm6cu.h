@@ -223,6 +223,21 @@ int lpm6_snapshot_save(const uint64_t* boundaries, const uint32_t* next_hops, ui
 /* Validate a PBT1 image and extract its interval map (arrays NULL: *m, *k only). */
 int lpm6_snapshot_decode(const void* buf, uint64_t size, uint64_t* boundaries, uint32_t* next_hops, uint64_t cap,
                          uint64_t* m, uint32_t* k);
+/* memory_footprint (tree.hpp:76-88): exact bytes of each array. */
+typedef struct {
+  uint64_t leaf_bytes;     /* leaf keys (B200: whole leaf lines, next hops included) */
+  uint64_t internal_bytes; /* internal levels */
+  uint64_t value_bytes;    /* separate value array (reference: u32 per leaf slot; B200: 0) */
+  uint64_t image_bytes;    /* B200: the shared-memory image copy (reference: 0) */
+  uint64_t total_bytes;
+  double bytes_per_interval;
+  uint64_t total_bytes_value8;       /* with 8-byte value slots (the paper's 18 B/interval basis) */
+  double bytes_per_interval_value8;
+} lpm6cu_footprint;
+int lpm6_memory_footprint(const lpm6cu_geometry* g, lpm6cu_footprint* out);
+/* The reference layout's footprint for m intervals at k keys per node. */
+int lpm6_ref_memory_footprint(uint64_t m, uint32_t k, lpm6cu_footprint* out);
+
 /* PBT1 file -> device FIB without an interval sweep (load_snapshot_file, tree.hpp:96). */
 int lpm6cu_fib_load_snapshot(int device, const char* path, uint32_t default_next_hop, const lpm6cu_build_opts* opts,
                              void* stream, lpm6cu_fib** out);

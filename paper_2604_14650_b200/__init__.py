@@ -6,7 +6,8 @@ replicates the FIB across GPUs. See DESIGN.md.
 """
 from ._lib import Lpm6Error
 from .fib import (FibTable, Geometry, IntervalMap, Prefix, Tree, WORKLOADS, build_intervals, build_tree,
-                  decode_snapshot, encode_snapshot, load_fib, parse_prefix, plan_layout, save_snapshot, save_trace,
+                  decode_snapshot, encode_snapshot, load_fib, parse_prefix, plan_layout, ref_memory_footprint,
+                  save_snapshot, save_trace,
                   trace_count, workload_fib, workload_info, workload_queries_host)
 from .gpu import Fib, QueryGen, load_trace, probe_l2_gather, probe_smem
 from .store import FibStore, Snapshot, UpdateOp, apply_updates, load_update_trace, parse_update
@@ -16,5 +17,5 @@ __all__ = [
     "build_tree", "load_fib", "parse_prefix", "plan_layout", "workload_fib", "workload_info",
     "workload_queries_host", "Fib", "QueryGen", "probe_l2_gather", "probe_smem", "FibStore", "Snapshot",
     "UpdateOp", "apply_updates", "load_update_trace", "parse_update", "decode_snapshot", "encode_snapshot",
-    "save_snapshot", "save_trace", "trace_count", "load_trace",
+    "save_snapshot", "save_trace", "trace_count", "load_trace", "ref_memory_footprint",
 ]

@@ -70,6 +70,12 @@ class StoreStats_t(C.Structure):
                 ("last_build_ms", C.c_double), ("last_publish_us", C.c_double)]
 
 
+class Footprint_t(C.Structure):
+    _fields_ = [("leaf_bytes", C.c_uint64), ("internal_bytes", C.c_uint64), ("value_bytes", C.c_uint64),
+                ("image_bytes", C.c_uint64), ("total_bytes", C.c_uint64), ("bytes_per_interval", C.c_double),
+                ("total_bytes_value8", C.c_uint64), ("bytes_per_interval_value8", C.c_double)]
+
+
 P = C.c_void_p
 U64 = C.c_uint64
 U32 = C.c_uint32
@@ -114,6 +120,8 @@ SIGNATURES = {
     "lpm6_snapshot_decode": (I32, [P, U64, P, P, U64, C.POINTER(U64), C.POINTER(U32)]),
     "lpm6cu_fib_load_snapshot": (I32, [I32, C.c_char_p, U32, C.POINTER(BuildOpts_t), P, C.POINTER(P)]),
     "lpm6_trace_save": (I32, [P, U64, C.c_char_p]),
+    "lpm6_memory_footprint": (I32, [C.POINTER(Geometry_t), C.POINTER(Footprint_t)]),
+    "lpm6_ref_memory_footprint": (I32, [U64, U32, C.POINTER(Footprint_t)]),
     "lpm6_trace_count": (I32, [P, U64, C.POINTER(U64)]),
     "lpm6cu_trace_load": (I32, [I32, C.c_char_p, P, U64, C.POINTER(U64), P]),
     "lpm6_parse_update": (I32, [C.c_char_p, C.POINTER(UpdateOp_t)]),

@@ -92,6 +92,37 @@ int lpm6cu_fib_load_snapshot(int device, const char* path, uint32_t default_nh, 
   });
 }
 
+int lpm6_memory_footprint(const lpm6cu_geometry* g, lpm6cu_footprint* out) {
+  return guard([&] {
+    if (!g || !out) throw Error(Errc::InvalidArgument, "NULL argument");
+    std::memset(out, 0, sizeof *out);
+    out->internal_bytes = g->level_start[g->depth] * 8;
+    out->leaf_bytes = g->leaf_nodes * 128;  // next hops are inside the leaf lines
+    out->value_bytes = 0;
+    out->image_bytes = (g->total_words - g->image_start) * 8;
+    out->total_bytes = g->total_words * 8;
+    out->bytes_per_interval = g->num_keys ? double(out->total_bytes) / double(g->num_keys) : 0.0;
+    out->total_bytes_value8 = out->total_bytes;  // no separate value array to widen
+    out->bytes_per_interval_value8 = out->bytes_per_interval;
+  });
+}
+
+int lpm6_ref_memory_footprint(uint64_t m, uint32_t k, lpm6cu_footprint* out) {
+  return guard([&] {
+    if (!out) throw Error(Errc::InvalidArgument, "NULL argument");
+    const RefGeometry g = plan_ref_geometry(m, k);
+    std::memset(out, 0, sizeof *out);
+    const uint64_t slots = g.allocated_leaf_nodes * k;
+    out->leaf_bytes = slots * 8;
+    out->internal_bytes = g.leaf_start * 8;
+    out->value_bytes = slots * 4;
+    out->total_bytes = out->leaf_bytes + out->internal_bytes + out->value_bytes;
+    out->bytes_per_interval = m ? double(out->total_bytes) / double(m) : 0.0;
+    out->total_bytes_value8 = out->leaf_bytes + out->internal_bytes + slots * 8;
+    out->bytes_per_interval_value8 = m ? double(out->total_bytes_value8) / double(m) : 0.0;
+  });
+}
+
 int lpm6_trace_save(const uint64_t* keys, uint64_t n, const char* path) {
   return guard([&] {
     if (!path || (n && !keys)) throw Error(Errc::InvalidArgument, "NULL argument");

@@ -188,6 +188,22 @@ class Geometry:
     def tree_bytes(self) -> int:
         return self.total_words * 8
 
+    def memory_footprint(self) -> dict:
+        """Exact bytes of the B200 layout (memory_footprint, tree.hpp:76-88)."""
+        from ._lib import Footprint_t
+        f = Footprint_t()
+        g = self.to_c()
+        check(lib().lpm6_memory_footprint(C.byref(g), C.byref(f)))
+        return {k: getattr(f, k) for k, _ in Footprint_t._fields_}
+
+
+def ref_memory_footprint(m: int, k: int = 8) -> dict:
+    """memory_footprint of the reference's layout for m intervals."""
+    from ._lib import Footprint_t
+    f = Footprint_t()
+    check(lib().lpm6_ref_memory_footprint(m, k, C.byref(f)))
+    return {name: getattr(f, name) for name, _ in Footprint_t._fields_}
+
 
 def plan_layout(m: int, value_bytes: int = 1) -> Geometry:
     g = Geometry_t()

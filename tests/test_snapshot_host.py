@@ -167,3 +167,23 @@ def test_trace_format(lpm, tmp_path):
         with pytest.raises(lpm.Lpm6Error) as e:
             lpm.trace_count(b)
         assert e.value.code == "BadTraceFile", name
+
+
+def test_memory_footprint(lpm):
+    # full depth-5 tree, m = 472,392, k = 8: leaf 3,779,136 B, internal 472,384 B
+    f = lpm.ref_memory_footprint(472392, 8)
+    assert f["leaf_bytes"] == 3779136 and f["internal_bytes"] == 472384
+    assert f["value_bytes"] == 472392 * 4 and f["total_bytes"] == 3779136 + 472384 + 472392 * 4
+    assert abs(f["bytes_per_interval_value8"] - 18.0) / 18.0 < 0.10  # the paper's "18 bytes"
+    # m = 5 -> 64 B of keys + value bytes
+    f5 = lpm.ref_memory_footprint(5, 8)
+    assert f5["leaf_bytes"] + f5["internal_bytes"] == 64 and f5["total_bytes"] == 64 + 32
+    # the reference footprint equals the bytes of its PBT1 snapshot minus the 26-byte header
+    imap = lpm.build_intervals(lpm.workload_fib(0))
+    assert lpm.ref_memory_footprint(len(imap))["total_bytes"] == len(lpm.encode_snapshot(imap)) - 26
+    # B200 layout: every byte of the line array accounted for
+    tree = lpm.build_tree(imap)
+    g = tree.geometry
+    b = g.memory_footprint()
+    assert b["total_bytes"] == g.total_words * 8 == b["internal_bytes"] + b["leaf_bytes"] + b["image_bytes"]
+    assert b["bytes_per_interval"] == b["total_bytes"] / len(imap)
