@@ -53,6 +53,9 @@ def parse_args():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also time every kernel shape (extra key)")
     ap.add_argument("--no-extras", action="store_true", help="skip the key/packet-input and store timings")
+    ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
+                    help="replay each step's launch from a CUDA graph (auto: batches under 2^24 queries, "
+                         "where the host launch path would otherwise bound the step)")
     return ap.parse_args()
 
 
@@ -494,8 +497,18 @@ def main():
 
     stream = torch.cuda.current_stream()
 
-    def step():
-        fdev.lookup_batch(addrs, out, stream)
+    def launch(s=stream):
+        fdev.lookup_batch(addrs, out, s)
+
+    step = launch
+    use_graph = args.graph == "on" or (args.graph == "auto" and n < (1 << 24))
+    if use_graph:
+        launch()  # resolves and caches the launch plan outside the capture
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):  # captured on torch's side stream, replayed on the current one
+            launch(torch.cuda.current_stream())
+        step = graph.replay
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -637,6 +650,7 @@ def main():
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": args.steps,
+        "cuda_graph": use_graph,
         "clocks": clk.summary(),
         "parity_sample": parity,
         "fib_build_ms": build_ms,

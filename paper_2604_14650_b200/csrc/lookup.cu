@@ -515,6 +515,15 @@ struct HostPipeline {
   unsigned long long chunk = 0;
 };
 
+// Kernel choice, occupancy and the dynamic-smem attribute for one input format
+// and checked flag: resolved on the first launch, reused until the kernel
+// config changes (the launch path then does no driver queries).
+struct LaunchPlan {
+  bool valid = false;
+  void (*fn)(const LookupParams) = nullptr;
+  int per_sm = 0;
+};
+
 struct lpm6cu_fib {
   int device = 0;
   lpm6cu_geometry g{};
@@ -526,6 +535,14 @@ struct lpm6cu_fib {
   size_t max_smem_optin = 0;
   std::mutex host_mu;
   std::unique_ptr<HostPipeline> pipe;
+  std::mutex plan_mu;
+  LaunchPlan plans[3][2];  // [input format][checked]
+
+  void invalidate_plans() {
+    std::lock_guard<std::mutex> lk(plan_mu);
+    for (auto& row : plans)
+      for (auto& pl : row) pl = LaunchPlan{};
+  }
 
   ~lpm6cu_fib() {
     int prev = -1;
@@ -608,6 +625,7 @@ void resolve_config(lpm6cu_fib* f, const lpm6cu_kernel_config* req) {
     throw Error(Errc::InvalidArgument, "smem_levels=" + std::to_string(c.smem_levels) + " needs " +
                                            std::to_string(staged) + " B of shared memory");
   f->cfg = c;
+  f->invalidate_plans();
 }
 
 unsigned long long staged_bytes(const lpm6cu_fib* f) { return image_bytes_of(f->g, f->cfg.smem_levels); }
@@ -626,9 +644,30 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
   const unsigned tiles = dflt ? 1 : f->cfg.queries_per_lane;
   const unsigned threads_cta = dflt ? 1024 : f->cfg.threads_per_cta;
   const unsigned minb = dflt ? 1 : f->cfg.min_ctas_per_sm;
-  KernelFn fn = pick_kernel(static_cast<int>(f->g.value_bytes), static_cast<int>(f->g.depth), static_cast<int>(tiles),
-                            static_cast<int>(threads_cta), static_cast<int>(minb), f->d_err != nullptr, input);
-  if (!fn) throw Error(Errc::InvalidArgument, "no kernel instantiated for this configuration");
+  const size_t smem = staged_bytes(f);
+  const int threads = static_cast<int>(threads_cta);
+  LaunchPlan plan;
+  {
+    auto* mf = const_cast<lpm6cu_fib*>(f);
+    std::lock_guard<std::mutex> lk(mf->plan_mu);
+    LaunchPlan& slot = mf->plans[input][f->d_err != nullptr ? 1 : 0];
+    if (!slot.valid) {
+      KernelFn fn = pick_kernel(static_cast<int>(f->g.value_bytes), static_cast<int>(f->g.depth),
+                                static_cast<int>(tiles), threads, static_cast<int>(minb), f->d_err != nullptr, input);
+      if (!fn) throw Error(Errc::InvalidArgument, "no kernel instantiated for this configuration");
+      if (smem > 48 * 1024)
+        check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+                   "cudaFuncSetAttribute");
+      int per_sm = 0;
+      check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem), "occupancy");
+      if (per_sm < 1) throw Error(Errc::CudaError, "lookup kernel cannot be resident with this configuration");
+      if (f->cfg.ctas_per_sm > 0) per_sm = std::min<int>(per_sm, static_cast<int>(f->cfg.ctas_per_sm));
+      slot.fn = fn;
+      slot.per_sm = per_sm;
+      slot.valid = true;
+    }
+    plan = slot;
+  }
   LookupParams p{};
   p.lines = f->d_lines;
   for (int l = 0; l < LPM6CU_MAX_LEVELS; ++l) p.level_start[l] = f->g.level_start[l];
@@ -649,20 +688,11 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
   p.image = f->d_lines + f->g.image_start;
   for (int l = 0; l < LPM6CU_MAX_LEVELS; ++l) p.level_nodes[l] = f->g.level_nodes[l];
   p.err = f->d_err;
-  const int threads = static_cast<int>(threads_cta);
-  const size_t smem = p.smem_bytes;
-  if (smem > 48 * 1024)
-    check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
-               "cudaFuncSetAttribute");
-  int per_sm = 0;
-  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem), "occupancy");
-  if (per_sm < 1) throw Error(Errc::CudaError, "lookup kernel cannot be resident with this configuration");
-  if (f->cfg.ctas_per_sm > 0) per_sm = std::min<int>(per_sm, static_cast<int>(f->cfg.ctas_per_sm));
   const unsigned long long ntiles = (n + 32ull * tiles - 1) / (32ull * tiles);
   const unsigned long long warps_per_cta = threads / 32;
-  unsigned long long grid = static_cast<unsigned long long>(f->num_sms) * per_sm;
+  unsigned long long grid = static_cast<unsigned long long>(f->num_sms) * plan.per_sm;
   grid = std::min(grid, (ntiles + warps_per_cta - 1) / warps_per_cta);
-  fn<<<static_cast<unsigned>(grid), threads, smem, stream>>>(p);
+  plan.fn<<<static_cast<unsigned>(grid), threads, smem, stream>>>(p);
   check_cuda(cudaGetLastError(), "lookup launch");
 }
 
@@ -840,6 +870,7 @@ int lpm6cu_fib_set_checked(lpm6cu_fib* f, int on) {
       check_cuda(cudaFree(f->d_err), "cudaFree err");
       f->d_err = nullptr;
     }
+    f->invalidate_plans();
   });
 }
 

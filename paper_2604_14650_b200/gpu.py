@@ -54,6 +54,7 @@ class Fib:
         self.device = device
         self._keepalive = keepalive
         self._owned = owned  # False: a store snapshot's FIB, freed by the store
+        self._vb = None      # next-hop width, cached (a FIB is immutable)
 
     # -- construction ---------------------------------------------------------
     @classmethod
@@ -129,6 +130,12 @@ class Fib:
 
     # -- introspection --------------------------------------------------------
     @property
+    def value_bytes(self) -> int:
+        if self._vb is None:
+            self._vb = self.geometry.value_bytes
+        return self._vb
+
+    @property
     def geometry(self) -> Geometry:
         g = Geometry_t()
         check(lib().lpm6cu_fib_geometry(self._h, C.byref(g)))
@@ -180,7 +187,7 @@ class Fib:
         torch's current stream). Host buffers: pipelined copy-in/lookup/copy-out,
         returns when ``out`` is filled.
         """
-        vb = self.geometry.value_bytes
+        vb = self.value_bytes
         aptr, n, adev = _ptr_len(addrs, 16)
         if out is None:
             if adev:
@@ -202,7 +209,7 @@ class Fib:
     def lookup_keys(self, keys, out=None, stream=None):
         """Next hops of n 8-byte keys (search_batch's input): device buffers,
         one asynchronous kernel launch on ``stream``."""
-        vb = self.geometry.value_bytes
+        vb = self.value_bytes
         kptr, n, kdev = _ptr_len(keys, 8)
         if out is None:
             torch = _torch()
@@ -217,7 +224,7 @@ class Fib:
     def lookup_packets(self, frames, n: int, stride: int, dst_offset: int = 38, out=None, stream=None):
         """Next hops of n frames ``stride`` bytes apart in a device buffer, the IPv6
         destination at ``dst_offset`` (network order; 38 = Ethernet + IPv6)."""
-        vb = self.geometry.value_bytes
+        vb = self.value_bytes
         fptr, nbytes, fdev = _ptr_len(frames, 1)
         if n and (n - 1) * stride + dst_offset + 16 > nbytes:
             raise Lpm6Error(9, "frame buffer too small for n frames")
