@@ -195,6 +195,23 @@ def time_extras(lpm, torch, fdev, fib, addrs, n, vb, stream, device):
     out["packets64"] = {"value": m / ms / 1e6, "unit": UNIT, "frames": m, "stride": 64, "dst_offset": 38, "ms": ms,
                         "matches_address_path": bool(torch.equal(po, ref.view(torch.uint8)[: m * vb]))}
     del frames, po
+    # serving-size batches through the C ABI (device buffers): back-to-back calls and call-to-result
+    small = []
+    for b in (256, 4096, 65536):
+        if b > n:
+            continue
+        sub, so = addrs[:b], torch.empty(b * vb, dtype=torch.uint8, device=addrs.device)
+        ms = _time_ms(torch, lambda: fdev.lookup_batch(sub, so, stream), stream, reps=200)
+        lat = []
+        for _ in range(50):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fdev.lookup_batch(sub, so, stream)
+            torch.cuda.synchronize()
+            lat.append((time.perf_counter() - t0) * 1e6)
+        small.append({"batch": b, "us_per_call_back_to_back": ms * 1e3, "us_call_to_result_median": float(np.median(lat)),
+                      "glps_back_to_back": b / ms / 1e6})
+    out["small_batches"] = small
     # store: create (device build) + commits of 1,000 announces each
     from paper_2604_14650_b200.fib import Prefix
     st = lpm.FibStore(fib, device, value_bytes=vb)
