@@ -161,6 +161,16 @@ int lpm6cu_fib_create(int device, const lpm6cu_geometry* g, const uint64_t* line
  * freed by lpm6cu_fib_destroy. */
 int lpm6cu_fib_wrap_device(int device, const lpm6cu_geometry* g, const void* d_lines, lpm6cu_fib** out);
 
+/* Like wrap_device, but the handle takes ownership: cudaFree on destroy. */
+int lpm6cu_fib_adopt_device(int device, const lpm6cu_geometry* g, void* d_lines, lpm6cu_fib** out);
+
+/* Single-process replication: broadcast src's line array to
+ * devices[1..ndev-1] with one grouped ncclBroadcast over NVLink (devices[0] must
+ * be src's device; out[0] is a fresh copy there). NCCL is loaded at run time
+ * (libnccl.so.2); failures report LPM6CU_E_NCCL. The one-process-per-GPU path
+ * broadcasts the same array with torch.distributed (dispatch.py). */
+int lpm6cu_fib_replicate(const lpm6cu_fib* src, const int* devices, int ndev, lpm6cu_fib** out);
+
 int lpm6cu_fib_geometry(const lpm6cu_fib* fib, lpm6cu_geometry* g);
 int lpm6cu_fib_device_lines(const lpm6cu_fib* fib, const void** d_lines);
 /* Copy the device line array (g.total_words u64 words) to host memory. */

@@ -95,6 +95,8 @@ SIGNATURES = {
     "lpm6cu_build_intervals_device": (I32, [I32, P, U64, U32, I32, P, P, U64, C.POINTER(U64)]),
     "lpm6cu_fib_create": (I32, [I32, C.POINTER(Geometry_t), P, C.POINTER(P)]),
     "lpm6cu_fib_wrap_device": (I32, [I32, C.POINTER(Geometry_t), P, C.POINTER(P)]),
+    "lpm6cu_fib_adopt_device": (I32, [I32, C.POINTER(Geometry_t), P, C.POINTER(P)]),
+    "lpm6cu_fib_replicate": (I32, [P, C.POINTER(I32), I32, P]),
     "lpm6cu_fib_geometry": (I32, [P, C.POINTER(Geometry_t)]),
     "lpm6cu_fib_device_lines": (I32, [P, C.POINTER(P)]),
     "lpm6cu_fib_copy_lines": (I32, [P, P, U64]),

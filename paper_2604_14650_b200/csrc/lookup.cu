@@ -785,6 +785,19 @@ int lpm6cu_fib_wrap_device(int device, const lpm6cu_geometry* g, const void* d_l
   });
 }
 
+int lpm6cu_fib_adopt_device(int device, const lpm6cu_geometry* g, void* d_lines, lpm6cu_fib** out) {
+  return guard([&] {
+    if (!d_lines || !out) throw Error(Errc::InvalidArgument, "NULL argument");
+    if (reinterpret_cast<uintptr_t>(d_lines) % 128 != 0)
+      throw Error(Errc::InvalidArgument, "device lines must be 128-byte aligned");
+    DeviceGuard dg(device);
+    std::unique_ptr<lpm6cu_fib> f(new_fib(device, g));
+    f->d_lines = static_cast<unsigned long long*>(d_lines);
+    f->owns = true;
+    *out = f.release();
+  });
+}
+
 int lpm6cu_fib_build(int device, const lpm6cu_prefix* rules, uint64_t n, uint32_t default_nh,
                      const lpm6cu_build_opts* opts, lpm6cu_fib** out) {
   return guard([&] {

@@ -116,6 +116,14 @@ class Fib:
         check(lib().lpm6cu_fib_wrap_device(device, C.byref(g), lines.data_ptr(), C.byref(h)))
         return cls(h.value, device, keepalive=lines)
 
+    def replicate(self, devices) -> list["Fib"]:
+        """Copies of this FIB on `devices` (devices[0] = this FIB's device) by one
+        grouped NCCL broadcast in this process (lpm6cu_fib_replicate)."""
+        devs = (C.c_int * len(devices))(*devices)
+        outs = (C.c_void_p * len(devices))()
+        check(lib().lpm6cu_fib_replicate(self._h, devs, len(devices), outs))
+        return [Fib(outs[i], devices[i]) for i in range(len(devices))]
+
     def close(self) -> None:
         if self._h and self._h.value:
             if self._owned:

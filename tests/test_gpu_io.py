@@ -140,3 +140,27 @@ def test_lookup_packets_matches_oracle(lpm, orc, cuda, stride, off):
         np.testing.assert_array_equal(out.cpu().numpy().astype(np.uint32), want)
     with pytest.raises(lpm.Lpm6Error):
         dev.lookup_packets(frames, len(addrs) + 1, stride, off)  # past the buffer
+
+
+def test_single_process_nccl_replication(lpm, orc, cuda):
+    """lpm6cu_fib_replicate: one grouped NCCL broadcast per call (here over the one
+    visible GPU; the same call fans out to every device of a node)."""
+    torch = cuda
+    fib = lpm.workload_fib(1)
+    src = lpm.Fib.build(fib)
+    devices = list(range(torch.cuda.device_count()))
+    reps = src.replicate(devices)
+    assert len(reps) == len(devices)
+    want_lines = device_lines(src)
+    for r in reps:
+        assert r.geometry == src.geometry
+        np.testing.assert_array_equal(device_lines(r), want_lines)
+    imap = lpm.build_intervals(fib)
+    keys = np.random.default_rng(3).integers(0, 2**64, 1 << 16, dtype=np.uint64)
+    want, _ = orc.lookup_batch(0, imap.boundaries, imap.next_hops, addrs_from_keys(keys), threads=8)
+    got = reps[0].lookup_keys(torch.from_numpy(keys.view(np.int64)).cuda())
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(got.cpu().numpy().astype(np.uint32), want)
+    with pytest.raises(lpm.Lpm6Error) as e:
+        src.replicate([len(devices)])  # devices[0] must be the source device
+    assert e.value.code in ("InvalidArgument", "CudaError")
