@@ -244,3 +244,45 @@ def test_reference_dropin(cuda):
     assert " 0 mismatches" in r.stdout
     # the store phase: per-op outcomes equal the reference FibTable mutators', 3 commits
     assert r.stdout.count("store: epoch") == 3 and "store: epoch 4" in r.stdout
+
+
+def test_concurrent_lookups_on_many_streams(lpm, orc, cuda):
+    """A FIB handle is immutable: lookups from several host threads on their own
+    streams (device buffers) and the host-buffer pipeline at the same time all
+    return the oracle's answers (the reference's contract)."""
+    import threading
+    torch = cuda
+    fib = lpm.workload_fib(1)
+    imap = lpm.build_intervals(fib)
+    dev = lpm.Fib.build(fib)
+    rng = np.random.default_rng(9)
+    addrs = addrs_from_keys(rng.integers(0, 2**64, 1 << 18, dtype=np.uint64), rng)
+    want, _ = orc.lookup_batch(0, imap.boundaries, imap.next_hops, addrs, threads=8)
+    da = torch.from_numpy(addrs.view(np.uint8).reshape(-1, 16)).cuda()
+    errors = []
+
+    def device_worker():
+        try:
+            s = torch.cuda.Stream()
+            for _ in range(20):
+                out = dev.lookup_batch(da, stream=s)
+                s.synchronize()
+                assert np.array_equal(out.cpu().numpy().astype(np.uint32), want)
+        except BaseException as e:  # noqa: BLE001
+            errors.append(e)
+
+    def host_worker():
+        try:
+            for _ in range(5):
+                out = dev.lookup_batch(addrs)
+                assert np.array_equal(out.astype(np.uint32), want)
+        except BaseException as e:  # noqa: BLE001
+            errors.append(e)
+
+    threads = [threading.Thread(target=device_worker) for _ in range(4)] + \
+              [threading.Thread(target=host_worker) for _ in range(2)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
