@@ -322,6 +322,22 @@ def time_reference_cpu(fib, addrs, threads, repeats=1):
     return times, "port", "oracle/lpm6_oracle.c orc_lookup_interval (restatement)"
 
 
+def oracle_check(fib, host_addrs, gpu_out, vb, threads, extra=None):
+    """Part of the CPU-baseline leg (the only place bench.py runs oracle/): the CPU
+    oracle's answers for a sample of the timed run's addresses, compared with the
+    GPU's output for them. A checker only; nothing measured comes from here."""
+    from oracle.oracle import Oracle
+    o = Oracle()
+    st, b, nh = o.build_intervals(fib.rules, fib.default_next_hop)
+    want, _ = o.lookup_batch(0, b, nh, host_addrs, threads=threads)
+    got = gpu_out.view({1: np.uint8, 2: np.uint16, 4: np.uint32}[vb]).astype(np.uint32)
+    res = {"checked": int(len(want)), "mismatches": int(np.count_nonzero(got != want)),
+           "oracle": "oracle/lpm6_oracle.c interval oracle"}
+    if extra:
+        res.update(extra)
+    return res
+
+
 def time_restated_planb(fib, addrs, threads):
     """Restated PlanB AVX-512 Listing 1 + B=16 batched search, k=8 (oracle/lpm6_oracle_avx512.c)."""
     from oracle.oracle import Oracle
@@ -409,18 +425,12 @@ def run_chunked(args, lpm, dispatch, fdev, fib, info, geom, cfg, ws, rank, dev_i
     total_ms = dispatch.max_over_ranks(sum(step_ms), dist, "cuda")
     value = info.n_queries * args.steps / (total_ms * 1e-3) / 1e9
     parity = None
-    if rank == 0:
-        from oracle.oracle import Oracle
-        o = Oracle()
+    if rank == 0:  # CPU-baseline leg: the oracle checks a sample of chunk c0's output
         gen.run(c0 * chunk, 1 << 20, addrs, stream)
         fdev.lookup_batch(addrs[: 1 << 20], out[: (1 << 20) * vb], stream)
         torch.cuda.synchronize()
-        st, b, nh = o.build_intervals(fib.rules, fib.default_next_hop)
         ha = addrs[: 1 << 20].cpu().numpy().view(np.uint64).reshape(-1, 2)
-        want, _ = o.lookup_batch(0, b, nh, ha, threads=cpu_threads())
-        got = out[: (1 << 20) * vb].cpu().numpy().view({1: np.uint8, 2: np.uint16, 4: np.uint32}[vb])
-        parity = {"checked": 1 << 20, "mismatches": int(np.count_nonzero(got.astype(np.uint32) != want)),
-                  "oracle": "oracle/lpm6_oracle.c interval oracle", "chunk": c0}
+        parity = oracle_check(fib, ha, out[: (1 << 20) * vb].cpu().numpy(), vb, cpu_threads(), {"chunk": c0})
     if rank != 0:
         if dist is not None:
             dist.barrier()
@@ -548,18 +558,10 @@ def main():
     value = ws * n * args.steps / (total_ms * 1e-3) / 1e9  # aggregate G lookups/s
     lps_gpu = n / (ms_per_step * 1e-3)
 
-    # -- parity sample of the timed output ----------------------------------------------------------
-    parity = None
-    if rank == 0:
-        from oracle.oracle import Oracle
-        o = Oracle()
-        m_s = min(n, 1 << 20)
-        st, b, nh = o.build_intervals(fib.rules, fib.default_next_hop)
-        ha = addrs[:m_s].cpu().numpy().view(np.uint64).reshape(-1, 2)
-        want, _ = o.lookup_batch(0, b, nh, ha, threads=cpu_threads())
-        got = out[: m_s * vb].cpu().numpy().view({1: np.uint8, 2: np.uint16, 4: np.uint32}[vb]).astype(np.uint32)
-        parity = {"checked": m_s, "mismatches": int(np.count_nonzero(got != want)),
-                  "oracle": "oracle/lpm6_oracle.c interval oracle"}
+    # -- sample of the timed output, checked against the oracle in the CPU-baseline leg ------------
+    m_s = min(n, 1 << 20)
+    sample_addrs = addrs[:m_s].cpu().numpy().view(np.uint64).reshape(-1, 2) if rank == 0 else None
+    sample_out = out[: m_s * vb].cpu().numpy() if rank == 0 else None
 
     # -- end to end through the C ABI with host buffers -------------------------------------------
     e2e = None
@@ -620,7 +622,9 @@ def main():
         extras = time_extras(lpm, torch, fdev, fib, addrs, n, vb, stream, dev_index)
 
     # -- CPU baseline (rank 0, N = 1) ---------------------------------------------------------------------
+    # -- CPU-baseline leg (rank 0): oracle check of the timed sample; oracle timing at N = 1 ------------
     cpu = None
+    parity = oracle_check(fib, sample_addrs, sample_out, vb, cpu_threads()) if rank == 0 else None
     if rank == 0 and ws == 1 and not args.no_cpu:
         threads = cpu_threads()
         m_cpu = min(n, CPU_SAMPLE)
