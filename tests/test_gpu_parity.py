@@ -286,3 +286,56 @@ def test_concurrent_lookups_on_many_streams(lpm, orc, cuda):
     for t in threads:
         t.join()
     assert not errors, errors
+
+
+def test_small_and_ragged_batches(lpm, orc, cuda):
+    """Batch sizes around the 32-query tile and the 4-lane group, and n = 0."""
+    torch = cuda
+    fib = lpm.workload_fib(1)
+    imap = lpm.build_intervals(fib)
+    dev = lpm.Fib.build(fib)
+    rng = np.random.default_rng(11)
+    addrs = addrs_from_keys(rng.integers(0, 2**64, 5000, dtype=np.uint64), rng)
+    want = oracle_next_hops(orc, imap.boundaries, imap.next_hops, addrs)
+    da = torch.from_numpy(addrs.view(np.uint8).reshape(-1, 16)).cuda()
+    for n in (1, 2, 3, 4, 5, 31, 32, 33, 127, 129, 1023, 4095, 5000):
+        out = torch.full((n + 64,), 0xAB, dtype=torch.uint8, device="cuda")  # canary past the end
+        dev.lookup_batch(da[:n], out[:n])
+        torch.cuda.synchronize()
+        o = out.cpu().numpy()
+        np.testing.assert_array_equal(o[:n].astype(np.uint32), want[:n], err_msg=f"n={n}")
+        assert np.all(o[n:] == 0xAB), f"n={n}: wrote past the end"
+    empty = torch.empty((0, 16), dtype=torch.uint8, device="cuda")
+    dev.lookup_batch(empty, torch.empty(0, dtype=torch.uint8, device="cuda"))  # no launch, no error
+
+
+def test_depth6_tree(lpm, orc, cuda):
+    """A 16M-interval map (depth 6, the deepest a realistic FIB reaches) laid out on
+    the device from intervals; lookups against the interval oracle, every smem split."""
+    torch = cuda
+    m = 16_000_000
+    rng = np.random.default_rng(12)
+    gaps = rng.integers(1, 1 << 30, m, dtype=np.uint64)
+    b = np.cumsum(gaps, dtype=np.uint64)
+    b[0] = 0
+    nh = rng.integers(1, 250, m, dtype=np.uint32)
+    nh[1:][nh[1:] == nh[:-1]] ^= 1  # merged map: adjacent next hops differ
+    imap = lpm.IntervalMap(b, nh, 0)
+    dev = lpm.Fib.from_intervals(imap)
+    g = dev.geometry
+    assert g.depth == 6
+    keys = np.concatenate([b[rng.integers(0, m, 100000)], rng.integers(0, int(b[-1]) + (1 << 32), 100000,
+                                                                        dtype=np.uint64)])
+    keys = np.concatenate([keys, keys + np.uint64(1), keys - np.uint64(1)])
+    addrs = addrs_from_keys(keys, rng)
+    want = oracle_next_hops(orc, b, nh, addrs)
+    da = torch.from_numpy(addrs.view(np.uint8).reshape(-1, 16)).cuda()
+    for t in range(g.image_levels + 1):
+        dev.set_kernel_config(smem_levels=t)
+        for checked in (False, True):
+            dev.set_checked(checked)
+            out = dev.lookup_batch(da)
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(out.cpu().numpy().astype(np.uint32), want, err_msg=f"T={t}")
+            if checked:
+                assert dev.violations() == 0
