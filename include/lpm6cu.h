@@ -185,6 +185,9 @@ void lpm6cu_fib_destroy(lpm6cu_fib* fib);
 int lpm6cu_fib_set_checked(lpm6cu_fib* fib, int on);
 /* OR of the violation bits since the last reset (synchronizes the device). */
 int lpm6cu_fib_violations(lpm6cu_fib* fib, uint32_t* bits, int reset);
+/* Checked mode also counts the tree lines each query visited (shared-memory
+ * image levels included): always depth + 1 per query. */
+int lpm6cu_fib_node_visits(lpm6cu_fib* fib, uint64_t* visits, int reset);
 
 /* ---- lookup --------------------------------------------------------------- */
 

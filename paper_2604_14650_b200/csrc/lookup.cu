@@ -302,6 +302,7 @@ template <int DEPTH, int VB, int TILES, int THREADS, int MINB, bool CHECKED, int
 __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const LookupParams p) {
   using F = LeafFmt<VB>;
   unsigned violations = 0;
+  unsigned long long visits = 0;  // CHECKED: lines visited by this lane's own queries
   constexpr int NS = 4 * TILES;  // queries in flight per 4-lane group
   extern __shared__ __align__(128) unsigned long long s_lines[];
   __shared__ __align__(8) uint64_t s_bar;
@@ -375,6 +376,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
             violations |= 1u;
             node[t] = 0;
           }
+          if (CHECKED && (st * TILES + t) * 32ull + lane < p.n) ++visits;
         }
       }
 
@@ -405,6 +407,11 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
       }
 #pragma unroll
       for (int s = 0; s < NS; ++s) ld_line_quarter(p.lines + (base_w + nd[s] * 16u), w[s]);
+      if (CHECKED) {  // one line per query: the lane owning query (t, j) counts it
+#pragma unroll
+        for (int t = 0; t < TILES; ++t)
+          if ((st * TILES + t) * 32ull + lane < p.n) ++visits;
+      }
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
         const unsigned r = group_rank(qk[s], w[s], l < DEPTH ? 4u : leaf_valid, gmask);
@@ -424,7 +431,12 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
       }
     }
   }
-  if (CHECKED && violations) atomicOr(p.err, violations);
+  if (CHECKED) {
+    if (violations) atomicOr(p.err, violations);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) visits += __shfl_xor_sync(kFull, visits, o);
+    if (lane == 0 && visits) atomicAdd(reinterpret_cast<unsigned long long*>(p.err + 2), visits);
+  }
 }
 
 using KernelFn = void (*)(const LookupParams);
@@ -528,7 +540,7 @@ struct lpm6cu_fib {
   int device = 0;
   lpm6cu_geometry g{};
   unsigned long long* d_lines = nullptr;
-  unsigned int* d_err = nullptr;  // non-null: checked mode (bounds-checked kernel)
+  unsigned int* d_err = nullptr;  // non-null: checked mode; [0] violation bits, [2..3] u64 node visits
   bool owns = true;
   lpm6cu_kernel_config cfg{};  // resolved
   int num_sms = 0;
@@ -877,8 +889,8 @@ int lpm6cu_fib_set_checked(lpm6cu_fib* f, int on) {
     if (!f) throw Error(Errc::InvalidArgument, "NULL fib");
     DeviceGuard dg(f->device);
     if (on && !f->d_err) {
-      check_cuda(cudaMalloc(&f->d_err, sizeof(unsigned)), "cudaMalloc err");
-      check_cuda(cudaMemset(f->d_err, 0, sizeof(unsigned)), "memset err");
+      check_cuda(cudaMalloc(&f->d_err, 4 * sizeof(unsigned)), "cudaMalloc err");
+      check_cuda(cudaMemset(f->d_err, 0, 4 * sizeof(unsigned)), "memset err");
     } else if (!on && f->d_err) {
       check_cuda(cudaFree(f->d_err), "cudaFree err");
       f->d_err = nullptr;
@@ -897,6 +909,19 @@ int lpm6cu_fib_violations(lpm6cu_fib* f, uint32_t* bits, int reset) {
     check_cuda(cudaMemcpy(&v, f->d_err, sizeof v, cudaMemcpyDeviceToHost), "read err");  // syncs the device
     *bits = v;
     if (reset) check_cuda(cudaMemset(f->d_err, 0, sizeof(unsigned)), "reset err");
+  });
+}
+
+int lpm6cu_fib_node_visits(lpm6cu_fib* f, uint64_t* visits, int reset) {
+  return guard([&] {
+    if (!f || !visits) throw Error(Errc::InvalidArgument, "NULL argument");
+    *visits = 0;
+    if (!f->d_err) return;
+    DeviceGuard dg(f->device);
+    unsigned long long v = 0;
+    check_cuda(cudaMemcpy(&v, f->d_err + 2, sizeof v, cudaMemcpyDeviceToHost), "read visits");
+    *visits = v;
+    if (reset) check_cuda(cudaMemset(f->d_err + 2, 0, sizeof v), "reset visits");
   });
 }
 

@@ -184,6 +184,12 @@ class Fib:
         check(lib().lpm6cu_fib_violations(self._h, C.byref(v), int(reset)))
         return v.value
 
+    def node_visits(self, reset: bool = True) -> int:
+        """Checked mode: tree lines visited since the last reset (depth + 1 per query)."""
+        v = C.c_uint64(0)
+        check(lib().lpm6cu_fib_node_visits(self._h, C.byref(v), int(reset)))
+        return v.value
+
     # -- lookup ---------------------------------------------------------------
     def lookup_batch(self, addrs, out=None, stream=None):
         """Next hops of n 16-byte little-endian u128 addresses.

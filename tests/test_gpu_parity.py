@@ -42,12 +42,16 @@ def check_fib(lpm, orc, cuda, fib, addrs, lanes=LANES, smem_levels=(None, 0, 1, 
             dev.set_kernel_config(lanes_per_query=g, smem_levels=t)
             for checked in (False, True):
                 dev.set_checked(checked)
+                if checked:
+                    dev.node_visits(reset=True)
                 got = run_lookup(cuda, dev, addrs).astype(np.uint32)
                 bad = np.nonzero(got != want)[0]
                 assert len(bad) == 0, (f"G={g} T={t} checked={checked}: {len(bad)} mismatches, first key "
                                        f"{int(addrs[bad[0], 1]):#x} want {want[bad[0]]} got {got[bad[0]]}")
                 if checked:
                     assert dev.violations() == 0
+                    # fixed node visits: depth + 1 lines per query whatever the split
+                    assert dev.node_visits() == len(addrs) * (dev.geometry.depth + 1)
     dev.set_checked(False)
     return dev, want
 

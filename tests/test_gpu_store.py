@@ -206,7 +206,7 @@ def test_epoch_monotonic_over_1000_commits(lpm, cuda, st):
 
 
 def test_concurrent_readers_see_whole_snapshots(lpm, orc, cuda, st):
-    """Readers loop acquire -> lookups -> release while a writer commits: every
+    """8 readers loop acquire -> lookups -> release while a writer commits: every
     window's results equal the oracle of exactly one epoch's FIB."""
     torch = cuda
     rng = np.random.default_rng(7)
@@ -240,7 +240,7 @@ def test_concurrent_readers_see_whole_snapshots(lpm, orc, cuda, st):
         except BaseException as e:  # noqa: BLE001
             errors.append(e)
 
-    threads = [threading.Thread(target=reader) for _ in range(3)]
+    threads = [threading.Thread(target=reader) for _ in range(8)]  # 8 readers, 1 committer
     for t in threads:
         t.start()
     view = fib
@@ -297,4 +297,22 @@ def test_update_trace_replay_c1(lpm, orc, cuda, st):
         addrs = addrs_from_keys(keys, rng)
         np.testing.assert_array_equal(lookup(cuda, store, addrs), expected(lpm, orc, view, addrs))
     assert store.epoch == 7
+    store.close()
+
+
+def test_1m_prefix_rebuild_under_5s(lpm, cuda, st):
+    """Acceptance S:494: a 1M-prefix rebuild completes in <= 5 s (the paper: 850 ms)."""
+    import time
+    from paper_2604_14650_b200.fib import Prefix
+    fib = lpm.workload_fib(2)
+    store = st.FibStore(fib)
+    rules = fib.rules
+    ops = [st.UpdateOp(st.ANNOUNCE, Prefix(int(rules[i]["value_hi"]) << 64, int(rules[i]["length"]), 7))
+           for i in range(0, len(rules), 1000)]
+    store.stage(ops)
+    t0 = time.perf_counter()
+    assert store.commit() == 2
+    dt = time.perf_counter() - t0
+    assert dt < 5.0, dt
+    assert store.stats.last_build_ms < 1000
     store.close()
