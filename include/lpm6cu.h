@@ -87,7 +87,9 @@ typedef struct {
   uint64_t level_nodes[LPM6CU_MAX_LEVELS]; /* reachable nodes per level (level depth = leaves) */
   uint64_t level_start[LPM6CU_MAX_LEVELS]; /* u64-word offset of each level */
   uint32_t default_next_hop;
-  uint32_t reserved;
+  uint32_t leaf_image;   /* 1: small tree — the leaf lines also have a shared-memory image (16 words
+                            at a 17-word stride) right after the internal image; smem_levels =
+                            depth + 1 then serves the whole lookup from shared memory */
 } lpm6cu_geometry;
 
 typedef struct {

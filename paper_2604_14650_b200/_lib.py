@@ -42,7 +42,7 @@ class Geometry_t(C.Structure):
                 ("num_keys", C.c_uint64), ("leaf_nodes", C.c_uint64), ("total_words", C.c_uint64),
                 ("image_start", C.c_uint64),
                 ("level_nodes", C.c_uint64 * MAX_LEVELS), ("level_start", C.c_uint64 * MAX_LEVELS),
-                ("default_next_hop", C.c_uint32), ("reserved", C.c_uint32)]
+                ("default_next_hop", C.c_uint32), ("leaf_image", C.c_uint32)]
 
 
 class BuildOpts_t(C.Structure):

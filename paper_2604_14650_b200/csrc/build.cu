@@ -234,6 +234,13 @@ __global__ void leaf_kernel(const Geo g, const u64d* bnd, const unsigned* nh, u6
   }
 }
 
+// Leaf image of a small tree (layout.hpp): leaf line words at a 17-word stride.
+__global__ void leaf_image_kernel(const Geo g, u64d dst_start, u64d* lines) {
+  const u64d words = g.leaf_nodes * 16;
+  for (u64d t = blockIdx.x * 256ull + threadIdx.x; t < words; t += gridDim.x * 256ull)
+    lines[dst_start + (t >> 4) * kLeafImageStride + (t & 15u)] = lines[g.level_start[g.depth] + t];
+}
+
 __global__ void image_kernel(const Geo g, u64d* lines) {
   const u64d nodes = g.level_start[g.image_levels] >> 4;  // nodes of levels [0, image_levels)
   for (u64d t = blockIdx.x * 256ull + threadIdx.x; t < nodes * kNodeKeys; t += gridDim.x * 256ull) {
@@ -407,6 +414,9 @@ void* device_layout(const DeviceIntervals& iv, u32 vb, uint32_t default_nh, cuda
   if (t.image_levels > 0)
     image_kernel<<<blocks_for((t.level_start[t.image_levels] >> 4) * kNodeKeys), 256, 0, s>>>(
         g, static_cast<u64d*>(lines.p));
+  if (t.leaf_image)
+    leaf_image_kernel<<<blocks_for(t.leaf_nodes * 16), 256, 0, s>>>(g, leaf_image_start(t),
+                                                                   static_cast<u64d*>(lines.p));
   ck(cudaGetLastError(), "layout fill");
   ck(cudaStreamSynchronize(s), "layout fill");
   export_geometry(t, geom);

@@ -38,6 +38,7 @@ void export_geometry(const TreeLayout& t, lpm6cu_geometry* g) {
   g->total_words = t.total_words;
   g->image_levels = t.image_levels;
   g->image_start = t.image_start;
+  g->leaf_image = t.leaf_image;
   for (int l = 0; l < kMaxLevels; ++l) {
     g->level_nodes[l] = t.level_nodes[l];
     g->level_start[l] = t.level_start[l];

@@ -222,7 +222,8 @@ struct LookupParams {
   unsigned long long n;
   const unsigned long long* image;  // packed 15-key copy of internal levels 0.. (layout.hpp)
   unsigned int smem_levels;  // phase A levels [0, smem_levels), <= depth
-  unsigned int smem_bytes;   // image bytes staged for those levels
+  unsigned int smem_bytes;   // image bytes staged for those levels (+ the leaf image when LEAFS)
+  unsigned int leaf_image_off;  // LEAFS: word offset of the leaf image in shared memory
   unsigned long long level_nodes[LPM6CU_MAX_LEVELS];  // checked mode: node-index bounds
   unsigned int* err;         // checked mode: OR of violation bits (1 smem level, 2 line level, 4 leaf rank)
 };
@@ -293,12 +294,36 @@ __device__ __forceinline__ void store_group(const LookupParams& p, unsigned long
   }
 }
 
+// Leaf search in the shared-memory leaf image (small trees): the same 4-probe
+// binary search as an internal node over the line's 16 words, with slots past
+// kL (the next-hop words) counting as greater than every query; then the next
+// hop of ordinal rank - 1 read from the line's value bytes.
+template <int VB>
+__device__ __forceinline__ unsigned leaf_search_smem(const unsigned long long* lf, unsigned long long q,
+                                                     unsigned& rank) {
+  constexpr unsigned kL = LeafFmt<VB>::kL;
+  auto le = [&](unsigned slot) { return slot < kL && lf[slot] <= q; };
+  unsigned c = le(7) ? 8u : 0u;
+  c |= le(c | 3u) ? 4u : 0u;
+  c |= le(c | 1u) ? 2u : 0u;
+  c |= le(c) ? 1u : 0u;
+  rank = c;
+  const unsigned ord = c ? c - 1u : 0u;
+  const unsigned char* vals = reinterpret_cast<const unsigned char*>(lf + kL);
+  if constexpr (VB == 1) return vals[ord];
+  else if constexpr (VB == 2) return reinterpret_cast<const unsigned short*>(vals)[ord];
+  else return reinterpret_cast<const unsigned*>(vals)[ord];
+}
+
 // TILES consecutive 32-query tiles per warp iteration (lane L owns query L of
 // each); MINB > 0 caps registers so that MINB CTAs of THREADS threads fit an SM.
 // CHECKED adds bounds checks on every node index and leaf rank: a violation
 // (only possible with a corrupted tree) is clamped, never read out of bounds,
 // and reported through p.err — the fail-loudly mode the tests run.
-template <int DEPTH, int VB, int TILES, int THREADS, int MINB, bool CHECKED, int INPUT = kInAddr>
+// LEAFS (small trees, layout.hpp leaf image): every level including the leaves
+// is staged in shared memory and each thread finishes its own query there — no
+// L2 line loads and no cross-lane traffic.
+template <int DEPTH, int VB, int TILES, int THREADS, int MINB, bool CHECKED, int INPUT = kInAddr, bool LEAFS = false>
 __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const LookupParams p) {
   using F = LeafFmt<VB>;
   unsigned violations = 0;
@@ -380,6 +405,27 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
         }
       }
 
+    if constexpr (LEAFS) {
+#pragma unroll
+      for (int t = 0; t < TILES; ++t) {
+        const unsigned long long qi = (st * TILES + t) * 32ull + lane;
+        if (CHECKED && node[t] >= p.level_nodes[DEPTH]) {
+          violations |= 1u;
+          node[t] = 0;
+        }
+        unsigned rank;
+        const unsigned v = leaf_search_smem<VB>(s_lines + p.leaf_image_off + node[t] * kLeafImageStride, key[t], rank);
+        if (CHECKED && rank == 0) violations |= 4u;
+        if (CHECKED && qi < p.n) ++visits;
+        if (qi < p.n) {
+          if constexpr (VB == 1) asm volatile("st.global.cs.u8 [%0], %1;" ::"l"(p.out + qi), "h"((unsigned short)v));
+          else if constexpr (VB == 2) asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(p.out + 2 * qi), "h"((unsigned short)v));
+          else asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p.out + 4 * qi), "r"(v));
+        }
+      }
+      continue;
+    }
+
     // Phase B: the group's queries, one 128-byte line per query per level.
     unsigned long long qk[NS];
     unsigned nd[NS];
@@ -443,6 +489,17 @@ using KernelFn = void (*)(const LookupParams);
 
 // Instantiated shapes: (queries per lane, min CTAs per SM) for every depth and
 // value width; the tuning grid below is measured by bench.py --sweep.
+template <int VB, bool CHECKED>
+KernelFn pick_depth_leafs(int depth) {
+  switch (depth) {
+    case 0: return lpm6_lookup_kernel<0, VB, 1, 1024, 1, CHECKED, kInAddr, true>;
+    case 1: return lpm6_lookup_kernel<1, VB, 1, 1024, 1, CHECKED, kInAddr, true>;
+    case 2: return lpm6_lookup_kernel<2, VB, 1, 1024, 1, CHECKED, kInAddr, true>;
+    case 3: return lpm6_lookup_kernel<3, VB, 1, 1024, 1, CHECKED, kInAddr, true>;
+    default: return nullptr;
+  }
+}
+
 template <int VB, int TILES, int THREADS, int MINB, bool CHECKED, int INPUT>
 KernelFn pick_depth(int depth) {
   switch (depth) {
@@ -471,7 +528,16 @@ KernelFn pick_vb(int vb, int depth) {
 // Instantiated shapes (queries per lane, threads per CTA, min CTAs per SM);
 // bench.py --sweep measures them. The checked variant exists for the default shape.
 KernelFn pick_kernel(int vb, int depth, int tiles, int threads, int minb, bool checked = false,
-                     int input = kInAddr) {
+                     int input = kInAddr, bool leafs = false) {
+  if (leafs) {  // leaf image: address input, default shape, depth <= kMaxLeafImageDepth
+    if (input != kInAddr || tiles != 1 || threads != 1024 || minb != 1) return nullptr;
+    switch (vb) {
+      case 1: return checked ? pick_depth_leafs<1, true>(depth) : pick_depth_leafs<1, false>(depth);
+      case 2: return checked ? pick_depth_leafs<2, true>(depth) : pick_depth_leafs<2, false>(depth);
+      case 4: return checked ? pick_depth_leafs<4, true>(depth) : pick_depth_leafs<4, false>(depth);
+      default: return nullptr;
+    }
+  }
   if (input != kInAddr) {  // key / packet input: the default shape, unchecked and checked
     if (tiles != 1 || threads != 1024 || minb != 1) return nullptr;
     if (input == kInKey)
@@ -594,8 +660,17 @@ struct lpm6cu_querygen {
 namespace {
 
 // Bytes of the shared-memory image for `levels` levels (layout.hpp image_bytes).
+// Bytes of the shared-memory image for `levels` levels (layout.hpp image_bytes);
+// levels = depth + 1 adds the leaf image of a small tree (leaf_image_bytes).
 unsigned long long image_bytes_of(const lpm6cu_geometry& g, unsigned levels) {
+  if (levels > g.depth)
+    return image_bytes_of(g, g.depth) + (g.leaf_nodes * kLeafImageStride * 8 + 15) / 16 * 16;
   return (g.level_start[levels] / kLineWords * kNodeKeys * 8 + 15) / 16 * 16;
+}
+
+// Shape of the default kernel (the only one with the leaf-image variant).
+bool default_shape(const lpm6cu_kernel_config& c) {
+  return c.queries_per_lane == 1 && c.threads_per_cta == 1024 && c.min_ctas_per_sm == 1;
 }
 
 // Resolve automatic kernel settings against the device and the tree.
@@ -618,7 +693,10 @@ void resolve_config(lpm6cu_fib* f, const lpm6cu_kernel_config* req) {
                                            " min_ctas_per_sm=" + std::to_string(c.min_ctas_per_sm));
   const unsigned depth = f->g.depth;
   const size_t budget = f->max_smem_optin;
-  const unsigned tmax = std::min<unsigned>(depth, f->g.image_levels);  // phase A: imaged internal levels
+  // Phase A: imaged internal levels; depth + 1 = the leaves too (small trees, default shape).
+  const unsigned tmax = f->g.leaf_image && default_shape(c) && depth <= kMaxLeafImageDepth
+                            ? depth + 1
+                            : std::min<unsigned>(depth, f->g.image_levels);
   if (req == nullptr || req->smem_levels == 0xFF) {
     // Auto: the deepest prefix of internal levels whose image fits the shared
     // memory one CTA may use; with 256-thread CTAs keep >= 4 CTAs per SM.
@@ -641,6 +719,7 @@ void resolve_config(lpm6cu_fib* f, const lpm6cu_kernel_config* req) {
 }
 
 unsigned long long staged_bytes(const lpm6cu_fib* f) { return image_bytes_of(f->g, f->cfg.smem_levels); }
+bool leaf_image_mode(const lpm6cu_fib* f) { return f->cfg.smem_levels > f->g.depth; }
 
 struct PacketInput {
   unsigned long long stride = 0;
@@ -656,7 +735,10 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
   const unsigned tiles = dflt ? 1 : f->cfg.queries_per_lane;
   const unsigned threads_cta = dflt ? 1024 : f->cfg.threads_per_cta;
   const unsigned minb = dflt ? 1 : f->cfg.min_ctas_per_sm;
-  const size_t smem = staged_bytes(f);
+  // Leaf-image mode serves address input; key / packet input uses the internal image only.
+  const bool leafs = leaf_image_mode(f) && input == kInAddr;
+  const unsigned smem_levels = leaf_image_mode(f) && !leafs ? f->g.depth : f->cfg.smem_levels;
+  const size_t smem = image_bytes_of(f->g, smem_levels);
   const int threads = static_cast<int>(threads_cta);
   LaunchPlan plan;
   {
@@ -665,7 +747,8 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
     LaunchPlan& slot = mf->plans[input][f->d_err != nullptr ? 1 : 0];
     if (!slot.valid) {
       KernelFn fn = pick_kernel(static_cast<int>(f->g.value_bytes), static_cast<int>(f->g.depth),
-                                static_cast<int>(tiles), threads, static_cast<int>(minb), f->d_err != nullptr, input);
+                                static_cast<int>(tiles), threads, static_cast<int>(minb), f->d_err != nullptr, input,
+                                leafs);
       if (!fn) throw Error(Errc::InvalidArgument, "no kernel instantiated for this configuration");
       if (smem > 48 * 1024)
         check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
@@ -695,8 +778,9 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
   }
   p.out = static_cast<unsigned char*>(d_out);
   p.n = n;
-  p.smem_bytes = static_cast<unsigned>(staged_bytes(f));
-  p.smem_levels = f->cfg.smem_levels;
+  p.smem_bytes = static_cast<unsigned>(smem);
+  p.smem_levels = std::min<unsigned>(smem_levels, f->g.depth);
+  p.leaf_image_off = static_cast<unsigned>(image_bytes_of(f->g, f->g.depth) / 8);
   p.image = f->d_lines + f->g.image_start;
   for (int l = 0; l < LPM6CU_MAX_LEVELS; ++l) p.level_nodes[l] = f->g.level_nodes[l];
   p.err = f->d_err;
@@ -715,6 +799,14 @@ lpm6cu_fib* new_fib(int device, const lpm6cu_geometry* g) {
   if (g->depth > kMaxKernelDepth) throw Error(Errc::InvalidArgument, "tree depth above 7");
   if (g->value_bytes != 1 && g->value_bytes != 2 && g->value_bytes != 4)
     throw Error(Errc::InvalidArgument, "value_bytes must be 1, 2 or 4");
+  // The geometry must describe a line array that holds what the kernels will read.
+  if (g->image_levels > g->depth || g->level_start[g->depth] + g->leaf_nodes * kLineWords > g->image_start)
+    throw Error(Errc::InvalidArgument, "inconsistent geometry (levels / image offset)");
+  const unsigned imaged = g->leaf_image ? g->depth + 1 : g->image_levels;
+  if (g->image_start + image_bytes_of(*g, imaged) / 8 > g->total_words)
+    throw Error(Errc::InvalidArgument, "inconsistent geometry (image past total_words)");
+  if (g->leaf_image && (g->image_levels != g->depth || image_bytes_of(*g, g->depth + 1) > 232448 - 1024))
+    throw Error(Errc::InvalidArgument, "inconsistent geometry (leaf image)");
   int ndev = 0;
   check_cuda(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
   if (device < 0 || device >= ndev) throw Error(Errc::CudaError, "no CUDA device " + std::to_string(device));

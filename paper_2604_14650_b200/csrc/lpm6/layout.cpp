@@ -31,6 +31,10 @@ TreeLayout plan_layout(u64 m, u32 value_bytes) {
   g.image_levels = s;
   g.image_start = off;
   g.total_words = off + image_bytes(g, s) / 8;
+  if (s == d && d <= kMaxLeafImageDepth && image_bytes(g, d) + leaf_image_bytes(g) <= kImageMaxBytes) {
+    g.leaf_image = 1;
+    g.total_words = leaf_image_start(g) + leaf_image_bytes(g) / 8;
+  }
   if (g.total_words >= (u64(1) << 32))
     throw Error(Errc::InvalidArgument, "tree larger than 32 GiB (word offsets are 32-bit in the kernel)");
   return g;
@@ -98,6 +102,12 @@ Tree build_tree(const IntervalMap& map, u32 value_bytes) {
     u64* dst = t.lines.data() + g.image_start + image_level_start(g, l);
     for (u64 n = 0; n < g.level_nodes[l]; ++n)
       for (u32 p = 0; p < kNodeKeys; ++p) dst[image_slot(n, p)] = src[n * kLineWords + p];
+  }
+  // Leaf image (small trees): leaf lines at a 17-word stride; the pad word stays sentinel.
+  if (g.leaf_image) {
+    u64* dst = t.lines.data() + leaf_image_start(g);
+    for (u64 n = 0; n < g.leaf_nodes; ++n)
+      std::memcpy(dst + n * kLeafImageStride, leaves + n * kLineWords, kLineWords * 8);
   }
   return t;
 }

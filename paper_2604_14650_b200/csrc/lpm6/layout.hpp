@@ -58,16 +58,26 @@ struct TreeLayout {
   // image_level_start(l) = (level_start[l] / 16) * 15.
   u32 image_levels = 0;
   u64 image_start = 0;
+  // Small trees only: when every internal level is imaged and the leaves fit
+  // too, a second image follows the first — each leaf line's 16 words at a
+  // 17-word stride (the odd stride skews banks like the 15-word internal nodes)
+  // — and the kernel serves the whole lookup from shared memory.
+  u32 leaf_image = 0;
   u32 default_next_hop = 0;
 };
 
 inline constexpr u64 kImageMaxBytes = 232448 - 1024;  // B200 opt-in smem per CTA minus static smem
+inline constexpr u32 kLeafImageStride = 17;              // words per leaf in the leaf image
+inline constexpr u32 kMaxLeafImageDepth = 3;             // leaf-image kernels are instantiated for depth <= 3
 
 // Word offset of level l / of key p of node n (within its level) in the image.
 constexpr u64 image_level_start(const TreeLayout& g, u32 l) { return g.level_start[l] / kLineWords * kNodeKeys; }
 constexpr u64 image_slot(u64 n, u32 p) { return n * kNodeKeys + p; }
 // Bytes the kernel stages for `levels` imaged levels (TMA sizes are 16-byte multiples).
 constexpr u64 image_bytes(const TreeLayout& g, u32 levels) { return (image_level_start(g, levels) * 8 + 15) / 16 * 16; }
+// The leaf image: word offset in the line array and bytes (16-byte multiple).
+constexpr u64 leaf_image_start(const TreeLayout& g) { return g.image_start + image_bytes(g, g.depth) / 8; }
+constexpr u64 leaf_image_bytes(const TreeLayout& g) { return (g.leaf_nodes * kLeafImageStride * 8 + 15) / 16 * 16; }
 
 template <class T, size_t Align>
 struct AlignedAllocator {

@@ -167,11 +167,13 @@ class Geometry:
     level_nodes: list[int]
     level_start: list[int]
     default_next_hop: int
+    leaf_image: int = 0
 
     @classmethod
     def from_c(cls, g: Geometry_t) -> "Geometry":
         return cls(g.k, g.b, g.depth, g.value_bytes, g.leaf_keys, g.image_levels, g.num_keys, g.leaf_nodes,
-                   g.total_words, g.image_start, list(g.level_nodes), list(g.level_start), g.default_next_hop)
+                   g.total_words, g.image_start, list(g.level_nodes), list(g.level_start), g.default_next_hop,
+                   g.leaf_image)
 
     def to_c(self) -> Geometry_t:
         g = Geometry_t()
@@ -182,6 +184,7 @@ class Geometry:
             g.level_nodes[i] = self.level_nodes[i]
             g.level_start[i] = self.level_start[i]
         g.default_next_hop = self.default_next_hop
+        g.leaf_image = self.leaf_image
         return g
 
     @property

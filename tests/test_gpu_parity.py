@@ -37,7 +37,8 @@ def check_fib(lpm, orc, cuda, fib, addrs, lanes=LANES, smem_levels=(None, 0, 1, 
     dev = lpm.Fib.build(fib)
     for g in lanes:
         for t in smem_levels:
-            if t is not None and t > dev.geometry.depth:
+            geo = dev.geometry
+            if t is not None and t > geo.depth + geo.leaf_image:  # depth + 1: leaf image (small trees)
                 continue
             dev.set_kernel_config(lanes_per_query=g, smem_levels=t)
             for checked in (False, True):
@@ -143,12 +144,22 @@ def test_corrupted_device_fib_is_detected(lpm, orc, cuda):
     word = g.level_start[g.depth] + (slot // g.leaf_keys) * 16 + slot % g.leaf_keys
     assert lines[word] == imap.boundaries[slot]
     lines[word] += np.uint64(1)  # the boundary moves one key to the right
-    dl = torch.from_numpy(lines.view(np.int64)).cuda()
-    dev = lpm.Fib.wrap_device(g, dl, 0)
+    assert g.leaf_image  # C0 is small: its leaves also have a shared-memory image
+    img_start = g.image_start + ((g.level_start[g.depth] // 16 * 15 * 8 + 15) // 16 * 16) // 8
+    img_word = img_start + (slot // g.leaf_keys) * 17 + slot % g.leaf_keys
+    assert lines[img_word] == imap.boundaries[slot]
     probe = addrs_from_keys(np.array([imap.boundaries[slot]], np.uint64))
     want = oracle_next_hops(orc, imap.boundaries, imap.next_hops, probe)
-    got = run_lookup(cuda, dev, probe).astype(np.uint32)
-    assert got[0] != want[0]
+    # leaves read from L2 (smem_levels = depth): the corrupted line is detected
+    dev = lpm.Fib.wrap_device(g, torch.from_numpy(lines.view(np.int64)).cuda(), 0)
+    dev.set_kernel_config(smem_levels=g.depth)
+    assert run_lookup(cuda, dev, probe).astype(np.uint32)[0] != want[0]
+    # leaves read from the shared-memory leaf image: corrupting that copy is detected
+    lines2 = tree.lines.copy()
+    lines2[img_word] += np.uint64(1)
+    dev2 = lpm.Fib.wrap_device(g, torch.from_numpy(lines2.view(np.int64)).cuda(), 0)
+    assert dev2.kernel_config()["smem_levels"] == g.depth + 1
+    assert run_lookup(cuda, dev2, probe).astype(np.uint32)[0] != want[0]
     ok = lpm.Fib.from_tree(tree)
     assert run_lookup(cuda, ok, probe).astype(np.uint32)[0] == want[0]
 

@@ -106,6 +106,15 @@ def check_layout(lpm, orc, fib, n_random=20000, seed=0):
         img = tree.lines[off: off + nodes * 15].reshape(nodes, 15)
         np.testing.assert_array_equal(img, src[:, :15])
     assert (g.total_words - g.image_start) * 8 <= 232448 - 1024
+    # small trees: the leaf lines again at a 17-word stride after the internal image
+    if g.leaf_image:
+        assert g.image_levels == g.depth <= 3
+        start = g.image_start + ((g.level_start[g.depth] // 16 * 15 * 8 + 15) // 16 * 16) // 8
+        leaves = tree.lines[g.level_start[g.depth]: g.level_start[g.depth] + g.leaf_nodes * 16].reshape(-1, 16)
+        img = tree.lines[start: start + g.leaf_nodes * 17].reshape(-1, 17)
+        np.testing.assert_array_equal(img[:, :16], leaves)
+        assert np.all(img[:, 16] == np.uint64(MASK64))
+        assert g.total_words == start + (g.leaf_nodes * 17 * 8 + 15) // 16 * 16 // 8
     # the descent the kernel performs gives the oracle's answer
     rng = np.random.default_rng(seed)
     keys = np.concatenate([boundary_probe_keys(imap.boundaries), rng.integers(0, 2**64, n_random, dtype=np.uint64)])
@@ -118,6 +127,7 @@ def check_layout(lpm, orc, fib, n_random=20000, seed=0):
 def test_layout_workload_fibs(lpm, orc, kind):
     tree = check_layout(lpm, orc, lpm.workload_fib(kind))
     assert tree.geometry.depth == {0: 2, 1: 4}[kind]
+    assert tree.geometry.leaf_image == {0: 1, 1: 0}[kind]  # C0's whole tree fits shared memory
 
 
 @pytest.mark.parametrize("n,dflt", [(0, False), (1, True), (13, False), (14, True), (300, False), (5000, True)])
