@@ -78,11 +78,6 @@ __device__ __forceinline__ uint4 ld_stream_v4(const uint4* p, uint64_t pol) {
   return r;
 }
 
-__device__ __forceinline__ unsigned long long ld_stream_u64(const unsigned long long* p, uint64_t pol) {
-  unsigned long long r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(pol));
-  return r;
-}
 
 // Input formats of the lookup kernel.
 enum : int { kInAddr = 0, kInKey = 1, kInPacket = 2 };
@@ -113,13 +108,6 @@ __device__ __forceinline__ unsigned long long bswap64(unsigned long long v) {
   return (static_cast<unsigned long long>(__byte_perm(lo, 0, 0x0123)) << 32) | __byte_perm(hi, 0, 0x0123);
 }
 
-__device__ __forceinline__ uint4 ld_stream_v4u(const void* p, uint64_t pol) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p), "l"(pol));
-  return r;
-}
 
 // Bytes [sh, sh + 8) of the little-endian pair (w0, w1), sh in 0..8.
 __device__ __forceinline__ unsigned long long extract8(unsigned long long w0, unsigned long long w1, unsigned sh) {
@@ -138,7 +126,7 @@ __device__ __forceinline__ unsigned long long load_dst_key(const unsigned char* 
   if (align >= 16) {
     const unsigned sh = off & 15u;
     const unsigned char* c = frame + (off - sh);
-    const uint4 v = ld_stream_v4u(c, pol);
+    const uint4 v = ld_stream_v4(reinterpret_cast<const uint4*>(c), pol);
     const unsigned long long w0 = v.x | (static_cast<unsigned long long>(v.y) << 32);
     const unsigned long long w1 = v.z | (static_cast<unsigned long long>(v.w) << 32);
     if (sh <= 8) {
@@ -366,7 +354,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
     unsigned long long k = 0;
     if (qi < p.n) {
       if constexpr (INPUT == kInKey) {
-        k = ld_stream_u64(p.keys + qi, pol_stream);
+        k = ld_stream<unsigned long long>(p.keys + qi, pol_stream);
       } else if constexpr (INPUT == kInPacket) {
         k = load_dst_key(p.pkts + qi * p.pkt_stride, p.pkt_off, p.pkt_align, pol_stream);
       } else {
@@ -718,7 +706,6 @@ void resolve_config(lpm6cu_fib* f, const lpm6cu_kernel_config* req) {
   f->invalidate_plans();
 }
 
-unsigned long long staged_bytes(const lpm6cu_fib* f) { return image_bytes_of(f->g, f->cfg.smem_levels); }
 bool leaf_image_mode(const lpm6cu_fib* f) { return f->cfg.smem_levels > f->g.depth; }
 
 struct PacketInput {
