@@ -108,6 +108,16 @@ class Fib {
     lpm6cu::check(lpm6cu_lookup_batch(h_, addrs, n, out_next_hops, stream));
   }
 
+  // One address (the reference's lookup(t, addr)): a batch of one through
+  // the host path — correct but latency-bound; batch where throughput matters.
+  template <class U128>
+  uint32_t lookup(const U128& addr) const {
+    static_assert(sizeof(U128) == 16, "address must be a 16-byte little-endian u128");
+    uint32_t out = 0;
+    lpm6cu::check(lpm6cu_lookup_batch(h_, &addr, 1, &out, nullptr));
+    return out & (value_bytes() == 4 ? 0xFFFFFFFFu : (1u << (8 * value_bytes())) - 1u);
+  }
+
   // 8-byte keys (search_batch's input); device buffers.
   void lookup_keys(const uint64_t* d_keys, uint64_t n, void* d_out, void* stream = nullptr) const {
     lpm6cu::check(lpm6cu_lookup_keys(h_, d_keys, n, d_out, stream));

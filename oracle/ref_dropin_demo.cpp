@@ -76,6 +76,11 @@ int main(int argc, char** argv) {
         if (bad++ < 5) std::printf("linear-oracle mismatch at %zu\n", i);
       }
     }
+    // single-address lookup(t, addr) on a few of them
+    for (size_t i = 0; i < 64 && i < addrs.size(); ++i)
+      if (gfib.lookup(addrs[i]) != lpm6::lookup_interval_oracle(ref_map, static_cast<uint64_t>(addrs[i] >> 64)) &&
+          bad++ < 5)
+        std::printf("single lookup mismatch at %zu\n", i);
     std::printf("dropin: %zu rules, %zu intervals, %zu queries, %lu mismatches\n", fib.size(), ref_map.size(),
                 addrs.size(), static_cast<unsigned long>(bad));
     if (bad) return 3;
