@@ -214,6 +214,7 @@ struct LookupParams {
   unsigned int leaf_image_off;  // LEAFS: word offset of the leaf image in shared memory
   unsigned long long level_nodes[LPM6CU_MAX_LEVELS];  // checked mode: node-index bounds
   unsigned int* err;         // checked mode: OR of violation bits (1 smem level, 2 line level, 4 leaf rank)
+  unsigned long long root[16];  // the root's 15 separators (+ sentinel), read from the constant bank
 };
 
 // Count of the 15 separators of node n of a shared-memory image level that are
@@ -384,7 +385,19 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
       if (static_cast<unsigned>(l) < TA) {
 #pragma unroll
         for (int t = 0; t < TILES; ++t) {
-          node[t] = node[t] * 16u + node_rank_smem(s_lines + (p.level_start[l] >> 4) * 15u, node[t], key[t]);
+          if (l == 0) {
+            // Root from the kernel-parameter constant bank: all lanes start at the
+            // same node, so the probes are (nearly) uniform LDCs and keep the
+            // shared-memory data pipe free for the deeper levels.
+            const unsigned long long q = key[t];
+            unsigned c = (p.root[7] <= q) ? 8u : 0u;
+            c |= (p.root[c | 3u] <= q) ? 4u : 0u;
+            c |= (p.root[c | 1u] <= q) ? 2u : 0u;
+            c |= (p.root[c] <= q) ? 1u : 0u;
+            node[t] = c;
+          } else {
+            node[t] = node[t] * 16u + node_rank_smem(s_lines + (p.level_start[l] >> 4) * 15u, node[t], key[t]);
+          }
           if (CHECKED && node[t] >= p.level_nodes[l + 1]) {
             violations |= 1u;
             node[t] = 0;
@@ -603,6 +616,8 @@ struct lpm6cu_fib {
   std::unique_ptr<HostPipeline> pipe;
   std::mutex plan_mu;
   LaunchPlan plans[3][2];  // [input format][checked]
+  unsigned long long root[16] = {};  // host copy of the root line (kernel parameter)
+  bool root_ready = false;
 
   void invalidate_plans() {
     std::lock_guard<std::mutex> lk(plan_mu);
@@ -771,6 +786,7 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
   p.image = f->d_lines + f->g.image_start;
   for (int l = 0; l < LPM6CU_MAX_LEVELS; ++l) p.level_nodes[l] = f->g.level_nodes[l];
   p.err = f->d_err;
+  std::memcpy(p.root, f->root, sizeof p.root);
   const unsigned long long ntiles = (n + 32ull * tiles - 1) / (32ull * tiles);
   const unsigned long long warps_per_cta = threads / 32;
   unsigned long long grid = static_cast<unsigned long long>(f->num_sms) * plan.per_sm;
@@ -806,6 +822,14 @@ lpm6cu_fib* new_fib(int device, const lpm6cu_geometry* g) {
   f->max_smem_optin = static_cast<size_t>(optin) - 1024;  // static smem + slack
   resolve_config(f.get(), nullptr);
   return f.release();
+}
+
+// The root line as kernel parameters (LookupParams::root); the line array must
+// hold the tree when the handle is created.
+void load_root(lpm6cu_fib* f) {
+  DeviceGuard dg(f->device);
+  check_cuda(cudaMemcpy(f->root, f->d_lines, sizeof f->root, cudaMemcpyDeviceToHost), "read root line");
+  f->root_ready = true;
 }
 
 bool is_device_ptr(const void* p) {
@@ -859,6 +883,7 @@ int lpm6cu_fib_create(int device, const lpm6cu_geometry* g, const uint64_t* line
     const size_t bytes = g->total_words * 8;
     check_cuda(cudaMalloc(&f->d_lines, bytes), "cudaMalloc lines");
     check_cuda(cudaMemcpy(f->d_lines, lines, bytes, cudaMemcpyHostToDevice), "copy lines");
+    load_root(f.get());
     *out = f.release();
   });
 }
@@ -872,6 +897,7 @@ int lpm6cu_fib_wrap_device(int device, const lpm6cu_geometry* g, const void* d_l
     std::unique_ptr<lpm6cu_fib> f(new_fib(device, g));
     f->d_lines = static_cast<unsigned long long*>(const_cast<void*>(d_lines));
     f->owns = false;
+    load_root(f.get());
     *out = f.release();
   });
 }
@@ -885,6 +911,7 @@ int lpm6cu_fib_adopt_device(int device, const lpm6cu_geometry* g, void* d_lines,
     std::unique_ptr<lpm6cu_fib> f(new_fib(device, g));
     f->d_lines = static_cast<unsigned long long*>(d_lines);
     f->owns = true;
+    load_root(f.get());
     *out = f.release();
   });
 }
@@ -900,6 +927,7 @@ int lpm6cu_fib_build(int device, const lpm6cu_prefix* rules, uint64_t n, uint32_
     std::unique_ptr<lpm6cu_fib> f(new_fib(device, &g));
     check_cuda(cudaMalloc(&f->d_lines, t.lines.size() * 8), "cudaMalloc lines");
     check_cuda(cudaMemcpy(f->d_lines, t.lines.data(), t.lines.size() * 8, cudaMemcpyHostToDevice), "copy lines");
+    load_root(f.get());
     *out = f.release();
   });
 }
@@ -929,6 +957,7 @@ int lpm6cu_fib_build_device(int device, const lpm6cu_prefix* rules, uint64_t n, 
       throw;
     }
     f->d_lines = static_cast<unsigned long long*>(lines);
+    load_root(f.get());
     *out = f.release();
   });
 }
@@ -1080,6 +1109,7 @@ int lpm6cu_fib_build_from_intervals(int device, const uint64_t* boundaries, cons
       throw;
     }
     f->d_lines = static_cast<unsigned long long*>(lines);
+    load_root(f.get());
     *out = f.release();
   });
 }
