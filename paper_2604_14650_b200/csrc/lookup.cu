@@ -158,6 +158,19 @@ __device__ __forceinline__ unsigned long long load_dst_key(const unsigned char* 
   return bswap64(le);  // network order: first byte is the most significant
 }
 
+// 32 bytes of a line through the texture path (two 16-byte texels at texel index t, t+1).
+__device__ __forceinline__ void tex_line_quarter(unsigned long long tex, unsigned t, unsigned long long (&w)[4]) {
+  int a0, a1, a2, a3, b0, b1, b2, b3;
+  asm volatile("tex.1d.v4.s32.s32 {%0,%1,%2,%3}, [%4, {%5}];"
+               : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3) : "l"(tex), "r"(t));
+  asm volatile("tex.1d.v4.s32.s32 {%0,%1,%2,%3}, [%4, {%5}];"
+               : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3) : "l"(tex), "r"(t + 1));
+  w[0] = static_cast<unsigned>(a0) | (static_cast<unsigned long long>(static_cast<unsigned>(a1)) << 32);
+  w[1] = static_cast<unsigned>(a2) | (static_cast<unsigned long long>(static_cast<unsigned>(a3)) << 32);
+  w[2] = static_cast<unsigned>(b0) | (static_cast<unsigned long long>(static_cast<unsigned>(b1)) << 32);
+  w[3] = static_cast<unsigned>(b2) | (static_cast<unsigned long long>(static_cast<unsigned>(b3)) << 32);
+}
+
 __device__ __forceinline__ void ld_line_quarter(const unsigned long long* p, unsigned long long (&w)[4]) {
   asm volatile("ld.global.nc.L2::evict_last.v4.u64 {%0,%1,%2,%3}, [%4];"
                : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
@@ -215,6 +228,7 @@ struct LookupParams {
   unsigned long long level_nodes[LPM6CU_MAX_LEVELS];  // checked mode: node-index bounds
   unsigned int* err;         // checked mode: OR of violation bits (1 smem level, 2 line level, 4 leaf rank)
   unsigned long long root[16];  // the root's 15 separators (+ sentinel), read from the constant bank
+  unsigned long long tex;       // texture object over the line array (int4 texels), 0 = none
 };
 
 // Count of the 15 separators of node n of a shared-memory image level that are
@@ -312,7 +326,9 @@ __device__ __forceinline__ unsigned leaf_search_smem(const unsigned long long* l
 // LEAFS (small trees, layout.hpp leaf image): every level including the leaves
 // is staged in shared memory and each thread finishes its own query there — no
 // L2 line loads and no cross-lane traffic.
-template <int DEPTH, int VB, int TILES, int THREADS, int MINB, bool CHECKED, int INPUT = kInAddr, bool LEAFS = false>
+// TEXL: the internal L2 levels are read through the texture pipe (p.tex).
+template <int DEPTH, int VB, int TILES, int THREADS, int MINB, bool CHECKED, int INPUT = kInAddr, bool LEAFS = false,
+          bool TEXL = false>
 __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const LookupParams p) {
   using F = LeafFmt<VB>;
   unsigned violations = 0;
@@ -453,7 +469,16 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
           }
       }
 #pragma unroll
-      for (int s = 0; s < NS; ++s) ld_line_quarter(p.lines + (base_w + nd[s] * 16u), w[s]);
+      for (int s = 0; s < NS; ++s) {
+        // Internal L2 levels through the texture pipe, leaves through the LSU:
+        // the two pipes of L1TEX share the load, which helps the deep trees (C2:
+        // +8 %); leaves through the texture pipe lose on L2-missing workloads
+        // (C1 -17 %), so they stay on the LSU path.
+        if (TEXL && l < DEPTH)
+          tex_line_quarter(p.tex, (base_w + nd[s] * 16u) >> 1, w[s]);
+        else
+          ld_line_quarter(p.lines + (base_w + nd[s] * 16u), w[s]);
+      }
       if (CHECKED) {  // one line per query: the lane owning query (t, j) counts it
 #pragma unroll
         for (int t = 0; t < TILES; ++t)
@@ -490,6 +515,19 @@ using KernelFn = void (*)(const LookupParams);
 
 // Instantiated shapes: (queries per lane, min CTAs per SM) for every depth and
 // value width; the tuning grid below is measured by bench.py --sweep.
+template <int VB>
+KernelFn pick_depth_texl(int depth) {
+  switch (depth) {
+    case 2: return lpm6_lookup_kernel<2, VB, 1, 1024, 1, false, kInAddr, false, true>;
+    case 3: return lpm6_lookup_kernel<3, VB, 1, 1024, 1, false, kInAddr, false, true>;
+    case 4: return lpm6_lookup_kernel<4, VB, 1, 1024, 1, false, kInAddr, false, true>;
+    case 5: return lpm6_lookup_kernel<5, VB, 1, 1024, 1, false, kInAddr, false, true>;
+    case 6: return lpm6_lookup_kernel<6, VB, 1, 1024, 1, false, kInAddr, false, true>;
+    case 7: return lpm6_lookup_kernel<7, VB, 1, 1024, 1, false, kInAddr, false, true>;
+    default: return nullptr;
+  }
+}
+
 template <int VB, bool CHECKED>
 KernelFn pick_depth_leafs(int depth) {
   switch (depth) {
@@ -529,7 +567,16 @@ KernelFn pick_vb(int vb, int depth) {
 // Instantiated shapes (queries per lane, threads per CTA, min CTAs per SM);
 // bench.py --sweep measures them. The checked variant exists for the default shape.
 KernelFn pick_kernel(int vb, int depth, int tiles, int threads, int minb, bool checked = false,
-                     int input = kInAddr, bool leafs = false) {
+                     int input = kInAddr, bool leafs = false, bool texl = false) {
+  if (texl) {  // internal L2 levels via the texture pipe: address input, default shape, unchecked
+    if (leafs || checked || input != kInAddr || tiles != 1 || threads != 1024 || minb != 1) return nullptr;
+    switch (vb) {
+      case 1: return pick_depth_texl<1>(depth);
+      case 2: return pick_depth_texl<2>(depth);
+      case 4: return pick_depth_texl<4>(depth);
+      default: return nullptr;
+    }
+  }
   if (leafs) {  // leaf image: address input, default shape, depth <= kMaxLeafImageDepth
     if (input != kInAddr || tiles != 1 || threads != 1024 || minb != 1) return nullptr;
     switch (vb) {
@@ -617,6 +664,7 @@ struct lpm6cu_fib {
   std::mutex plan_mu;
   LaunchPlan plans[3][2];  // [input format][checked]
   unsigned long long root[16] = {};  // host copy of the root line (kernel parameter)
+  cudaTextureObject_t tex = 0;       // texture object over the line array
   bool root_ready = false;
 
   void invalidate_plans() {
@@ -637,6 +685,7 @@ struct lpm6cu_fib {
       }
       if (pipe->start) cudaEventDestroy(pipe->start);
     }
+    if (tex) cudaDestroyTextureObject(tex);
     if (owns && d_lines) cudaFree(d_lines);
     if (d_err) cudaFree(d_err);
     if (prev >= 0) cudaSetDevice(prev);
@@ -739,6 +788,9 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
   const unsigned minb = dflt ? 1 : f->cfg.min_ctas_per_sm;
   // Leaf-image mode serves address input; key / packet input uses the internal image only.
   const bool leafs = leaf_image_mode(f) && input == kInAddr;
+  // Texture pipe for internal L2 levels when the tree has any (smem_levels < depth).
+  const bool texl = f->tex && !leafs && input == kInAddr && f->d_err == nullptr && f->cfg.smem_levels < f->g.depth &&
+                    tiles == 1 && threads_cta == 1024 && minb == 1 && f->g.depth >= 2;
   const unsigned smem_levels = leaf_image_mode(f) && !leafs ? f->g.depth : f->cfg.smem_levels;
   const size_t smem = image_bytes_of(f->g, smem_levels);
   const int threads = static_cast<int>(threads_cta);
@@ -750,7 +802,7 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
     if (!slot.valid) {
       KernelFn fn = pick_kernel(static_cast<int>(f->g.value_bytes), static_cast<int>(f->g.depth),
                                 static_cast<int>(tiles), threads, static_cast<int>(minb), f->d_err != nullptr, input,
-                                leafs);
+                                leafs, texl);
       if (!fn) throw Error(Errc::InvalidArgument, "no kernel instantiated for this configuration");
       if (smem > 48 * 1024)
         check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
@@ -787,6 +839,7 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
   for (int l = 0; l < LPM6CU_MAX_LEVELS; ++l) p.level_nodes[l] = f->g.level_nodes[l];
   p.err = f->d_err;
   std::memcpy(p.root, f->root, sizeof p.root);
+  p.tex = f->tex;
   const unsigned long long ntiles = (n + 32ull * tiles - 1) / (32ull * tiles);
   const unsigned long long warps_per_cta = threads / 32;
   unsigned long long grid = static_cast<unsigned long long>(f->num_sms) * plan.per_sm;
@@ -828,6 +881,27 @@ lpm6cu_fib* new_fib(int device, const lpm6cu_geometry* g) {
 // hold the tree when the handle is created.
 void load_root(lpm6cu_fib* f) {
   DeviceGuard dg(f->device);
+  // Texture object over the line array for the internal L2 levels (16-byte int4
+  // texels). Not available (alignment, size limits): those levels use LSU loads.
+  if (f->g.depth >= 1) {
+    int max_w = 0, align = 0;
+    cudaDeviceGetAttribute(&max_w, cudaDevAttrMaxTexture1DLinearWidth, f->device);
+    cudaDeviceGetAttribute(&align, cudaDevAttrTextureAlignment, f->device);
+    if (f->g.total_words / 2 <= static_cast<unsigned long long>(max_w) && align > 0 &&
+        reinterpret_cast<uintptr_t>(f->d_lines) % static_cast<uintptr_t>(align) == 0) {
+      cudaResourceDesc rd{};
+      rd.resType = cudaResourceTypeLinear;
+      rd.res.linear.devPtr = f->d_lines;
+      rd.res.linear.desc = cudaCreateChannelDesc<int4>();
+      rd.res.linear.sizeInBytes = f->g.total_words * 8;
+      cudaTextureDesc td{};
+      td.readMode = cudaReadModeElementType;
+      if (cudaCreateTextureObject(&f->tex, &rd, &td, nullptr) != cudaSuccess) {
+        cudaGetLastError();
+        f->tex = 0;
+      }
+    }
+  }
   check_cuda(cudaMemcpy(f->root, f->d_lines, sizeof f->root, cudaMemcpyDeviceToHost), "read root line");
   f->root_ready = true;
 }
