@@ -354,3 +354,24 @@ def test_depth6_tree(lpm, orc, cuda):
             np.testing.assert_array_equal(out.cpu().numpy().astype(np.uint32), want, err_msg=f"T={t}")
             if checked:
                 assert dev.violations() == 0
+
+
+def test_golden_fixtures_on_gpu(lpm, cuda):
+    """The reference-generated golden answers (tests/golden, make_golden.py): every
+    fixture key looked up on the GPU equals the reference's own interval oracle and
+    linear (brute-force) oracle, every kernel mode."""
+    from pathlib import Path
+    files = sorted((Path(__file__).resolve().parent / "golden").glob("*.npz"))
+    assert files
+    for f in files:
+        d = np.load(f)
+        fib = lpm.FibTable(int(d["default_nh"][0]), d["rules"])
+        keys = d["keys"].astype(np.uint64)
+        addrs = addrs_from_keys(keys, np.random.default_rng(0))
+        dev = lpm.Fib.build(fib)
+        geo = dev.geometry
+        for t in [None] + list(range(geo.depth + geo.leaf_image + 1)):
+            dev.set_kernel_config(smem_levels=t)
+            got = run_lookup(cuda, dev, addrs).astype(np.uint32)
+            np.testing.assert_array_equal(got, d["interval_oracle"], err_msg=f"{f.name} T={t}")
+            np.testing.assert_array_equal(got, d["linear_oracle"], err_msg=f"{f.name} T={t}")
