@@ -245,6 +245,22 @@ __device__ __forceinline__ unsigned node_rank_smem(const unsigned long long* lvl
   return c;
 }
 
+// The same search on a shared-memory byte address: each probe is one LDS at an
+// immediate offset, one 64-bit compare and one predicated add of the address
+// (4 instructions; the compiler's own lowering of the index form takes 6).
+// Returns the byte offset of the final position, 8 * rank.
+__device__ __forceinline__ unsigned node_rank_saddr(uint32_t a, unsigned long long q) {
+  const uint32_t a0 = a;
+  asm("{\n\t.reg .pred p;\n\t.reg .b64 k;\n\t"
+      "ld.shared.u64 k, [%0+56];\n\tsetp.le.u64 p, k, %1;\n\t@p add.u32 %0, %0, 64;\n\t"
+      "ld.shared.u64 k, [%0+24];\n\tsetp.le.u64 p, k, %1;\n\t@p add.u32 %0, %0, 32;\n\t"
+      "ld.shared.u64 k, [%0+8];\n\tsetp.le.u64 p, k, %1;\n\t@p add.u32 %0, %0, 16;\n\t"
+      "ld.shared.u64 k, [%0];\n\tsetp.le.u64 p, k, %1;\n\t@p add.u32 %0, %0, 8;\n\t}"
+      : "+r"(a)
+      : "l"(q));
+  return a - a0;
+}
+
 // Rank of q over the 4-lane group's line quarter: lane j holds keys 4j..4j+3;
 // `nvalid` of them (per lane) are keys. Listing 1's popcnt(cmpge(q, node)).
 __device__ __forceinline__ unsigned group_rank(unsigned long long q, const unsigned long long (&w)[4], unsigned nvalid,
@@ -360,6 +376,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
   const unsigned long long nwarps = (static_cast<unsigned long long>(gridDim.x) * blockDim.x) >> 5;
   const uint64_t pol_stream = policy_evict_first();
   const unsigned TA = p.smem_levels;
+  const uint32_t s_base = smem_u32(s_lines);  // shared-space byte address of the image
   const unsigned leaf_valid = (F::kL - 4 * static_cast<int>(j)) < 0 ? 0u
                               : (F::kL - 4 * static_cast<int>(j)) > 4 ? 4u
                                                                       : static_cast<unsigned>(F::kL - 4 * j);
@@ -412,7 +429,8 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
             c |= (p.root[c] <= q) ? 1u : 0u;
             node[t] = c;
           } else {
-            node[t] = node[t] * 16u + node_rank_smem(s_lines + (p.level_start[l] >> 4) * 15u, node[t], key[t]);
+            const uint32_t lvl = s_base + static_cast<uint32_t>(p.level_start[l] >> 4) * 120u;
+            node[t] = node[t] * 16u + (node_rank_saddr(lvl + node[t] * 120u, key[t]) >> 3);
           }
           if (CHECKED && node[t] >= p.level_nodes[l + 1]) {
             violations |= 1u;
