@@ -472,11 +472,16 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
         nd[4 * t + s] = __shfl_sync(kFull, node[t], s, 4);
       }
     unsigned long long w[NS][4];
+    // Internal L2 levels [TA, DEPTH): a runtime-count loop (one back-edge per
+    // level instead of a compare-and-branch per possible level), then the leaf.
 #pragma unroll
-    for (int l = 0; l <= DEPTH; ++l) {
-      if (l < DEPTH && static_cast<unsigned>(l) < TA) continue;
-      // 32-bit word offsets (the layout keeps the array below 2^32 words): one
-      // IMAD + one IMAD.WIDE per address.
+    for (int li = 0; li < DEPTH; ++li) {
+      // Fully unrolled (static register indexing, scheduled across levels); the
+      // level index is TA-relative so the common TA == DEPTH case skips it with
+      // one uniform branch.
+      if (li >= DEPTH - static_cast<int>(TA)) break;
+      const unsigned l = TA + li;
+      // 32-bit word offsets (the layout keeps the array below 2^32 words).
       const unsigned base_w = static_cast<unsigned>(p.level_start[l]) + j * 4u;
       if (CHECKED) {
 #pragma unroll
@@ -492,7 +497,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
         // the two pipes of L1TEX share the load, which helps the deep trees (C2:
         // +8 %); leaves through the texture pipe lose on L2-missing workloads
         // (C1 -17 %), so they stay on the LSU path.
-        if (TEXL && l < DEPTH)
+        if (TEXL)
           tex_line_quarter(p.tex, (base_w + nd[s] * 16u) >> 1, w[s]);
         else
           ld_line_quarter(p.lines + (base_w + nd[s] * 16u), w[s]);
@@ -503,10 +508,30 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
           if ((st * TILES + t) * 32ull + lane < p.n) ++visits;
       }
 #pragma unroll
+      for (int s = 0; s < NS; ++s) nd[s] = nd[s] * 16u + group_rank(qk[s], w[s], 4u, gmask);
+    }
+    {  // the leaf line: ordinal = rank - 1
+      const unsigned base_w = static_cast<unsigned>(p.level_start[DEPTH]) + j * 4u;
+      if (CHECKED) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+          if (nd[s] >= p.level_nodes[DEPTH]) {
+            violations |= 2u;
+            nd[s] = 0;
+          }
+      }
+#pragma unroll
+      for (int s = 0; s < NS; ++s) ld_line_quarter(p.lines + (base_w + nd[s] * 16u), w[s]);
+      if (CHECKED) {
+#pragma unroll
+        for (int t = 0; t < TILES; ++t)
+          if ((st * TILES + t) * 32ull + lane < p.n) ++visits;
+      }
+#pragma unroll
       for (int s = 0; s < NS; ++s) {
-        const unsigned r = group_rank(qk[s], w[s], l < DEPTH ? 4u : leaf_valid, gmask);
-        if (CHECKED && l == DEPTH && r == 0) violations |= 4u;
-        nd[s] = (l < DEPTH) ? nd[s] * 16u + r : (CHECKED && r == 0 ? 0u : r - 1u);  // leaf: ordinal in line
+        const unsigned r = group_rank(qk[s], w[s], leaf_valid, gmask);
+        if (CHECKED && r == 0) violations |= 4u;
+        nd[s] = CHECKED && r == 0 ? 0u : r - 1u;
       }
     }
 
