@@ -206,6 +206,13 @@ int lpm6cu_lookup_batch(const lpm6cu_fib* fib, const void* addrs, uint64_t n, vo
  * only; one kernel launch on `stream`. Keys are clamped like address keys. */
 int lpm6cu_lookup_keys(const lpm6cu_fib* fib, const uint64_t* keys, uint64_t n, void* out, void* stream);
 
+/* search_batch: for n 8-byte keys, the interval ordinal of each —
+ * SearchResult::interval_ordinal, the index i into the interval map with
+ * boundaries[i] <= key < boundaries[i+1] — and, when next_hops is not NULL, its
+ * next hop. Device buffers; one kernel launch on `stream`. */
+int lpm6cu_search_batch(const lpm6cu_fib* fib, const uint64_t* keys, uint64_t n, uint32_t* ordinals, void* next_hops,
+                        void* stream);
+
 /* Packet-path ingest: n frames `stride` bytes apart in device memory
  * (e.g. a NIC RX ring written by GPUDirect), the IPv6 destination address at byte
  * `dst_offset` of each frame in network byte order (38 for Ethernet + IPv6). The

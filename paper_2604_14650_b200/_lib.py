@@ -117,6 +117,7 @@ SIGNATURES = {
     "lpm6cu_probe_smem": (I32, [I32, C.POINTER(C.c_double)]),
     "lpm6cu_lookup_keys": (I32, [P, P, U64, P, P]),
     "lpm6cu_lookup_packets": (I32, [P, P, U64, U64, U32, P, P]),
+    "lpm6cu_search_batch": (I32, [P, P, U64, P, P, P]),
     "lpm6cu_fib_build_from_intervals": (I32, [I32, P, P, U64, U32, C.POINTER(BuildOpts_t), P, C.POINTER(P)]),
     "lpm6_snapshot_encode": (I32, [P, P, U64, U32, P, U64, C.POINTER(U64)]),
     "lpm6_snapshot_save": (I32, [P, P, U64, U32, C.c_char_p]),

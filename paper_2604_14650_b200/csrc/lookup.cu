@@ -80,7 +80,7 @@ __device__ __forceinline__ uint4 ld_stream_v4(const uint4* p, uint64_t pol) {
 
 
 // Input formats of the lookup kernel.
-enum : int { kInAddr = 0, kInKey = 1, kInPacket = 2 };
+enum : int { kInAddr = 0, kInKey = 1, kInPacket = 2, kInKeyOrd = 3 };  // kInKeyOrd: keys in, ordinals out too
 
 template <class T>
 __device__ __forceinline__ T ld_stream(const void* p, uint64_t pol);
@@ -214,7 +214,8 @@ struct LookupParams {
   const unsigned long long* lines;                     // the tree, 16 u64 words per line
   unsigned long long level_start[LPM6CU_MAX_LEVELS];  // word offset of each level
   const uint4* addrs;               // kInAddr: 16-byte addresses (lookup_batch), or
-  const unsigned long long* keys;   // kInKey: 8-byte keys (lookup_keys: search_batch's input), or
+  const unsigned long long* keys;   // kInKey / kInKeyOrd: 8-byte keys (search_batch's input), or
+  unsigned int* ord;                // kInKeyOrd: interval ordinal per query (SearchResult::interval_ordinal)
   const unsigned char* pkts;        // kInPacket: frames, destination address at pkt_off of each
   unsigned long long pkt_stride;    //   bytes between frames
   unsigned int pkt_off;             //   byte offset of the IPv6 destination address in a frame
@@ -387,7 +388,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
     const unsigned long long qi = (st_ * TILES + t) * 32ull + lane;
     unsigned long long k = 0;
     if (qi < p.n) {
-      if constexpr (INPUT == kInKey) {
+      if constexpr (INPUT == kInKey || INPUT == kInKeyOrd) {
         k = ld_stream<unsigned long long>(p.keys + qi, pol_stream);
       } else if constexpr (INPUT == kInPacket) {
         k = load_dst_key(p.pkts + qi * p.pkt_stride, p.pkt_off, p.pkt_align, pol_stream);
@@ -510,6 +511,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
 #pragma unroll
       for (int s = 0; s < NS; ++s) nd[s] = nd[s] * 16u + group_rank(qk[s], w[s], 4u, gmask);
     }
+    unsigned leafn[INPUT == kInKeyOrd ? NS : 1];  // kInKeyOrd: leaf node of each query
     {  // the leaf line: ordinal = rank - 1
       const unsigned base_w = static_cast<unsigned>(p.level_start[DEPTH]) + j * 4u;
       if (CHECKED) {
@@ -522,6 +524,10 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
       }
 #pragma unroll
       for (int s = 0; s < NS; ++s) ld_line_quarter(p.lines + (base_w + nd[s] * 16u), w[s]);
+      if constexpr (INPUT == kInKeyOrd) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) leafn[s] = nd[s];
+      }
       if (CHECKED) {
 #pragma unroll
         for (int t = 0; t < TILES; ++t)
@@ -535,6 +541,17 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
       }
     }
 
+    if constexpr (INPUT == kInKeyOrd) {  // lane j stores the ordinal of its own query (4t + j of the group)
+#pragma unroll
+      for (int t = 0; t < TILES; ++t) {
+        unsigned o = leafn[4 * t] * F::kL + nd[4 * t];
+#pragma unroll
+        for (int s = 1; s < 4; ++s) o = j == static_cast<unsigned>(s) ? leafn[4 * t + s] * F::kL + nd[4 * t + s] : o;
+        const unsigned long long qi = (st * TILES + t) * 32ull + lane;
+        if (qi < p.n) asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p.ord + qi), "r"(o));
+      }
+      if (p.out == nullptr) continue;  // ordinals only
+    }
     // Leaf values: the value lane extracts the group's next hops and stores them.
     if (j == static_cast<unsigned>(F::kValueLane)) {
 #pragma unroll
@@ -636,6 +653,9 @@ KernelFn pick_kernel(int vb, int depth, int tiles, int threads, int minb, bool c
     if (input == kInPacket)
       return checked ? pick_vb<1, 1024, 1, true, kInPacket>(vb, depth)
                      : pick_vb<1, 1024, 1, false, kInPacket>(vb, depth);
+    if (input == kInKeyOrd)
+      return checked ? pick_vb<1, 1024, 1, true, kInKeyOrd>(vb, depth)
+                     : pick_vb<1, 1024, 1, false, kInKeyOrd>(vb, depth);
     return nullptr;
   }
   if (checked) return (tiles == 1 && threads == 1024 && minb == 1) ? pick_vb<1, 1024, 1, true>(vb, depth) : nullptr;
@@ -705,7 +725,7 @@ struct lpm6cu_fib {
   std::mutex host_mu;
   std::unique_ptr<HostPipeline> pipe;
   std::mutex plan_mu;
-  LaunchPlan plans[3][2];  // [input format][checked]
+  LaunchPlan plans[4][2];  // [input format][checked]
   unsigned long long root[16] = {};  // host copy of the root line (kernel parameter)
   cudaTextureObject_t tex = 0;       // texture object over the line array
   bool root_ready = false;
@@ -823,7 +843,7 @@ struct PacketInput {
 // input: kInAddr (d_in = 16-byte addresses, configured shape), kInKey (8-byte
 // keys) or kInPacket (frames described by pk); the last two use the default shape.
 void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, void* d_out, cudaStream_t stream,
-                   int input = kInAddr, const PacketInput* pk = nullptr) {
+                   int input = kInAddr, const PacketInput* pk = nullptr, unsigned* d_ord = nullptr) {
   if (n == 0) return;
   const bool dflt = input != kInAddr;
   const unsigned tiles = dflt ? 1 : f->cfg.queries_per_lane;
@@ -863,8 +883,9 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
   LookupParams p{};
   p.lines = f->d_lines;
   for (int l = 0; l < LPM6CU_MAX_LEVELS; ++l) p.level_start[l] = f->g.level_start[l];
-  if (input == kInKey) {
+  if (input == kInKey || input == kInKeyOrd) {
     p.keys = static_cast<const unsigned long long*>(d_in);
+    p.ord = d_ord;
   } else if (input == kInPacket) {
     p.pkts = static_cast<const unsigned char*>(d_in);
     p.pkt_stride = pk->stride;
@@ -1178,6 +1199,21 @@ int lpm6cu_lookup_keys(const lpm6cu_fib* fib, const uint64_t* keys, uint64_t n, 
       throw Error(Errc::InvalidArgument, "lpm6cu_lookup_keys takes device buffers");
     if (reinterpret_cast<uintptr_t>(keys) % 8 != 0) throw Error(Errc::InvalidArgument, "keys must be 8-byte aligned");
     launch_lookup(fib, keys, n, out, static_cast<cudaStream_t>(stream), kInKey);
+  });
+}
+
+int lpm6cu_search_batch(const lpm6cu_fib* fib, const uint64_t* keys, uint64_t n, uint32_t* ordinals, void* next_hops,
+                        void* stream) {
+  return guard([&] {
+    if (!fib) throw Error(Errc::InvalidArgument, "NULL fib");
+    if (n == 0) return;
+    if (!keys || !ordinals) throw Error(Errc::InvalidArgument, "NULL buffer");
+    DeviceGuard dg(fib->device);
+    if (!is_device_ptr(keys) || !is_device_ptr(ordinals) || (next_hops && !is_device_ptr(next_hops)))
+      throw Error(Errc::InvalidArgument, "lpm6cu_search_batch takes device buffers");
+    if (reinterpret_cast<uintptr_t>(keys) % 8 != 0 || reinterpret_cast<uintptr_t>(ordinals) % 4 != 0)
+      throw Error(Errc::InvalidArgument, "keys must be 8-byte and ordinals 4-byte aligned");
+    launch_lookup(fib, keys, n, next_hops, static_cast<cudaStream_t>(stream), kInKeyOrd, nullptr, ordinals);
   });
 }
 

@@ -235,6 +235,29 @@ class Fib:
         check(lib().lpm6cu_lookup_keys(self._h, kptr, n, optr, _stream_handle(stream)))
         return out
 
+    def search_batch(self, keys, ordinals=None, next_hops=None, stream=None, with_next_hops: bool = True):
+        """search_batch (S:299-307): interval ordinals (int32 tensor; SearchResult::
+        interval_ordinal) and, unless with_next_hops is False, next hops of n 8-byte
+        keys. Device buffers; one kernel launch on ``stream``."""
+        torch = _torch()
+        vb = self.value_bytes
+        kptr, n, kdev = _ptr_len(keys, 8)
+        if ordinals is None:
+            ordinals = torch.empty(n, dtype=torch.int32, device=keys.device)
+        if next_hops is None and with_next_hops:
+            dt = {1: torch.uint8, 2: torch.int16, 4: torch.int32}[vb]
+            next_hops = torch.empty(n, dtype=dt, device=keys.device)
+        optr, nout, _ = _ptr_len(ordinals, 4)
+        if nout < n:
+            raise Lpm6Error(9, f"ordinals holds {nout} entries, need {n}")
+        hptr = None
+        if next_hops is not None:
+            hptr, nh, _ = _ptr_len(next_hops, vb)
+            if nh < n:
+                raise Lpm6Error(9, f"next_hops holds {nh} entries, need {n}")
+        check(lib().lpm6cu_search_batch(self._h, kptr, n, optr, hptr, _stream_handle(stream)))
+        return ordinals, next_hops
+
     def lookup_packets(self, frames, n: int, stride: int, dst_offset: int = 38, out=None, stream=None):
         """Next hops of n frames ``stride`` bytes apart in a device buffer, the IPv6
         destination at ``dst_offset`` (network order; 38 = Ethernet + IPv6)."""

@@ -164,3 +164,33 @@ def test_single_process_nccl_replication(lpm, orc, cuda):
     with pytest.raises(lpm.Lpm6Error) as e:
         src.replicate([len(devices)])  # devices[0] must be the source device
     assert e.value.code in ("InvalidArgument", "CudaError")
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2])
+def test_search_batch_ordinals(lpm, orc, cuda, kind):
+    """search_batch: the interval ordinal of every key is the oracle's
+    upper_bound - 1 (intervals.cpp:142-145), and the next hops match; ordinals-only
+    mode writes no next hops."""
+    torch = cuda
+    fib = lpm.workload_fib(kind)
+    imap = lpm.build_intervals(fib)
+    rng = np.random.default_rng(20 + kind)
+    keys = np.concatenate([boundary_probe_keys(imap.boundaries), rng.integers(0, 2**64, 1 << 18, dtype=np.uint64)])
+    clamped = np.minimum(keys, np.uint64(2**64 - 2))
+    want_ord = np.searchsorted(imap.boundaries, clamped, side="right") - 1
+    want_nh, _ = orc.lookup_batch(0, imap.boundaries, imap.next_hops, addrs_from_keys(keys), threads=8)
+    dev = lpm.Fib.build(fib)
+    dk = torch.from_numpy(keys.view(np.int64)).cuda()
+    for checked in (False, True):
+        dev.set_checked(checked)
+        ords, nhs = dev.search_batch(dk)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(ords.cpu().numpy().astype(np.int64), want_ord)
+        np.testing.assert_array_equal(nhs.cpu().numpy().view(VDT[dev.geometry.value_bytes]).astype(np.uint32),
+                                      want_nh)
+        assert np.array_equal(imap.next_hops[want_ord], want_nh)
+    dev.set_checked(False)
+    ords, nhs = dev.search_batch(dk, with_next_hops=False)
+    torch.cuda.synchronize()
+    assert nhs is None
+    np.testing.assert_array_equal(ords.cpu().numpy().astype(np.int64), want_ord)
