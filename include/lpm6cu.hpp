@@ -123,6 +123,12 @@ class Fib {
     lpm6cu::check(lpm6cu_lookup_keys(h_, d_keys, n, d_out, stream));
   }
 
+  // search_batch: interval ordinals (+ next hops when d_next_hops != nullptr); device buffers.
+  void search_batch(const uint64_t* d_keys, uint64_t n, uint32_t* d_ordinals, void* d_next_hops = nullptr,
+                    void* stream = nullptr) const {
+    lpm6cu::check(lpm6cu_search_batch(h_, d_keys, n, d_ordinals, d_next_hops, stream));
+  }
+
   // Frames `stride` bytes apart, IPv6 destination at `dst_offset` (38 = Ethernet + IPv6); device buffers.
   void lookup_packets(const void* d_frames, uint64_t n, uint64_t stride, uint32_t dst_offset, void* d_out,
                       void* stream = nullptr) const {
