@@ -209,9 +209,9 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
   // Leaf-image mode serves address input; key / packet input uses the internal image only.
   const bool leafs = leaf_image_mode(f) && input == kInAddr;
   // Texture pipe for internal L2 levels when the tree has any (smem_levels < depth).
-  const bool texl = f->tex && !leafs && input == kInAddr && f->d_err == nullptr && f->cfg.smem_levels < f->g.depth &&
-                    tiles == 1 && threads_cta == 1024 && minb == 1 && f->g.depth >= 2;
   const unsigned smem_levels = leaf_image_mode(f) && !leafs ? f->g.depth : f->cfg.smem_levels;
+  const bool texl = f->tex && !leafs && input != kInKeyOrd && f->d_err == nullptr && smem_levels < f->g.depth &&
+                    tiles == 1 && threads_cta == 1024 && minb == 1 && f->g.depth >= 2;
   const size_t smem = image_bytes_of(f->g, smem_levels);
   const int threads = static_cast<int>(threads_cta);
   LaunchPlan plan;

@@ -564,15 +564,25 @@ using KernelFn = void (*)(const LookupParams);
 
 // Instantiated shapes: (queries per lane, min CTAs per SM) for every depth and
 // value width; the tuning grid below is measured by bench.py --sweep.
-template <int VB>
+template <int VB, int INPUT>
 KernelFn pick_depth_texl(int depth) {
   switch (depth) {
-    case 2: return lpm6_lookup_kernel<2, VB, 1, 1024, 1, false, kInAddr, false, true>;
-    case 3: return lpm6_lookup_kernel<3, VB, 1, 1024, 1, false, kInAddr, false, true>;
-    case 4: return lpm6_lookup_kernel<4, VB, 1, 1024, 1, false, kInAddr, false, true>;
-    case 5: return lpm6_lookup_kernel<5, VB, 1, 1024, 1, false, kInAddr, false, true>;
-    case 6: return lpm6_lookup_kernel<6, VB, 1, 1024, 1, false, kInAddr, false, true>;
-    case 7: return lpm6_lookup_kernel<7, VB, 1, 1024, 1, false, kInAddr, false, true>;
+    case 2: return lpm6_lookup_kernel<2, VB, 1, 1024, 1, false, INPUT, false, true>;
+    case 3: return lpm6_lookup_kernel<3, VB, 1, 1024, 1, false, INPUT, false, true>;
+    case 4: return lpm6_lookup_kernel<4, VB, 1, 1024, 1, false, INPUT, false, true>;
+    case 5: return lpm6_lookup_kernel<5, VB, 1, 1024, 1, false, INPUT, false, true>;
+    case 6: return lpm6_lookup_kernel<6, VB, 1, 1024, 1, false, INPUT, false, true>;
+    case 7: return lpm6_lookup_kernel<7, VB, 1, 1024, 1, false, INPUT, false, true>;
+    default: return nullptr;
+  }
+}
+
+template <int INPUT>
+KernelFn pick_vb_texl(int vb, int depth) {
+  switch (vb) {
+    case 1: return pick_depth_texl<1, INPUT>(depth);
+    case 2: return pick_depth_texl<2, INPUT>(depth);
+    case 4: return pick_depth_texl<4, INPUT>(depth);
     default: return nullptr;
   }
 }
@@ -617,13 +627,13 @@ KernelFn pick_vb(int vb, int depth) {
 // bench.py --sweep measures them. The checked variant exists for the default shape.
 KernelFn pick_kernel(int vb, int depth, int tiles, int threads, int minb, bool checked = false,
                      int input = kInAddr, bool leafs = false, bool texl = false) {
-  if (texl) {  // internal L2 levels via the texture pipe: address input, default shape, unchecked
-    if (leafs || checked || input != kInAddr || tiles != 1 || threads != 1024 || minb != 1) return nullptr;
-    switch (vb) {
-      case 1: return pick_depth_texl<1>(depth);
-      case 2: return pick_depth_texl<2>(depth);
-      case 4: return pick_depth_texl<4>(depth);
-      default: return nullptr;
+  if (texl) {  // internal L2 levels via the texture pipe: default shape, unchecked
+    if (leafs || checked || tiles != 1 || threads != 1024 || minb != 1) return nullptr;
+    switch (input) {
+      case kInAddr: return pick_vb_texl<kInAddr>(vb, depth);
+      case kInKey: return pick_vb_texl<kInKey>(vb, depth);
+      case kInPacket: return pick_vb_texl<kInPacket>(vb, depth);
+      default: return nullptr;  // kInKeyOrd: LSU loads
     }
   }
   if (leafs) {  // leaf image: address input, default shape, depth <= kMaxLeafImageDepth
