@@ -182,7 +182,25 @@ def time_extras(lpm, torch, fdev, fib, addrs, n, vb, stream, device):
     ms = _time_ms(torch, lambda: fdev.lookup_keys(keys, ko, stream), stream)
     out["keys8"] = {"value": n / ms / 1e6, "unit": UNIT, "ms": ms, "dram_bytes_per_query": 8 + vb,
                     "matches_address_path": bool(torch.equal(ko, ref))}
-    del keys, ko
+    # the same keys from pinned host memory through the C ABI: 8 + vb bytes over PCIe per query
+    hk = torch.empty(n, dtype=torch.int64, pin_memory=True)
+    hk.copy_(keys)
+    ho = torch.empty(n * vb, dtype=torch.uint8, pin_memory=True)
+    hk_np, ho_np = hk.numpy(), ho.numpy()
+    fdev.lookup_keys(hk_np, ho_np)  # warm-up
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(3):
+        fdev.lookup_keys(hk_np, ho_np)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 3
+    out["keys8_e2e"] = {"value": n / ms / 1e6, "unit": UNIT, "ms": ms, "h2d_bytes_per_step": n * 8,
+                        "d2h_bytes_per_step": n * vb,
+                        "matches_address_path": bool(np.array_equal(ho_np, ref.view(torch.uint8).cpu().numpy())),
+                        "path": "lpm6cu_lookup_keys(host pinned buffers)"}
+    del keys, ko, hk, ho
     m = min(n, 1 << 26)
     frames = torch.zeros((m, 64), dtype=torch.uint8, device=addrs.device)
     frames[:, 12] = 0x86  # EtherType 0x86DD

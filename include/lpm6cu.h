@@ -202,8 +202,9 @@ int lpm6cu_lookup_batch(const lpm6cu_fib* fib, const void* addrs, uint64_t n, vo
                         void* stream);
 
 /* 8-byte keys instead of 16-byte addresses — the input of the reference's
- * search_batch(t, keys[B]) and of its PBTR traces. Device buffers
- * only; one kernel launch on `stream`. Keys are clamped like address keys. */
+ * search_batch(t, keys[B]) and of its PBTR traces. Keys are clamped
+ * like address keys. Device buffers: one kernel launch on `stream`; host buffers:
+ * the pipelined H2D / kernel / D2H path with half the PCIe bytes of addresses. */
 int lpm6cu_lookup_keys(const lpm6cu_fib* fib, const uint64_t* keys, uint64_t n, void* out, void* stream);
 
 /* search_batch: for n 8-byte keys, the interval ordinal of each —

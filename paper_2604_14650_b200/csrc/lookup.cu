@@ -336,7 +336,11 @@ bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-void lookup_host(lpm6cu_fib* f, const void* addrs, unsigned long long n, void* out, cudaStream_t user) {
+// Host buffers: chunked H2D / kernel / D2H on three streams ordered after `user`.
+// input = kInAddr (16-byte addresses) or kInKey (8-byte keys: half the PCIe bytes).
+void lookup_host(lpm6cu_fib* f, const void* addrs, unsigned long long n, void* out, cudaStream_t user,
+                 int input = kInAddr) {
+  const unsigned long long in_bytes = input == kInKey ? 8 : 16;
   std::lock_guard<std::mutex> lk(f->host_mu);
   const unsigned vb = f->g.value_bytes;
   if (!f->pipe) {
@@ -359,8 +363,9 @@ void lookup_host(lpm6cu_fib* f, const void* addrs, unsigned long long n, void* o
   int s = 0;
   for (unsigned long long off = 0; off < n; off += pp.chunk, s = (s + 1) % HostPipeline::kStreams) {
     const unsigned long long m = std::min(pp.chunk, n - off);
-    check_cuda(cudaMemcpyAsync(pp.d_in[s], src + off * 16, m * 16, cudaMemcpyHostToDevice, pp.streams[s]), "H2D");
-    launch_lookup(f, pp.d_in[s], m, pp.d_out[s], pp.streams[s]);
+    check_cuda(cudaMemcpyAsync(pp.d_in[s], src + off * in_bytes, m * in_bytes, cudaMemcpyHostToDevice, pp.streams[s]),
+               "H2D");
+    launch_lookup(f, pp.d_in[s], m, pp.d_out[s], pp.streams[s], input);
     check_cuda(cudaMemcpyAsync(dst + off * vb, pp.d_out[s], m * vb, cudaMemcpyDeviceToHost, pp.streams[s]), "D2H");
   }
   for (int i = 0; i < HostPipeline::kStreams; ++i) check_cuda(cudaStreamSynchronize(pp.streams[i]), "sync");
@@ -552,10 +557,13 @@ int lpm6cu_lookup_keys(const lpm6cu_fib* fib, const uint64_t* keys, uint64_t n, 
     if (n == 0) return;
     if (!keys || !out) throw Error(Errc::InvalidArgument, "NULL buffer");
     DeviceGuard dg(fib->device);
-    if (!is_device_ptr(keys) || !is_device_ptr(out))
-      throw Error(Errc::InvalidArgument, "lpm6cu_lookup_keys takes device buffers");
+    const bool dk = is_device_ptr(keys), dout = is_device_ptr(out);
+    if (dk != dout) throw Error(Errc::InvalidArgument, "keys and results must both be device or both be host memory");
     if (reinterpret_cast<uintptr_t>(keys) % 8 != 0) throw Error(Errc::InvalidArgument, "keys must be 8-byte aligned");
-    launch_lookup(fib, keys, n, out, static_cast<cudaStream_t>(stream), kInKey);
+    if (dk)
+      launch_lookup(fib, keys, n, out, static_cast<cudaStream_t>(stream), kInKey);
+    else
+      lookup_host(const_cast<lpm6cu_fib*>(fib), keys, n, out, static_cast<cudaStream_t>(stream), kInKey);
   });
 }
 

@@ -221,18 +221,24 @@ class Fib:
 
 
     def lookup_keys(self, keys, out=None, stream=None):
-        """Next hops of n 8-byte keys (search_batch's input): device buffers,
-        one asynchronous kernel launch on ``stream``."""
+        """Next hops of n 8-byte keys (search_batch's input). Device
+        buffers: one asynchronous kernel launch on ``stream``; host buffers (numpy):
+        the pipelined copy path, returns when ``out`` is filled."""
         vb = self.value_bytes
         kptr, n, kdev = _ptr_len(keys, 8)
         if out is None:
-            torch = _torch()
-            dt = {1: torch.uint8, 2: torch.int16, 4: torch.int32}[vb]
-            out = torch.empty(n, dtype=dt, device=keys.device if kdev else "cuda")
+            if kdev:
+                torch = _torch()
+                dt = {1: torch.uint8, 2: torch.int16, 4: torch.int32}[vb]
+                out = torch.empty(n, dtype=dt, device=keys.device)
+            else:
+                out = np.empty(n, _NP_VDT[vb])
         optr, nout, odev = _ptr_len(out, vb)
         if nout < n:
             raise Lpm6Error(9, f"out holds {nout} next hops, need {n}")
-        check(lib().lpm6cu_lookup_keys(self._h, kptr, n, optr, _stream_handle(stream)))
+        if kdev != odev:
+            raise Lpm6Error(9, "keys and out must both be device or both be host buffers")
+        check(lib().lpm6cu_lookup_keys(self._h, kptr, n, optr, _stream_handle(stream) if kdev else None))
         return out
 
     def search_batch(self, keys, ordinals=None, next_hops=None, stream=None, with_next_hops: bool = True):

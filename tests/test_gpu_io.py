@@ -194,3 +194,16 @@ def test_search_batch_ordinals(lpm, orc, cuda, kind):
     torch.cuda.synchronize()
     assert nhs is None
     np.testing.assert_array_equal(ords.cpu().numpy().astype(np.int64), want_ord)
+
+
+def test_lookup_keys_host_buffers(lpm, orc, cuda):
+    """lookup_keys with numpy (host) buffers: the pipelined path with 8-byte keys."""
+    fib = lpm.workload_fib(1)
+    imap = lpm.build_intervals(fib)
+    rng = np.random.default_rng(31)
+    keys = np.concatenate([boundary_probe_keys(imap.boundaries),
+                           rng.integers(0, 2**64, (1 << 24) + 777, dtype=np.uint64)])  # > 2 chunks, ragged
+    want, _ = orc.lookup_batch(0, imap.boundaries, imap.next_hops, addrs_from_keys(keys), threads=8)
+    dev = lpm.Fib.build(fib)
+    got = dev.lookup_keys(keys)
+    np.testing.assert_array_equal(got.astype(np.uint32), want)
