@@ -25,6 +25,8 @@
  *   - Next hops are written at the FIB's value width (1, 2 or 4 bytes, little-endian).
  *   - A FIB handle is immutable after creation: any number of lookups on any
  *     streams may run on it concurrently (the reference's contract).
+ *     The tuning calls (lpm6cu_fib_set_kernel_config, lpm6cu_fib_set_checked)
+ *     change how later lookups run and must not race with lookups on the handle.
  *   - There is no CPU fallback: a lookup without a usable CUDA device fails with
  *     LPM6CU_E_CUDA.
  */
