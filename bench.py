@@ -298,13 +298,17 @@ def cpu_threads():
 
 
 def cpu_model():
+    """'<model name>, <nproc> CPUs, avx512f yes/no' (SURVEY §8d asks for all three)."""
+    name, avx512 = "unknown", False
     try:
         for line in open("/proc/cpuinfo"):
-            if line.startswith("model name"):
-                return line.split(":", 1)[1].strip()
+            if line.startswith("model name") and name == "unknown":
+                name = line.split(":", 1)[1].strip()
+            if line.startswith("flags"):
+                avx512 = avx512 or " avx512f" in line
     except Exception:
         pass
-    return "unknown"
+    return f"{name}, {os.cpu_count()} CPUs, avx512f {'yes' if avx512 else 'no'}"
 
 
 def reference_sample(lpm, workload, n):
