@@ -375,3 +375,23 @@ def test_golden_fixtures_on_gpu(lpm, cuda):
             got = run_lookup(cuda, dev, addrs).astype(np.uint32)
             np.testing.assert_array_equal(got, d["interval_oracle"], err_msg=f"{f.name} T={t}")
             np.testing.assert_array_equal(got, d["linear_oracle"], err_msg=f"{f.name} T={t}")
+
+
+@pytest.mark.parametrize("n", [50, 5000, 50000])
+def test_merge_on_off_same_answers(lpm, orc, cuda, n):
+    """Adjacent-interval merge ON vs OFF (intervals.hpp:26-29): different maps,
+    identical lookups on the GPU, both equal to the oracle."""
+    from paper_2604_14650_b200.fib import PREFIX_DTYPE
+    rng = np.random.default_rng(40 + n)
+    rules = random_fib_rules(rng, n, PREFIX_DTYPE, True, nest_p=0.5)
+    rules["next_hop"] = rng.integers(1, 4, len(rules))  # few next hops: many mergeable neighbours
+    fib = lpm.FibTable(0, rules)
+    on, off = lpm.build_intervals(fib, True), lpm.build_intervals(fib, False)
+    assert len(off) > len(on)
+    keys = np.concatenate([boundary_probe_keys(off.boundaries), rng.integers(0, 2**64, 20000, dtype=np.uint64)])
+    addrs = addrs_from_keys(keys, rng)
+    want = oracle_next_hops(orc, on.boundaries, on.next_hops, addrs)
+    for merge in (True, False):
+        dev = lpm.Fib.build(fib, merge_adjacent=merge)
+        assert dev.geometry.num_keys == (len(on) if merge else len(off))
+        np.testing.assert_array_equal(run_lookup(cuda, dev, addrs).astype(np.uint32), want)
