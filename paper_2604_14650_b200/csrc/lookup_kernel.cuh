@@ -343,21 +343,6 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
   extern __shared__ __align__(128) unsigned long long s_lines[];
   __shared__ __align__(8) uint64_t s_bar;
 
-  if (p.smem_bytes > 0) {
-    if (threadIdx.x == 0) {
-      mbar_init(&s_bar, 1);
-      mbar_arrive_expect_tx(&s_bar, p.smem_bytes);
-      constexpr uint32_t kChunk = 32768;
-      for (uint32_t off = 0; off < p.smem_bytes; off += kChunk) {
-        const uint32_t sz = min(kChunk, p.smem_bytes - off);
-        bulk_g2s(reinterpret_cast<char*>(s_lines) + off, reinterpret_cast<const char*>(p.image) + off, sz,
-                 &s_bar);
-      }
-    }
-    __syncthreads();
-    mbar_wait(&s_bar, 0);
-  }
-
   const unsigned lane = threadIdx.x & 31u;
   const unsigned j = lane & 3u;                 // lane within the 4-lane group
   const unsigned gbase = lane & ~3u;            // first lane (= first query) of the group
@@ -391,6 +376,23 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
   unsigned long long next_key[TILES];
 #pragma unroll
   for (int t = 0; t < TILES; ++t) next_key[t] = load_key(warp0, t);
+
+  // Stage the image after the first addresses are requested, so their DRAM/L2
+  // latency overlaps the bulk copy (it matters for small batches).
+  if (p.smem_bytes > 0) {
+    if (threadIdx.x == 0) {
+      mbar_init(&s_bar, 1);
+      mbar_arrive_expect_tx(&s_bar, p.smem_bytes);
+      constexpr uint32_t kChunk = 32768;
+      for (uint32_t off = 0; off < p.smem_bytes; off += kChunk) {
+        const uint32_t sz = min(kChunk, p.smem_bytes - off);
+        bulk_g2s(reinterpret_cast<char*>(s_lines) + off, reinterpret_cast<const char*>(p.image) + off, sz,
+                 &s_bar);
+      }
+    }
+    __syncthreads();
+    mbar_wait(&s_bar, 0);
+  }
 
   for (unsigned long long st = warp0; st * (32ull * TILES) < p.n; st += nwarps) {
     unsigned long long key[TILES];
