@@ -4,6 +4,7 @@ The layout is checked by walking it in numpy exactly as the kernel does (test
 code only — the product has no CPU lookup) and comparing with the oracle.
 """
 import ctypes as C
+import os
 import re
 from pathlib import Path
 
@@ -245,3 +246,14 @@ def test_reference_dropin_without_gpu():
     r = subprocess.run([str(exe), "3000", "20000", "--no-gpu-ok"], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "CudaError" in r.stdout
+
+
+def test_missing_library_fails_loudly():
+    """Without the built library the package refuses to run (no CPU fallback)."""
+    import subprocess
+    import sys
+    code = ("import paper_2604_14650_b200 as lpm\n"
+            "try:\n    lpm.workload_fib(0)\nexcept ImportError as e:\n    print('ImportError', e)\n")
+    env = dict(os.environ, LPM6CU_LIB="/nonexistent/liblpm6cu.so")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=120)
+    assert "ImportError" in r.stdout and "no CPU fallback" in r.stdout, r.stdout + r.stderr
