@@ -395,3 +395,18 @@ def test_merge_on_off_same_answers(lpm, orc, cuda, n):
         dev = lpm.Fib.build(fib, merge_adjacent=merge)
         assert dev.geometry.num_keys == (len(on) if merge else len(off))
         np.testing.assert_array_equal(run_lookup(cuda, dev, addrs).astype(np.uint32), want)
+
+
+def test_plain_c_caller(cuda, tmp_path):
+    """tests/c/capi_demo.c — a C99 program using only include/lpm6cu.h — on the GPU."""
+    import subprocess
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    lib = root / "paper_2604_14650_b200" / "lib"
+    exe = tmp_path / "capi_demo"
+    r = subprocess.run(["gcc", "-std=c99", "-I", str(root / "include"), str(root / "tests" / "c" / "capi_demo.c"),
+                        "-L", str(lib), "-llpm6cu", f"-Wl,-rpath,{lib}", "-o", str(exe)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    run = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert run.returncode == 0 and "capi_demo ok" in run.stdout, run.stdout + run.stderr

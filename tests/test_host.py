@@ -14,6 +14,7 @@ import pytest
 from _util import MASK64, addrs_from_keys, boundary_probe_keys, random_fib_rules
 
 ROOT = Path(__file__).resolve().parents[1]
+LIB_DIR = ROOT / "paper_2604_14650_b200" / "lib"
 
 
 # ---- the C ABI library -----------------------------------------------------------------------
@@ -257,3 +258,15 @@ def test_missing_library_fails_loudly():
     env = dict(os.environ, LPM6CU_LIB="/nonexistent/liblpm6cu.so")
     r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=120)
     assert "ImportError" in r.stdout and "no CPU fallback" in r.stdout, r.stdout + r.stderr
+
+
+def test_header_is_plain_c(tmp_path):
+    """include/lpm6cu.h compiles as C99 and a C program links against the library."""
+    import subprocess
+    exe = tmp_path / "capi_demo"
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-Werror", "-I", str(ROOT / "include"),
+                        str(ROOT / "tests" / "c" / "capi_demo.c"), "-L", str(LIB_DIR), "-llpm6cu",
+                        f"-Wl,-rpath,{LIB_DIR}", "-o", str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    run = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert run.returncode in (0, 2), run.stdout + run.stderr  # 2: no GPU in this container
