@@ -139,6 +139,7 @@ int lpm6_parse_prefix(const char* text, lpm6cu_prefix* out, int* masked) {
 
 int lpm6_workload_info_get(int workload, lpm6_workload_info* info) {
   return guard([&] {
+    if (!info) throw Error(Errc::InvalidArgument, "NULL info");
     WorkloadConfig c = workload_config(workload);
     std::memset(info, 0, sizeof(*info));
     info->id = c.id;
@@ -153,6 +154,7 @@ int lpm6_workload_info_get(int workload, lpm6_workload_info* info) {
 int lpm6_workload_fib(int fib_kind, lpm6cu_prefix* out, uint64_t capacity, uint64_t* n_out,
                       uint32_t* default_nh) {
   return guard([&] {
+    if (!n_out) throw Error(Errc::InvalidArgument, "NULL n_out");
     FibTable fib = make_fib(fib_kind);
     *n_out = fib.size();
     if (default_nh) *default_nh = fib.default_next_hop();
@@ -172,6 +174,7 @@ int lpm6_workload_fib(int fib_kind, lpm6cu_prefix* out, uint64_t capacity, uint6
 int lpm6_workload_queries_host(int workload, const lpm6cu_prefix* rules, uint64_t nrules,
                                uint64_t first, uint64_t n, void* out, int threads) {
   return guard([&] {
+    if ((nrules && !rules) || (n && !out)) throw Error(Errc::InvalidArgument, "NULL argument");
     WorkloadConfig c = workload_config(workload);
     auto prefixes = to_prefixes(rules, nrules);
     QueryTables t = make_query_tables(std::span<const Prefix>(prefixes), c);

@@ -420,6 +420,7 @@ int lpm6cu_fib_build(int device, const lpm6cu_prefix* rules, uint64_t n, uint32_
                      const lpm6cu_build_opts* opts, lpm6cu_fib** out) {
   return guard([&] {
     if (n > 0 && !rules) throw Error(Errc::InvalidArgument, "rules is NULL");
+    if (!out) throw Error(Errc::InvalidArgument, "NULL out");
     Tree t = capi::build_device_tree(rules, n, default_nh, opts);
     lpm6cu_geometry g;
     capi::export_geometry(t.g, &g);
@@ -635,6 +636,7 @@ int lpm6cu_fib_build_from_intervals(int device, const uint64_t* boundaries, cons
 int lpm6cu_querygen_create(int device, int workload, const lpm6cu_prefix* rules, uint64_t nrules,
                            lpm6cu_querygen** out) {
   return guard([&] {
+    if (!out || (nrules && !rules)) throw Error(Errc::InvalidArgument, "NULL argument");
     WorkloadConfig c = workload_config(workload);
     auto prefixes = capi::to_prefixes(rules, nrules);
     QueryTables t = make_query_tables(std::span<const Prefix>(prefixes), c);

@@ -92,7 +92,9 @@ extern "C" {
 
 int lpm6cu_probe_l2_gather(int device, uint64_t buffer_bytes, uint32_t line_bytes, double* gbps) {
   return guard([&] {
+    if (!gbps) throw Error(Errc::InvalidArgument, "NULL gbps");
     if (line_bytes != 32 && line_bytes != 128) throw Error(Errc::InvalidArgument, "line_bytes must be 32 or 128");
+    if (buffer_bytes < line_bytes) throw Error(Errc::InvalidArgument, "buffer smaller than a line");
     check(cudaSetDevice(device), "cudaSetDevice");
     int sms = 0;
     check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "attr");
@@ -117,6 +119,7 @@ int lpm6cu_probe_l2_gather(int device, uint64_t buffer_bytes, uint32_t line_byte
 
 int lpm6cu_probe_smem(int device, double* gbps) {
   return guard([&] {
+    if (!gbps) throw Error(Errc::InvalidArgument, "NULL gbps");
     check(cudaSetDevice(device), "cudaSetDevice");
     int sms = 0;
     check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "attr");

@@ -410,3 +410,10 @@ def test_plain_c_caller(cuda, tmp_path):
     assert r.returncode == 0, r.stderr
     run = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert run.returncode == 0 and "capi_demo ok" in run.stdout, run.stdout + run.stderr
+
+
+def test_abi_rejects_null_arguments_on_gpu(cuda):
+    """The NULL/zero-argument probe of every ABI entry point with a device present
+    (calls get past the device checks here)."""
+    from test_host import run_abi_null_probe
+    run_abi_null_probe()

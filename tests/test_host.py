@@ -270,3 +270,32 @@ def test_header_is_plain_c(tmp_path):
     assert r.returncode == 0, r.stderr
     run = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert run.returncode in (0, 2), run.stdout + run.stderr  # 2: no GPU in this container
+
+
+ABI_NULL_PROBE = r'''
+import ctypes as C
+from paper_2604_14650_b200._lib import SIGNATURES, lib
+L = lib()
+bad = []
+for name, (res, args) in SIGNATURES.items():
+    if res is not C.c_int:
+        continue
+    vals = [0 if a in (C.c_int, C.c_uint32, C.c_uint64) else None for a in args]
+    st = getattr(L, name)(*vals)
+    if st not in (0, 1, 2, 3, 6, 9, 10, 11, 12, 13, 14):
+        bad.append((name, st))
+print("ABI-OK" if not bad else bad)
+'''
+
+
+def run_abi_null_probe():
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, "-c", ABI_NULL_PROBE], cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ABI-OK" in r.stdout, (r.returncode, r.stdout[-2000:], r.stderr[-2000:])
+
+
+def test_abi_rejects_null_arguments():
+    """Every int-returning ABI entry point called with NULL / zero arguments returns
+    a status (never crashes): run in a subprocess so a segfault fails the test."""
+    run_abi_null_probe()
