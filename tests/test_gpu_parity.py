@@ -417,3 +417,42 @@ def test_abi_rejects_null_arguments_on_gpu(cuda):
     (calls get past the device checks here)."""
     from test_host import run_abi_null_probe
     run_abi_null_probe()
+
+
+def test_abi_valid_handles_null_buffers(lpm, cuda):
+    """Valid FIB / store handles with NULL buffers and n > 0: every call returns a
+    status, nothing crashes (subprocess)."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    code = r'''
+import ctypes as C
+import paper_2604_14650_b200 as lpm
+from paper_2604_14650_b200._lib import SIGNATURES, lib
+L = lib()
+fib = lpm.Fib.build(lpm.workload_fib(0))
+store = lpm.FibStore(lpm.workload_fib(0))
+snap = C.c_void_p()
+assert L.lpm6cu_store_acquire(store._h, C.byref(snap)) == 0
+handles = {"fib": fib._h, "store": store._h, "snapshot": snap}
+firsts = {"lpm6cu_fib_": "fib", "lpm6cu_lookup_": "fib", "lpm6cu_search_batch": "fib", "lpm6cu_store_": "store",
+          "lpm6cu_snapshot_": "snapshot"}
+bad = []
+for name, (res, args) in SIGNATURES.items():
+    if res is not C.c_int or name in ("lpm6cu_store_destroy", "lpm6cu_store_release", "lpm6cu_fib_destroy"):
+        continue
+    kind = next((v for k, v in firsts.items() if name.startswith(k)), None)
+    if kind is None or name in ("lpm6cu_fib_build", "lpm6cu_fib_build_device", "lpm6cu_fib_create",
+                                "lpm6cu_fib_wrap_device", "lpm6cu_fib_adopt_device", "lpm6cu_fib_load_snapshot",
+                                "lpm6cu_fib_build_from_intervals", "lpm6cu_store_create"):
+        continue
+    vals = [handles[kind]] + [5 if a in (C.c_int, C.c_uint32, C.c_uint64) else None for a in args[1:]]
+    st = getattr(L, name)(*vals)
+    if st not in (0, 9, 13):
+        bad.append((name, st))
+L.lpm6cu_store_release(snap, None)
+print("ABI-OK" if not bad else bad)
+'''
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ABI-OK" in r.stdout, (r.returncode, r.stdout[-2000:], r.stderr[-3000:])
