@@ -619,7 +619,7 @@ def main():
     if args.sweep and rank == 0:
         sweep = []
         shapes = [(1, 256, 0), (1, 256, 4), (2, 256, 0), (1, 512, 2), (1, 1024, 1)]
-        for t_lv in range(max(0, geom.depth - 2), geom.depth + 1):
+        for t_lv in range(max(0, geom.depth - 2), geom.depth + 1 + geom.leaf_image):
             for qpl, thr, minb in shapes:
                 try:
                     fdev.set_kernel_config(smem_levels=t_lv, queries_per_lane=qpl, threads_per_cta=thr,
