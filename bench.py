@@ -703,6 +703,7 @@ def main():
         "fib_build_device_ms": device_build_ms(lpm, fib, dev_index, vb),
         "fib_broadcast_ms": bcast_ms,
         "step_ms": step_ms,
+        "ms_per_step_median": float(np.median(step_ms)),
     }
     if sweep is not None:
         line["sweep"] = sweep
