@@ -68,6 +68,15 @@ def dist_env():
     return ws, rank, local
 
 
+def shared_gpu_mode():
+    """LPM6_BENCH_SHARED_GPU=1: a harness check of the torchrun path on a box with fewer
+    GPUs than ranks — ranks share devices (local rank mod device count) and the
+    collectives run over gloo (NCCL refuses two ranks on one GPU). The ranks' kernels
+    never wait on one another (lookups shard with no exchange), but they contend for
+    the same SMs, so the numbers of such a run are not bench values; the line says so."""
+    return os.environ.get("LPM6_BENCH_SHARED_GPU", "") not in ("", "0")
+
+
 def init_dist(ws, local, backend="nccl"):
     import torch
     import torch.distributed as dist
@@ -484,6 +493,8 @@ def run_chunked(args, lpm, dispatch, fdev, fib, info, geom, cfg, ws, rank, dev_i
         "fib_build_ms": build_ms, "fib_build_device_ms": device_build_ms(lpm, fib, dev_index, vb),
         "fib_broadcast_ms": bcast_ms, "step_ms": step_ms,
     }
+    if ws > 1 and shared_gpu_mode():
+        line["harness_check"] = "LPM6_BENCH_SHARED_GPU: ranks shared GPUs over gloo; not a bench value"
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
@@ -499,7 +510,10 @@ def main():
 
     import torch
     ws, rank, local = dist_env()
-    dist = init_dist(ws, local)
+    shared = ws > 1 and shared_gpu_mode()
+    if shared:
+        local = local % torch.cuda.device_count()
+    dist = init_dist(ws, local, "gloo" if shared else "nccl")
     torch.cuda.set_device(local)
     dev_index = local
     import paper_2604_14650_b200 as lpm
@@ -709,6 +723,8 @@ def main():
         line["sweep"] = sweep
     if extras is not None:
         line["extras"] = extras
+    if ws > 1 and shared_gpu_mode():
+        line["harness_check"] = "LPM6_BENCH_SHARED_GPU: ranks shared GPUs over gloo; not a bench value"
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
