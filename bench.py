@@ -581,6 +581,11 @@ def main():
     torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(dev_index) as clk:
+        if use_graph:
+            # Launch-bound steps (~12 us): hold the stream in an untimed device sleep
+            # while the host enqueues all K replays, so host submission gaps never
+            # land between the timing events (the sleep itself is before ev[0]).
+            torch.cuda._sleep(int(2e6 + 2e5 * args.steps))
         ev[0].record(stream)
         for i in range(args.steps):
             step()
