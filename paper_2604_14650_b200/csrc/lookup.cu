@@ -181,6 +181,7 @@ void resolve_config(lpm6cu_fib* f, const lpm6cu_kernel_config* req) {
     }
     c.smem_levels = t;
   }
+  if (c.leaf_path > 1) throw Error(Errc::InvalidArgument, "leaf_path must be 0 (LSU) or 1 (texture)");
   if (c.smem_levels > tmax) c.smem_levels = tmax;
   const unsigned long long staged = image_bytes_of(f->g, c.smem_levels);
   if (staged > budget)
@@ -212,6 +213,8 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
   const unsigned smem_levels = leaf_image_mode(f) && !leafs ? f->g.depth : f->cfg.smem_levels;
   const bool texl = f->tex && !leafs && input != kInKeyOrd && f->d_err == nullptr && smem_levels < f->g.depth &&
                     tiles == 1 && threads_cta == 1024 && minb == 1 && f->g.depth >= 2;
+  const bool leaftex = f->cfg.leaf_path == 1 && f->tex && !leafs && (input == kInAddr || input == kInKey) &&
+                       f->d_err == nullptr && tiles == 1 && threads_cta == 1024 && minb == 1 && f->g.depth >= 1;
   const size_t smem = image_bytes_of(f->g, smem_levels);
   const int threads = static_cast<int>(threads_cta);
   LaunchPlan plan;
@@ -222,7 +225,7 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
     if (!slot.valid) {
       KernelFn fn = pick_kernel(static_cast<int>(f->g.value_bytes), static_cast<int>(f->g.depth),
                                 static_cast<int>(tiles), threads, static_cast<int>(minb), f->d_err != nullptr, input,
-                                leafs, texl);
+                                leafs, texl, leaftex);
       if (!fn) throw Error(Errc::InvalidArgument, "no kernel instantiated for this configuration");
       if (smem > 48 * 1024)
         check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
@@ -488,6 +491,61 @@ int lpm6cu_fib_kernel_config(const lpm6cu_fib* f, lpm6cu_kernel_config* cfg) {
   return guard([&] {
     if (!f || !cfg) throw Error(Errc::InvalidArgument, "NULL argument");
     *cfg = f->cfg;
+  });
+}
+
+int lpm6cu_fib_tune_leaf_path(lpm6cu_fib* f, const void* d_addrs, uint64_t n, void* d_out, void* stream,
+                              uint32_t reps, uint32_t* leaf_path) {
+  return guard([&] {
+    if (!f || !d_addrs || !d_out) throw Error(Errc::InvalidArgument, "NULL argument");
+    if (n == 0) throw Error(Errc::InvalidArgument, "empty tuning batch");
+    DeviceGuard dg(f->device);
+    if (!is_device_ptr(d_addrs) || !is_device_ptr(d_out))
+      throw Error(Errc::InvalidArgument, "lpm6cu_fib_tune_leaf_path takes device buffers");
+    if (reinterpret_cast<uintptr_t>(d_addrs) % 16 != 0)
+      throw Error(Errc::InvalidArgument, "addresses must be 16-byte aligned");
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    lpm6cu_kernel_config c = f->cfg;
+    const bool possible = f->tex && f->d_err == nullptr && !leaf_image_mode(f) && f->g.depth >= 1 &&
+                          c.queries_per_lane == 1 && c.threads_per_cta == 1024 && c.min_ctas_per_sm == 1;
+    unsigned best = 0;
+    if (possible) {
+      cudaEvent_t ev[2];
+      check_cuda(cudaEventCreate(&ev[0]), "cudaEventCreate");
+      if (cudaEventCreate(&ev[1]) != cudaSuccess) {
+        cudaEventDestroy(ev[0]);
+        throw Error(Errc::CudaError, "cudaEventCreate");
+      }
+      float ms[2] = {0.f, 0.f};
+      try {
+        const unsigned r = reps ? reps : 3;
+        for (unsigned path = 0; path < 2; ++path) {
+          c.leaf_path = path;
+          f->cfg = c;
+          f->invalidate_plans();
+          launch_lookup(f, d_addrs, n, d_out, st);  // untimed: resolves the plan, warms L2
+          check_cuda(cudaEventRecord(ev[0], st), "cudaEventRecord");
+          for (unsigned i = 0; i < r; ++i) launch_lookup(f, d_addrs, n, d_out, st);
+          check_cuda(cudaEventRecord(ev[1], st), "cudaEventRecord");
+          check_cuda(cudaEventSynchronize(ev[1]), "cudaEventSynchronize");
+          check_cuda(cudaEventElapsedTime(&ms[path], ev[0], ev[1]), "cudaEventElapsedTime");
+        }
+      } catch (...) {
+        cudaEventDestroy(ev[0]);
+        cudaEventDestroy(ev[1]);
+        c.leaf_path = 0;
+        f->cfg = c;
+        f->invalidate_plans();
+        throw;
+      }
+      cudaEventDestroy(ev[0]);
+      cudaEventDestroy(ev[1]);
+      best = ms[1] < ms[0] ? 1u : 0u;
+    }
+    c.leaf_path = best;
+    f->cfg = c;
+    f->invalidate_plans();
+    if (leaf_path) *leaf_path = best;
   });
 }
 

@@ -333,8 +333,12 @@ __device__ __forceinline__ unsigned leaf_search_smem(const unsigned long long* l
 // is staged in shared memory and each thread finishes its own query there — no
 // L2 line loads and no cross-lane traffic.
 // TEXL: the internal L2 levels are read through the texture pipe (p.tex).
+// LEAFTEX: the leaf lines too. Texture hits return off the LSU data pipe, which
+// pays when leaf lines hit L1 often (skewed traffic: C3b +9 %); on L1-missing
+// traffic the texture path's miss throughput is lower (C1 -27 %), so the host
+// picks it only by measurement (lpm6cu_fib_tune_leaf_path).
 template <int DEPTH, int VB, int TILES, int THREADS, int MINB, bool CHECKED, int INPUT = kInAddr, bool LEAFS = false,
-          bool TEXL = false>
+          bool TEXL = false, bool LEAFTEX = false>
 __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const LookupParams p) {
   using F = LeafFmt<VB>;
   unsigned violations = 0;
@@ -514,7 +518,12 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
           }
       }
 #pragma unroll
-      for (int s = 0; s < NS; ++s) ld_line_quarter(p.lines + (base_w + nd[s] * 16u), w[s]);
+      for (int s = 0; s < NS; ++s) {
+        if (LEAFTEX)
+          tex_line_quarter(p.tex, (base_w + nd[s] * 16u) >> 1, w[s]);
+        else
+          ld_line_quarter(p.lines + (base_w + nd[s] * 16u), w[s]);
+      }
       if constexpr (INPUT == kInKeyOrd) {
 #pragma unroll
         for (int s = 0; s < NS; ++s) leafn[s] = nd[s];
@@ -566,27 +575,34 @@ using KernelFn = void (*)(const LookupParams);
 
 // Instantiated shapes: (queries per lane, min CTAs per SM) for every depth and
 // value width; the tuning grid below is measured by bench.py --sweep.
-template <int VB, int INPUT>
+template <int VB, int INPUT, bool TEXL, bool LEAFTEX>
 KernelFn pick_depth_texl(int depth) {
   switch (depth) {
-    case 2: return lpm6_lookup_kernel<2, VB, 1, 1024, 1, false, INPUT, false, true>;
-    case 3: return lpm6_lookup_kernel<3, VB, 1, 1024, 1, false, INPUT, false, true>;
-    case 4: return lpm6_lookup_kernel<4, VB, 1, 1024, 1, false, INPUT, false, true>;
-    case 5: return lpm6_lookup_kernel<5, VB, 1, 1024, 1, false, INPUT, false, true>;
-    case 6: return lpm6_lookup_kernel<6, VB, 1, 1024, 1, false, INPUT, false, true>;
-    case 7: return lpm6_lookup_kernel<7, VB, 1, 1024, 1, false, INPUT, false, true>;
+    case 1: return lpm6_lookup_kernel<1, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX>;
+    case 2: return lpm6_lookup_kernel<2, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX>;
+    case 3: return lpm6_lookup_kernel<3, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX>;
+    case 4: return lpm6_lookup_kernel<4, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX>;
+    case 5: return lpm6_lookup_kernel<5, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX>;
+    case 6: return lpm6_lookup_kernel<6, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX>;
+    case 7: return lpm6_lookup_kernel<7, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX>;
     default: return nullptr;
   }
 }
 
-template <int INPUT>
+template <int INPUT, bool TEXL = true, bool LEAFTEX = false>
 KernelFn pick_vb_texl(int vb, int depth) {
   switch (vb) {
-    case 1: return pick_depth_texl<1, INPUT>(depth);
-    case 2: return pick_depth_texl<2, INPUT>(depth);
-    case 4: return pick_depth_texl<4, INPUT>(depth);
+    case 1: return pick_depth_texl<1, INPUT, TEXL, LEAFTEX>(depth);
+    case 2: return pick_depth_texl<2, INPUT, TEXL, LEAFTEX>(depth);
+    case 4: return pick_depth_texl<4, INPUT, TEXL, LEAFTEX>(depth);
     default: return nullptr;
   }
+}
+
+// Leaf lines through the texture pipe (default shape, unchecked, address / key input).
+template <int INPUT>
+KernelFn pick_leaftex(int vb, int depth, bool texl) {
+  return texl ? pick_vb_texl<INPUT, true, true>(vb, depth) : pick_vb_texl<INPUT, false, true>(vb, depth);
 }
 
 template <int VB, bool CHECKED>
@@ -628,7 +644,15 @@ KernelFn pick_vb(int vb, int depth) {
 // Instantiated shapes (queries per lane, threads per CTA, min CTAs per SM);
 // bench.py --sweep measures them. The checked variant exists for the default shape.
 KernelFn pick_kernel(int vb, int depth, int tiles, int threads, int minb, bool checked = false,
-                     int input = kInAddr, bool leafs = false, bool texl = false) {
+                     int input = kInAddr, bool leafs = false, bool texl = false, bool leaftex = false) {
+  if (leaftex) {  // default shape, unchecked, no leaf image, depth >= 1
+    if (leafs || checked || tiles != 1 || threads != 1024 || minb != 1) return nullptr;
+    switch (input) {
+      case kInAddr: return pick_leaftex<kInAddr>(vb, depth, texl);
+      case kInKey: return pick_leaftex<kInKey>(vb, depth, texl);
+      default: return nullptr;
+    }
+  }
   if (texl) {  // internal L2 levels via the texture pipe: default shape, unchecked
     if (leafs || checked || tiles != 1 || threads != 1024 || minb != 1) return nullptr;
     switch (input) {

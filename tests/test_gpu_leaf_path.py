@@ -1,0 +1,92 @@
+"""Leaf lines through the texture pipe (lpm6cu_kernel_config.leaf_path = 1) and the
+measured choice between the two leaf paths (lpm6cu_fib_tune_leaf_path).
+
+The texture path changes only how a leaf line reaches registers, so every answer
+must equal the LSU path's and the oracle's; the tuner must leave the kernel
+config on one of the two paths and never change results."""
+import numpy as np
+import pytest
+
+from _util import addrs_from_keys, boundary_probe_keys
+
+pytestmark = pytest.mark.gpu
+
+VIEW = {1: np.uint8, 2: np.uint16, 4: np.uint32}
+
+
+@pytest.mark.parametrize("workload", ["C1", "C2", "C3b"])
+def test_texture_leaf_path_matches_oracle_on_workloads(lpm, orc, cuda, workload):
+    """2^22 queries of each workload plus every boundary ±1, both leaf paths, address
+    and key input: bit-exact against the oracle."""
+    torch = cuda
+    info = lpm.workload_info(workload)
+    fib = lpm.workload_fib(info.fib_kind)
+    imap = lpm.build_intervals(fib)
+    dev = lpm.Fib.build(fib)
+    gen = lpm.QueryGen(workload, fib)
+    n = 1 << 22
+    d = torch.empty((n, 16), dtype=torch.uint8, device="cuda")
+    gen.run(0, n, d)
+    torch.cuda.synchronize()
+    host = d.cpu().numpy().view(np.uint64).reshape(-1, 2)
+    probes = addrs_from_keys(boundary_probe_keys(imap.boundaries), np.random.default_rng(7))
+    addrs = np.concatenate([host, probes])
+    want, _ = orc.lookup_batch(0, imap.boundaries, imap.next_hops, addrs, threads=8)
+    da = torch.from_numpy(addrs.view(np.uint8).reshape(-1, 16)).cuda()
+    dk = torch.from_numpy(np.ascontiguousarray(addrs[:, 1]).view(np.int64)).cuda()
+    view = VIEW[dev.geometry.value_bytes]
+    for lp in (1, 0):
+        cfg = dev.set_kernel_config(leaf_path=lp)
+        assert cfg["leaf_path"] == lp
+        got = dev.lookup_batch(da)
+        gk = dev.lookup_keys(dk)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(got.cpu().numpy().view(view).astype(np.uint32), want, err_msg=f"lp={lp}")
+        np.testing.assert_array_equal(gk.cpu().numpy().view(view).astype(np.uint32), want, err_msg=f"keys lp={lp}")
+
+
+def test_tuner_picks_a_path_and_keeps_results(lpm, orc, cuda):
+    torch = cuda
+    for workload in ("C1", "C3b"):
+        info = lpm.workload_info(workload)
+        fib = lpm.workload_fib(info.fib_kind)
+        dev = lpm.Fib.build(fib)
+        gen = lpm.QueryGen(workload, fib)
+        n = 1 << 24
+        d = torch.empty((n, 16), dtype=torch.uint8, device="cuda")
+        gen.run(0, n, d)
+        base = dev.lookup_batch(d).clone()
+        chosen = dev.tune_leaf_path(d)
+        assert chosen in (0, 1)
+        assert dev.kernel_config()["leaf_path"] == chosen
+        again = dev.lookup_batch(d)
+        torch.cuda.synchronize()
+        assert torch.equal(base, again)
+
+
+def test_tuner_on_checked_and_leaf_image_fibs_stays_on_lsu(lpm, cuda):
+    """No texture leaf kernel exists for checked mode or the shared-memory leaf image:
+    the tuner reports the LSU path, and lookups keep working."""
+    torch = cuda
+    fib = lpm.workload_fib(lpm.workload_info("C0").fib_kind)  # leaf-image tree
+    dev = lpm.Fib.build(fib)
+    a = torch.zeros((4096, 16), dtype=torch.uint8, device="cuda")
+    assert dev.tune_leaf_path(a) == 0
+    big = lpm.Fib.build(lpm.workload_fib(1))
+    big.set_checked(True)
+    assert big.tune_leaf_path(a) == 0
+    big.lookup_batch(a)
+    torch.cuda.synchronize()
+    assert big.violations() == 0
+    big.set_checked(False)
+
+
+def test_leaf_path_argument_errors(lpm, cuda):
+    torch = cuda
+    dev = lpm.Fib.build(lpm.workload_fib(1))
+    with pytest.raises(lpm.Lpm6Error):
+        dev.set_kernel_config(leaf_path=2)
+    with pytest.raises(lpm.Lpm6Error):
+        dev.tune_leaf_path(np.zeros((16, 16), np.uint8))  # host buffers
+    with pytest.raises(lpm.Lpm6Error):
+        dev.tune_leaf_path(torch.zeros((0, 16), dtype=torch.uint8, device="cuda"))

@@ -1,8 +1,8 @@
 """Randomised parity stress: random FIBs (0–60,000 rules, nesting, minimum
 lengths, default route on/off, merge on/off, 1/2/4-byte next hops, host or
 device build) through every kernel mode the FIB admits — every shared-memory
-split incl. the leaf image, checked and unchecked, address / key / search_batch
-inputs — against the CPU oracle on every boundary ±1 and random keys."""
+split incl. the leaf image, both leaf paths, checked and unchecked, address / key /
+search_batch inputs — against the CPU oracle on every boundary ±1 and random keys."""
 import numpy as np
 import pytest
 
@@ -35,15 +35,16 @@ def test_random_fibs_every_mode(lpm, orc, cuda):
         dk = torch.from_numpy(keys.view(np.int64)).cuda()
         view = {1: np.uint8, 2: np.uint16, 4: np.uint32}[g.value_bytes]
         for t in [None] + list(range(g.depth + g.leaf_image + 1)):
-            dev.set_kernel_config(smem_levels=t)
-            for checked in (False, True):
-                dev.set_checked(checked)
-                for mode, got in (("addr", dev.lookup_batch(da)), ("keys", dev.lookup_keys(dk)),
-                                  ("search", dev.search_batch(dk)[1])):
-                    torch.cuda.synchronize()
-                    if not np.array_equal(got.cpu().numpy().view(view).astype(np.uint32), want):
-                        failures.append((it, n, t, checked, mode, g.depth, g.value_bytes))
-                if checked and dev.violations():
-                    failures.append((it, "violations"))
+            for lp in (0, 1):  # leaf lines through the LSU / the texture pipe
+                dev.set_kernel_config(smem_levels=t, leaf_path=lp)
+                for checked in (False, True):
+                    dev.set_checked(checked)
+                    for mode, got in (("addr", dev.lookup_batch(da)), ("keys", dev.lookup_keys(dk)),
+                                      ("search", dev.search_batch(dk)[1])):
+                        torch.cuda.synchronize()
+                        if not np.array_equal(got.cpu().numpy().view(view).astype(np.uint32), want):
+                            failures.append((it, n, t, lp, checked, mode, g.depth, g.value_bytes))
+                    if checked and dev.violations():
+                        failures.append((it, "violations"))
         dev.set_checked(False)
     assert not failures, failures[:10]
