@@ -363,9 +363,12 @@ void lookup_host(lpm6cu_fib* f, const void* addrs, unsigned long long n, void* o
     check_cuda(cudaStreamWaitEvent(pp.streams[i], pp.start, 0), "stream wait");
   const auto* src = static_cast<const unsigned char*>(addrs);
   auto* dst = static_cast<unsigned char*>(out);
+  // Small batches are cut into ~6 pieces (>= 64K queries) so their copies overlap too.
+  const unsigned long long step =
+      std::min(pp.chunk, (std::max<unsigned long long>(1ull << 16, (n + 5) / 6) + 63) & ~63ull);
   int s = 0;
-  for (unsigned long long off = 0; off < n; off += pp.chunk, s = (s + 1) % HostPipeline::kStreams) {
-    const unsigned long long m = std::min(pp.chunk, n - off);
+  for (unsigned long long off = 0; off < n; off += step, s = (s + 1) % HostPipeline::kStreams) {
+    const unsigned long long m = std::min(step, n - off);
     check_cuda(cudaMemcpyAsync(pp.d_in[s], src + off * in_bytes, m * in_bytes, cudaMemcpyHostToDevice, pp.streams[s]),
                "H2D");
     launch_lookup(f, pp.d_in[s], m, pp.d_out[s], pp.streams[s], input);
