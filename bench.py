@@ -53,8 +53,8 @@ def parse_args():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also time every kernel shape (extra key)")
     ap.add_argument("--no-extras", action="store_true", help="skip the key/packet-input and store timings")
-    ap.add_argument("--leaf-path", choices=["tune", "lsu", "tex"], default="tune",
-                    help="leaf lines through the LSU or the texture pipe; tune = time both on the step's "
+    ap.add_argument("--leaf-path", choices=["tune", "lsu", "tex", "split"], default="tune",
+                    help="leaf lines through the LSU, the texture pipe or half each (split); tune = time all on the step's "
                          "batch before the warm-up (lpm6cu_fib_tune_leaf_path) and keep the faster")
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
                     help="replay each step's launch from a CUDA graph (auto: batches under 2^24 queries, "
@@ -428,7 +428,7 @@ def choose_leaf_path(args, fdev, addrs, out, stream):
         fdev.set_kernel_config(lanes_per_query=c["lanes_per_query"], smem_levels=c["smem_levels"],
                                ctas_per_sm=c["ctas_per_sm"], threads_per_cta=c["threads_per_cta"],
                                queries_per_lane=c["queries_per_lane"], min_ctas_per_sm=c["min_ctas_per_sm"],
-                               leaf_path=1 if args.leaf_path == "tex" else 0)
+                               leaf_path={"lsu": 0, "tex": 1, "split": 2}[args.leaf_path])
     cfg = fdev.kernel_config()
     cfg["leaf_path_choice"] = args.leaf_path
     return cfg

@@ -181,7 +181,7 @@ void resolve_config(lpm6cu_fib* f, const lpm6cu_kernel_config* req) {
     }
     c.smem_levels = t;
   }
-  if (c.leaf_path > 1) throw Error(Errc::InvalidArgument, "leaf_path must be 0 (LSU) or 1 (texture)");
+  if (c.leaf_path > 2) throw Error(Errc::InvalidArgument, "leaf_path must be 0 (LSU), 1 (texture) or 2 (split)");
   if (c.smem_levels > tmax) c.smem_levels = tmax;
   const unsigned long long staged = image_bytes_of(f->g, c.smem_levels);
   if (staged > budget)
@@ -213,8 +213,10 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
   const unsigned smem_levels = leaf_image_mode(f) && !leafs ? f->g.depth : f->cfg.smem_levels;
   const bool texl = f->tex && !leafs && input != kInKeyOrd && f->d_err == nullptr && smem_levels < f->g.depth &&
                     tiles == 1 && threads_cta == 1024 && minb == 1 && f->g.depth >= 2;
-  const bool leaftex = f->cfg.leaf_path == 1 && f->tex && !leafs && (input == kInAddr || input == kInKey) &&
-                       f->d_err == nullptr && tiles == 1 && threads_cta == 1024 && minb == 1 && f->g.depth >= 1;
+  const int leaftex = f->cfg.leaf_path != 0 && f->tex && !leafs && (input == kInAddr || input == kInKey) &&
+                              f->d_err == nullptr && tiles == 1 && threads_cta == 1024 && minb == 1 && f->g.depth >= 1
+                          ? static_cast<int>(f->cfg.leaf_path)
+                          : 0;
   const size_t smem = image_bytes_of(f->g, smem_levels);
   const int threads = static_cast<int>(threads_cta);
   LaunchPlan plan;
@@ -519,10 +521,10 @@ int lpm6cu_fib_tune_leaf_path(lpm6cu_fib* f, const void* d_addrs, uint64_t n, vo
         cudaEventDestroy(ev[0]);
         throw Error(Errc::CudaError, "cudaEventCreate");
       }
-      float ms[2] = {0.f, 0.f};
+      float ms[3] = {0.f, 0.f, 0.f};
       try {
         const unsigned r = reps ? reps : 3;
-        for (unsigned path = 0; path < 2; ++path) {
+        for (unsigned path = 0; path < 3; ++path) {
           c.leaf_path = path;
           f->cfg = c;
           f->invalidate_plans();
@@ -543,7 +545,8 @@ int lpm6cu_fib_tune_leaf_path(lpm6cu_fib* f, const void* d_addrs, uint64_t n, vo
       }
       cudaEventDestroy(ev[0]);
       cudaEventDestroy(ev[1]);
-      best = ms[1] < ms[0] ? 1u : 0u;
+      for (unsigned path = 1; path < 3; ++path)
+        if (ms[path] < ms[best]) best = path;
     }
     c.leaf_path = best;
     f->cfg = c;

@@ -333,12 +333,14 @@ __device__ __forceinline__ unsigned leaf_search_smem(const unsigned long long* l
 // is staged in shared memory and each thread finishes its own query there — no
 // L2 line loads and no cross-lane traffic.
 // TEXL: the internal L2 levels are read through the texture pipe (p.tex).
-// LEAFTEX: the leaf lines too. Texture hits return off the LSU data pipe, which
-// pays when leaf lines hit L1 often (skewed traffic: C3b +9 %); on L1-missing
-// traffic the texture path's miss throughput is lower (C1 -27 %), so the host
-// picks it only by measurement (lpm6cu_fib_tune_leaf_path).
+// LEAFTEX: the leaf lines too — 1: every leaf line, 2: half of each group's
+// slots (a compile-time split, so both L1TEX pipes work in every warp).
+// Texture hits return off the LSU data pipe, which pays when leaf lines hit L1
+// often (skewed traffic: C3b +9 % with 1); on L1-missing traffic the texture
+// path's miss throughput is lower (C1 -27 % with 1, +1.2 % with 2), so the host
+// picks the mode by measurement (lpm6cu_fib_tune_leaf_path).
 template <int DEPTH, int VB, int TILES, int THREADS, int MINB, bool CHECKED, int INPUT = kInAddr, bool LEAFS = false,
-          bool TEXL = false, bool LEAFTEX = false>
+          bool TEXL = false, int LEAFTEX = 0>
 __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const LookupParams p) {
   using F = LeafFmt<VB>;
   unsigned violations = 0;
@@ -519,7 +521,9 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
       }
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
-        if (LEAFTEX)
+        // LEAFTEX 1: every slot through the texture pipe; 2: the upper half of the
+        // group's slots (compile-time split, both pipes busy in one warp).
+        if (LEAFTEX == 1 || (LEAFTEX == 2 && s >= NS / 2))
           tex_line_quarter(p.tex, (base_w + nd[s] * 16u) >> 1, w[s]);
         else
           ld_line_quarter(p.lines + (base_w + nd[s] * 16u), w[s]);
@@ -575,7 +579,7 @@ using KernelFn = void (*)(const LookupParams);
 
 // Instantiated shapes: (queries per lane, min CTAs per SM) for every depth and
 // value width; the tuning grid below is measured by bench.py --sweep.
-template <int VB, int INPUT, bool TEXL, bool LEAFTEX>
+template <int VB, int INPUT, bool TEXL, int LEAFTEX>
 KernelFn pick_depth_texl(int depth) {
   switch (depth) {
     case 1: return lpm6_lookup_kernel<1, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX>;
@@ -589,7 +593,7 @@ KernelFn pick_depth_texl(int depth) {
   }
 }
 
-template <int INPUT, bool TEXL = true, bool LEAFTEX = false>
+template <int INPUT, bool TEXL = true, int LEAFTEX = 0>
 KernelFn pick_vb_texl(int vb, int depth) {
   switch (vb) {
     case 1: return pick_depth_texl<1, INPUT, TEXL, LEAFTEX>(depth);
@@ -601,8 +605,10 @@ KernelFn pick_vb_texl(int vb, int depth) {
 
 // Leaf lines through the texture pipe (default shape, unchecked, address / key input).
 template <int INPUT>
-KernelFn pick_leaftex(int vb, int depth, bool texl) {
-  return texl ? pick_vb_texl<INPUT, true, true>(vb, depth) : pick_vb_texl<INPUT, false, true>(vb, depth);
+KernelFn pick_leaftex(int vb, int depth, bool texl, int mode) {
+  if (mode == 2)
+    return texl ? pick_vb_texl<INPUT, true, 2>(vb, depth) : pick_vb_texl<INPUT, false, 2>(vb, depth);
+  return texl ? pick_vb_texl<INPUT, true, 1>(vb, depth) : pick_vb_texl<INPUT, false, 1>(vb, depth);
 }
 
 template <int VB, bool CHECKED>
@@ -644,12 +650,12 @@ KernelFn pick_vb(int vb, int depth) {
 // Instantiated shapes (queries per lane, threads per CTA, min CTAs per SM);
 // bench.py --sweep measures them. The checked variant exists for the default shape.
 KernelFn pick_kernel(int vb, int depth, int tiles, int threads, int minb, bool checked = false,
-                     int input = kInAddr, bool leafs = false, bool texl = false, bool leaftex = false) {
+                     int input = kInAddr, bool leafs = false, bool texl = false, int leaftex = 0) {
   if (leaftex) {  // default shape, unchecked, no leaf image, depth >= 1
     if (leafs || checked || tiles != 1 || threads != 1024 || minb != 1) return nullptr;
     switch (input) {
-      case kInAddr: return pick_leaftex<kInAddr>(vb, depth, texl);
-      case kInKey: return pick_leaftex<kInKey>(vb, depth, texl);
+      case kInAddr: return pick_leaftex<kInAddr>(vb, depth, texl, leaftex);
+      case kInKey: return pick_leaftex<kInKey>(vb, depth, texl, leaftex);
       default: return nullptr;
     }
   }

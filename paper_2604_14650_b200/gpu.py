@@ -177,8 +177,8 @@ class Fib:
         return self.kernel_config()
 
     def tune_leaf_path(self, addrs, out=None, stream=None, reps: int = 3) -> int:
-        """Time both leaf paths (LSU, texture) on a representative device batch and
-        keep the faster in the kernel config; returns 0 (LSU) or 1 (texture)."""
+        """Time the leaf paths (0 LSU, 1 texture, 2 split) on a representative device
+        batch and keep the fastest in the kernel config; returns its number."""
         vb = self.value_bytes
         aptr, n, adev = _ptr_len(addrs, 16)
         if not adev:

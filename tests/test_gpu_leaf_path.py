@@ -16,7 +16,7 @@ VIEW = {1: np.uint8, 2: np.uint16, 4: np.uint32}
 
 @pytest.mark.parametrize("workload", ["C1", "C2", "C3b"])
 def test_texture_leaf_path_matches_oracle_on_workloads(lpm, orc, cuda, workload):
-    """2^22 queries of each workload plus every boundary ±1, both leaf paths, address
+    """2^22 queries of each workload plus every boundary ±1, every leaf path, address
     and key input: bit-exact against the oracle."""
     torch = cuda
     info = lpm.workload_info(workload)
@@ -35,7 +35,7 @@ def test_texture_leaf_path_matches_oracle_on_workloads(lpm, orc, cuda, workload)
     da = torch.from_numpy(addrs.view(np.uint8).reshape(-1, 16)).cuda()
     dk = torch.from_numpy(np.ascontiguousarray(addrs[:, 1]).view(np.int64)).cuda()
     view = VIEW[dev.geometry.value_bytes]
-    for lp in (1, 0):
+    for lp in (1, 2, 0):
         cfg = dev.set_kernel_config(leaf_path=lp)
         assert cfg["leaf_path"] == lp
         got = dev.lookup_batch(da)
@@ -57,7 +57,7 @@ def test_tuner_picks_a_path_and_keeps_results(lpm, orc, cuda):
         gen.run(0, n, d)
         base = dev.lookup_batch(d).clone()
         chosen = dev.tune_leaf_path(d)
-        assert chosen in (0, 1)
+        assert chosen in (0, 1, 2)
         assert dev.kernel_config()["leaf_path"] == chosen
         again = dev.lookup_batch(d)
         torch.cuda.synchronize()
@@ -85,7 +85,7 @@ def test_leaf_path_argument_errors(lpm, cuda):
     torch = cuda
     dev = lpm.Fib.build(lpm.workload_fib(1))
     with pytest.raises(lpm.Lpm6Error):
-        dev.set_kernel_config(leaf_path=2)
+        dev.set_kernel_config(leaf_path=3)
     with pytest.raises(lpm.Lpm6Error):
         dev.tune_leaf_path(np.zeros((16, 16), np.uint8))  # host buffers
     with pytest.raises(lpm.Lpm6Error):
