@@ -53,9 +53,9 @@ def parse_args():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also time every kernel shape (extra key)")
     ap.add_argument("--no-extras", action="store_true", help="skip the key/packet-input and store timings")
-    ap.add_argument("--leaf-path", choices=["tune", "lsu", "tex", "split"], default="tune",
-                    help="leaf lines through the LSU, the texture pipe or half each (split); tune = time all on the step's "
-                         "batch before the warm-up (lpm6cu_fib_tune_leaf_path) and keep the faster")
+    ap.add_argument("--line-path", choices=["tune", "lsu", "tex", "split", "tex-split"], default="tune",
+                    help="L2 lines through the LSU or the texture pipe (lpm6cu_kernel_config.line_path 0-3); tune = time all on the step's "
+                         "batch before the warm-up (lpm6cu_fib_tune_line_path) and keep the faster")
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
                     help="replay each step's launch from a CUDA graph (auto: batches under 2^24 queries, "
                          "where the host launch path would otherwise bound the step)")
@@ -418,19 +418,19 @@ def run_reference(args):
     return 0
 
 
-def choose_leaf_path(args, fdev, addrs, out, stream):
-    """Leaf path for the timed steps: fixed by --leaf-path, or measured on this batch
+def choose_line_path(args, fdev, addrs, out, stream):
+    """Leaf path for the timed steps: fixed by --line-path, or measured on this batch
     (untimed, before the warm-up) by the library's tuner. Returns the kernel config."""
-    if args.leaf_path == "tune":
-        fdev.tune_leaf_path(addrs, out, stream)
+    if args.line_path == "tune":
+        fdev.tune_line_path(addrs, out, stream)
     else:
         c = fdev.kernel_config()
         fdev.set_kernel_config(lanes_per_query=c["lanes_per_query"], smem_levels=c["smem_levels"],
                                ctas_per_sm=c["ctas_per_sm"], threads_per_cta=c["threads_per_cta"],
                                queries_per_lane=c["queries_per_lane"], min_ctas_per_sm=c["min_ctas_per_sm"],
-                               leaf_path={"lsu": 0, "tex": 1, "split": 2}[args.leaf_path])
+                               line_path={"lsu": 0, "tex": 1, "split": 2, "tex-split": 3}[args.line_path])
     cfg = fdev.kernel_config()
-    cfg["leaf_path_choice"] = args.leaf_path
+    cfg["line_path_choice"] = args.line_path
     return cfg
 
 
@@ -455,7 +455,7 @@ def run_chunked(args, lpm, dispatch, fdev, fib, info, geom, cfg, ws, rank, dev_i
     hbm_gbs, hbm_src = hbm_peak()
 
     gen.run(c0 * chunk, chunk, addrs, stream)
-    cfg = choose_leaf_path(args, fdev, addrs, out, stream)
+    cfg = choose_line_path(args, fdev, addrs, out, stream)
 
     def one_pass():
         evs = []
@@ -582,7 +582,7 @@ def main():
 
     stream = torch.cuda.current_stream()
 
-    cfg = choose_leaf_path(args, fdev, addrs, out, stream)
+    cfg = choose_line_path(args, fdev, addrs, out, stream)
 
     def launch(s=stream):
         fdev.lookup_batch(addrs, out, s)
@@ -683,7 +683,7 @@ def main():
         fdev.set_kernel_config(lanes_per_query=args.lanes, smem_levels=args.smem_levels,
                                ctas_per_sm=args.ctas_per_sm, queries_per_lane=args.queries_per_lane,
                                min_ctas_per_sm=args.min_ctas, threads_per_cta=args.threads,
-                               leaf_path=cfg["leaf_path"])
+                               line_path=cfg["line_path"])
 
     # -- other inputs and the update store (rank 0; extra keys, not the headline) ---------------------
     extras = None

@@ -111,11 +111,14 @@ typedef struct {
   uint32_t queries_per_lane; /* 32-query tiles each warp carries at once: 1, or 2 at 256 threads */
   uint32_t min_ctas_per_sm;  /* register cap (__launch_bounds__ min blocks): 1 at 1024 threads,
                                 2 at 512, 0 or 4 at 256 */
-  uint32_t leaf_path;        /* how leaf lines reach the SM (address / key input, default shape,
-                                unchecked): 0 = LSU (default); 1 = texture pipe, faster when leaf
-                                lines often hit L1 (skewed traffic); 2 = half of each warp's leaf
-                                lines through each pipe. Pick it on representative traffic with
-                                lpm6cu_fib_tune_leaf_path. */
+  uint32_t line_path;        /* which L1TEX pipe carries the 128-byte L2 lines (address / key
+                                input, default shape, unchecked): 0 = leaves through the LSU,
+                                internal L2 levels through the texture pipe (default); 1 = leaves
+                                through the texture pipe too, faster when leaf lines often hit L1
+                                (skewed traffic); 2 = half of each warp's leaf lines through each
+                                pipe; 3 = as 1 with half of the internal-level lines through the
+                                LSU. Pick it on representative traffic with
+                                lpm6cu_fib_tune_line_path. */
 } lpm6cu_kernel_config;
 
 typedef struct lpm6cu_fib lpm6cu_fib;
@@ -186,13 +189,14 @@ int lpm6cu_fib_device_lines(const lpm6cu_fib* fib, const void** d_lines);
 int lpm6cu_fib_copy_lines(const lpm6cu_fib* fib, uint64_t* host_lines, uint64_t words);
 int lpm6cu_fib_set_kernel_config(lpm6cu_fib* fib, const lpm6cu_kernel_config* cfg);
 int lpm6cu_fib_kernel_config(const lpm6cu_fib* fib, lpm6cu_kernel_config* cfg);
-/* Times the three leaf paths on a representative batch (device buffers, `reps`
- * timed launches each after one untimed, on `stream`; synchronizes it), keeps the
- * fastest in the kernel config and returns it in *leaf_path (0 LSU, 1 texture,
- * 2 split). Results are identical on every path; like the other tuning calls it
- * must not race with lookups on the handle. */
-int lpm6cu_fib_tune_leaf_path(lpm6cu_fib* fib, const void* d_addrs, uint64_t n, void* d_out, void* stream,
-                              uint32_t reps, uint32_t* leaf_path);
+/* Times the line paths on a representative batch (device buffers, `reps` timed
+ * launches each after one untimed, on `stream`; synchronizes it), keeps the
+ * fastest in the kernel config and returns it in *line_path (0..3, see
+ * lpm6cu_kernel_config; 3 only when the tree has internal L2 levels). Results are
+ * identical on every path; like the other tuning calls it must not race with
+ * lookups on the handle. */
+int lpm6cu_fib_tune_line_path(lpm6cu_fib* fib, const void* d_addrs, uint64_t n, void* d_out, void* stream,
+                              uint32_t reps, uint32_t* line_path);
 void lpm6cu_fib_destroy(lpm6cu_fib* fib);
 
 /* Checked mode: lookups run a bounds-checked kernel that never reads outside the

@@ -135,11 +135,12 @@ class Fib {
     lpm6cu::check(lpm6cu_lookup_packets(h_, d_frames, n, stride, dst_offset, d_out, stream));
   }
 
-  // Times the leaf paths (LSU / texture pipe / split) on a representative device batch
-  // and keeps the fastest; returns 0, 1 or 2. Not concurrent with lookups.
-  uint32_t tune_leaf_path(const void* d_addrs, uint64_t n, void* d_out, void* stream = nullptr, uint32_t reps = 3) {
+  // Times the line paths (which L1TEX pipe carries the L2 lines, lpm6cu_kernel_config)
+  // on a representative device batch and keeps the fastest; returns 0..3. Not
+  // concurrent with lookups.
+  uint32_t tune_line_path(const void* d_addrs, uint64_t n, void* d_out, void* stream = nullptr, uint32_t reps = 3) {
     uint32_t chosen = 0;
-    lpm6cu::check(lpm6cu_fib_tune_leaf_path(h_, d_addrs, n, d_out, stream, reps, &chosen));
+    lpm6cu::check(lpm6cu_fib_tune_line_path(h_, d_addrs, n, d_out, stream, reps, &chosen));
     return chosen;
   }
 

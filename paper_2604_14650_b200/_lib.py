@@ -53,7 +53,7 @@ class BuildOpts_t(C.Structure):
 class KernelConfig_t(C.Structure):
     _fields_ = [("lanes_per_query", C.c_uint32), ("smem_levels", C.c_uint32), ("ctas_per_sm", C.c_uint32),
                 ("threads_per_cta", C.c_uint32), ("queries_per_lane", C.c_uint32), ("min_ctas_per_sm", C.c_uint32),
-                ("leaf_path", C.c_uint32)]
+                ("line_path", C.c_uint32)]
 
 
 class WorkloadInfo_t(C.Structure):
@@ -103,7 +103,7 @@ SIGNATURES = {
     "lpm6cu_fib_copy_lines": (I32, [P, P, U64]),
     "lpm6cu_fib_set_kernel_config": (I32, [P, C.POINTER(KernelConfig_t)]),
     "lpm6cu_fib_kernel_config": (I32, [P, C.POINTER(KernelConfig_t)]),
-    "lpm6cu_fib_tune_leaf_path": (I32, [P, P, U64, P, P, U32, C.POINTER(U32)]),
+    "lpm6cu_fib_tune_line_path": (I32, [P, P, U64, P, P, U32, C.POINTER(U32)]),
     "lpm6cu_fib_destroy": (None, [P]),
     "lpm6cu_fib_set_checked": (I32, [P, I32]),
     "lpm6cu_fib_violations": (I32, [P, C.POINTER(U32), I32]),

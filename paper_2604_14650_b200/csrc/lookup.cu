@@ -181,7 +181,7 @@ void resolve_config(lpm6cu_fib* f, const lpm6cu_kernel_config* req) {
     }
     c.smem_levels = t;
   }
-  if (c.leaf_path > 2) throw Error(Errc::InvalidArgument, "leaf_path must be 0 (LSU), 1 (texture) or 2 (split)");
+  if (c.line_path > 3) throw Error(Errc::InvalidArgument, "line_path must be 0, 1, 2 or 3");
   if (c.smem_levels > tmax) c.smem_levels = tmax;
   const unsigned long long staged = image_bytes_of(f->g, c.smem_levels);
   if (staged > budget)
@@ -213,10 +213,14 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
   const unsigned smem_levels = leaf_image_mode(f) && !leafs ? f->g.depth : f->cfg.smem_levels;
   const bool texl = f->tex && !leafs && input != kInKeyOrd && f->d_err == nullptr && smem_levels < f->g.depth &&
                     tiles == 1 && threads_cta == 1024 && minb == 1 && f->g.depth >= 2;
-  const int leaftex = f->cfg.leaf_path != 0 && f->tex && !leafs && (input == kInAddr || input == kInKey) &&
+  // Line path plan (lpm6cu_kernel_config.line_path): 0 LSU leaves, 1 texture leaves,
+  // 2 split leaves, 3 texture leaves + split internal L2 levels.
+  const int plan_lp = static_cast<int>(f->cfg.line_path);
+  const int leaftex = plan_lp != 0 && f->tex && !leafs && (input == kInAddr || input == kInKey) &&
                               f->d_err == nullptr && tiles == 1 && threads_cta == 1024 && minb == 1 && f->g.depth >= 1
-                          ? static_cast<int>(f->cfg.leaf_path)
+                          ? (plan_lp == 2 ? 2 : 1)
                           : 0;
+  const int texl_mode = !texl ? 0 : (plan_lp == 3 && leaftex == 1) ? 2 : 1;
   const size_t smem = image_bytes_of(f->g, smem_levels);
   const int threads = static_cast<int>(threads_cta);
   LaunchPlan plan;
@@ -227,7 +231,7 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
     if (!slot.valid) {
       KernelFn fn = pick_kernel(static_cast<int>(f->g.value_bytes), static_cast<int>(f->g.depth),
                                 static_cast<int>(tiles), threads, static_cast<int>(minb), f->d_err != nullptr, input,
-                                leafs, texl, leaftex);
+                                leafs, texl_mode, leaftex);
       if (!fn) throw Error(Errc::InvalidArgument, "no kernel instantiated for this configuration");
       if (smem > 48 * 1024)
         check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
@@ -499,14 +503,14 @@ int lpm6cu_fib_kernel_config(const lpm6cu_fib* f, lpm6cu_kernel_config* cfg) {
   });
 }
 
-int lpm6cu_fib_tune_leaf_path(lpm6cu_fib* f, const void* d_addrs, uint64_t n, void* d_out, void* stream,
-                              uint32_t reps, uint32_t* leaf_path) {
+int lpm6cu_fib_tune_line_path(lpm6cu_fib* f, const void* d_addrs, uint64_t n, void* d_out, void* stream,
+                              uint32_t reps, uint32_t* line_path) {
   return guard([&] {
     if (!f || !d_addrs || !d_out) throw Error(Errc::InvalidArgument, "NULL argument");
     if (n == 0) throw Error(Errc::InvalidArgument, "empty tuning batch");
     DeviceGuard dg(f->device);
     if (!is_device_ptr(d_addrs) || !is_device_ptr(d_out))
-      throw Error(Errc::InvalidArgument, "lpm6cu_fib_tune_leaf_path takes device buffers");
+      throw Error(Errc::InvalidArgument, "lpm6cu_fib_tune_line_path takes device buffers");
     if (reinterpret_cast<uintptr_t>(d_addrs) % 16 != 0)
       throw Error(Errc::InvalidArgument, "addresses must be 16-byte aligned");
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -521,11 +525,13 @@ int lpm6cu_fib_tune_leaf_path(lpm6cu_fib* f, const void* d_addrs, uint64_t n, vo
         cudaEventDestroy(ev[0]);
         throw Error(Errc::CudaError, "cudaEventCreate");
       }
-      float ms[3] = {0.f, 0.f, 0.f};
+      float ms[4] = {0.f, 0.f, 0.f, 0.f};
       try {
         const unsigned r = reps ? reps : 3;
-        for (unsigned path = 0; path < 3; ++path) {
-          c.leaf_path = path;
+        // Plan 3 differs from plan 1 only when the tree has internal L2 levels.
+        const unsigned plans = (f->g.depth > f->cfg.smem_levels) ? 4u : 3u;
+        for (unsigned path = 0; path < plans; ++path) {
+          c.line_path = path;
           f->cfg = c;
           f->invalidate_plans();
           launch_lookup(f, d_addrs, n, d_out, st);  // untimed: resolves the plan, warms L2
@@ -538,20 +544,21 @@ int lpm6cu_fib_tune_leaf_path(lpm6cu_fib* f, const void* d_addrs, uint64_t n, vo
       } catch (...) {
         cudaEventDestroy(ev[0]);
         cudaEventDestroy(ev[1]);
-        c.leaf_path = 0;
+        c.line_path = 0;
         f->cfg = c;
         f->invalidate_plans();
         throw;
       }
       cudaEventDestroy(ev[0]);
       cudaEventDestroy(ev[1]);
-      for (unsigned path = 1; path < 3; ++path)
+      const unsigned plans = (f->g.depth > f->cfg.smem_levels) ? 4u : 3u;
+      for (unsigned path = 1; path < plans; ++path)
         if (ms[path] < ms[best]) best = path;
     }
-    c.leaf_path = best;
+    c.line_path = best;
     f->cfg = c;
     f->invalidate_plans();
-    if (leaf_path) *leaf_path = best;
+    if (line_path) *line_path = best;
   });
 }
 

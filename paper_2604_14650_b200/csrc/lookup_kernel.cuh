@@ -332,15 +332,17 @@ __device__ __forceinline__ unsigned leaf_search_smem(const unsigned long long* l
 // LEAFS (small trees, layout.hpp leaf image): every level including the leaves
 // is staged in shared memory and each thread finishes its own query there — no
 // L2 line loads and no cross-lane traffic.
-// TEXL: the internal L2 levels are read through the texture pipe (p.tex).
-// LEAFTEX: the leaf lines too — 1: every leaf line, 2: half of each group's
-// slots (a compile-time split, so both L1TEX pipes work in every warp).
-// Texture hits return off the LSU data pipe, which pays when leaf lines hit L1
-// often (skewed traffic: C3b +9 % with 1); on L1-missing traffic the texture
-// path's miss throughput is lower (C1 -27 % with 1, +1.2 % with 2), so the host
-// picks the mode by measurement (lpm6cu_fib_tune_leaf_path).
+// TEXL: the internal L2 levels are read through the texture pipe (p.tex) — 1:
+// every line, 2: the lower half of each group's slots (the rest through the LSU).
+// LEAFTEX: the leaf lines too — 1: every leaf line, 2: the upper half of each
+// group's slots. The halves are compile-time splits, so both L1TEX pipes work
+// in every warp. Texture hits return off the LSU data pipe, which pays when
+// leaf lines hit L1 often (skewed traffic: C3b +9 % with 1); on L1-missing
+// traffic the texture path's miss throughput is lower (C1 -27 % with 1, +1.2 %
+// with 2), so the host picks the line path by measurement
+// (lpm6cu_fib_tune_line_path).
 template <int DEPTH, int VB, int TILES, int THREADS, int MINB, bool CHECKED, int INPUT = kInAddr, bool LEAFS = false,
-          bool TEXL = false, int LEAFTEX = 0>
+          int TEXL = 0, int LEAFTEX = 0>
 __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const LookupParams p) {
   using F = LeafFmt<VB>;
   unsigned violations = 0;
@@ -495,7 +497,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
         // the two pipes of L1TEX share the load, which helps the deep trees (C2:
         // +8 %); leaves through the texture pipe lose on L2-missing workloads
         // (C1 -17 %), so they stay on the LSU path.
-        if (TEXL)
+        if (TEXL == 1 || (TEXL == 2 && s < NS / 2))
           tex_line_quarter(p.tex, (base_w + nd[s] * 16u) >> 1, w[s]);
         else
           ld_line_quarter(p.lines + (base_w + nd[s] * 16u), w[s]);
@@ -579,7 +581,7 @@ using KernelFn = void (*)(const LookupParams);
 
 // Instantiated shapes: (queries per lane, min CTAs per SM) for every depth and
 // value width; the tuning grid below is measured by bench.py --sweep.
-template <int VB, int INPUT, bool TEXL, int LEAFTEX>
+template <int VB, int INPUT, int TEXL, int LEAFTEX>
 KernelFn pick_depth_texl(int depth) {
   switch (depth) {
     case 1: return lpm6_lookup_kernel<1, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX>;
@@ -593,7 +595,7 @@ KernelFn pick_depth_texl(int depth) {
   }
 }
 
-template <int INPUT, bool TEXL = true, int LEAFTEX = 0>
+template <int INPUT, int TEXL = 1, int LEAFTEX = 0>
 KernelFn pick_vb_texl(int vb, int depth) {
   switch (vb) {
     case 1: return pick_depth_texl<1, INPUT, TEXL, LEAFTEX>(depth);
@@ -604,11 +606,13 @@ KernelFn pick_vb_texl(int vb, int depth) {
 }
 
 // Leaf lines through the texture pipe (default shape, unchecked, address / key input).
+// texl: internal-level mode (0 LSU, 1 texture, 2 split); mode: leaf mode (1 texture,
+// 2 split). Instantiated: texl 0/1 with either leaf mode, texl 2 with texture leaves.
 template <int INPUT>
-KernelFn pick_leaftex(int vb, int depth, bool texl, int mode) {
-  if (mode == 2)
-    return texl ? pick_vb_texl<INPUT, true, 2>(vb, depth) : pick_vb_texl<INPUT, false, 2>(vb, depth);
-  return texl ? pick_vb_texl<INPUT, true, 1>(vb, depth) : pick_vb_texl<INPUT, false, 1>(vb, depth);
+KernelFn pick_leaftex(int vb, int depth, int texl, int mode) {
+  if (texl == 2) return mode == 1 ? pick_vb_texl<INPUT, 2, 1>(vb, depth) : nullptr;
+  if (mode == 2) return texl ? pick_vb_texl<INPUT, 1, 2>(vb, depth) : pick_vb_texl<INPUT, 0, 2>(vb, depth);
+  return texl ? pick_vb_texl<INPUT, 1, 1>(vb, depth) : pick_vb_texl<INPUT, 0, 1>(vb, depth);
 }
 
 template <int VB, bool CHECKED>
@@ -650,7 +654,7 @@ KernelFn pick_vb(int vb, int depth) {
 // Instantiated shapes (queries per lane, threads per CTA, min CTAs per SM);
 // bench.py --sweep measures them. The checked variant exists for the default shape.
 KernelFn pick_kernel(int vb, int depth, int tiles, int threads, int minb, bool checked = false,
-                     int input = kInAddr, bool leafs = false, bool texl = false, int leaftex = 0) {
+                     int input = kInAddr, bool leafs = false, int texl = 0, int leaftex = 0) {
   if (leaftex) {  // default shape, unchecked, no leaf image, depth >= 1
     if (leafs || checked || tiles != 1 || threads != 1024 || minb != 1) return nullptr;
     switch (input) {

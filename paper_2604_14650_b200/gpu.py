@@ -160,13 +160,13 @@ class Fib:
         return {"lanes_per_query": c.lanes_per_query, "smem_levels": c.smem_levels,
                 "ctas_per_sm": c.ctas_per_sm, "threads_per_cta": c.threads_per_cta,
                 "queries_per_lane": c.queries_per_lane, "min_ctas_per_sm": c.min_ctas_per_sm,
-                "leaf_path": c.leaf_path}
+                "line_path": c.line_path}
 
     def set_kernel_config(self, lanes_per_query: int = 0, smem_levels: int | None = None,
                           ctas_per_sm: int = 0, threads_per_cta: int = 0, queries_per_lane: int = 0,
-                          min_ctas_per_sm: int = 0, leaf_path: int = 0) -> dict:
+                          min_ctas_per_sm: int = 0, line_path: int = 0) -> dict:
         c = KernelConfig_t()
-        c.leaf_path = leaf_path
+        c.line_path = line_path
         c.lanes_per_query = lanes_per_query
         c.smem_levels = 0xFF if smem_levels is None else smem_levels
         c.ctas_per_sm = ctas_per_sm
@@ -176,24 +176,24 @@ class Fib:
         check(lib().lpm6cu_fib_set_kernel_config(self._h, C.byref(c)))
         return self.kernel_config()
 
-    def tune_leaf_path(self, addrs, out=None, stream=None, reps: int = 3) -> int:
-        """Time the leaf paths (0 LSU, 1 texture, 2 split) on a representative device
-        batch and keep the fastest in the kernel config; returns its number."""
+    def tune_line_path(self, addrs, out=None, stream=None, reps: int = 3) -> int:
+        """Time the line paths (lpm6cu_kernel_config.line_path 0-3) on a representative
+        device batch and keep the fastest in the kernel config; returns its number."""
         vb = self.value_bytes
         aptr, n, adev = _ptr_len(addrs, 16)
         if not adev:
-            raise Lpm6Error(9, "tune_leaf_path takes device buffers")
+            raise Lpm6Error(9, "tune_line_path takes device buffers")
         if out is None:
             torch = _torch()
             dt = {1: torch.uint8, 2: torch.int16, 4: torch.int32}[vb]
             out = torch.empty(n, dtype=dt, device=addrs.device)
         optr, nout, odev = _ptr_len(out, vb)
         if not odev:
-            raise Lpm6Error(9, "tune_leaf_path takes device buffers")
+            raise Lpm6Error(9, "tune_line_path takes device buffers")
         if nout < n:
             raise Lpm6Error(9, f"out holds {nout} next hops, need {n}")
         chosen = C.c_uint32()
-        check(lib().lpm6cu_fib_tune_leaf_path(self._h, aptr, n, optr, _stream_handle(stream), reps,
+        check(lib().lpm6cu_fib_tune_line_path(self._h, aptr, n, optr, _stream_handle(stream), reps,
                                               C.byref(chosen)))
         return int(chosen.value)
 

@@ -1,9 +1,10 @@
-"""Leaf lines through the texture pipe (lpm6cu_kernel_config.leaf_path = 1) and the
-measured choice between the two leaf paths (lpm6cu_fib_tune_leaf_path).
+"""Line paths (lpm6cu_kernel_config.line_path: which L1TEX pipe carries the leaf
+and internal L2 lines) and the measured choice between them
+(lpm6cu_fib_tune_line_path).
 
-The texture path changes only how a leaf line reaches registers, so every answer
-must equal the LSU path's and the oracle's; the tuner must leave the kernel
-config on one of the two paths and never change results."""
+A line path changes only how a line reaches registers, so every answer must
+equal the oracle's on every path; the tuner must leave the kernel config on one
+of the paths and never change results."""
 import numpy as np
 import pytest
 
@@ -15,8 +16,8 @@ VIEW = {1: np.uint8, 2: np.uint16, 4: np.uint32}
 
 
 @pytest.mark.parametrize("workload", ["C1", "C2", "C3b"])
-def test_texture_leaf_path_matches_oracle_on_workloads(lpm, orc, cuda, workload):
-    """2^22 queries of each workload plus every boundary ±1, every leaf path, address
+def test_texture_line_path_matches_oracle_on_workloads(lpm, orc, cuda, workload):
+    """2^22 queries of each workload plus every boundary ±1, every line path, address
     and key input: bit-exact against the oracle."""
     torch = cuda
     info = lpm.workload_info(workload)
@@ -35,9 +36,9 @@ def test_texture_leaf_path_matches_oracle_on_workloads(lpm, orc, cuda, workload)
     da = torch.from_numpy(addrs.view(np.uint8).reshape(-1, 16)).cuda()
     dk = torch.from_numpy(np.ascontiguousarray(addrs[:, 1]).view(np.int64)).cuda()
     view = VIEW[dev.geometry.value_bytes]
-    for lp in (1, 2, 0):
-        cfg = dev.set_kernel_config(leaf_path=lp)
-        assert cfg["leaf_path"] == lp
+    for lp in (1, 2, 3, 0):
+        cfg = dev.set_kernel_config(line_path=lp)
+        assert cfg["line_path"] == lp
         got = dev.lookup_batch(da)
         gk = dev.lookup_keys(dk)
         torch.cuda.synchronize()
@@ -47,7 +48,7 @@ def test_texture_leaf_path_matches_oracle_on_workloads(lpm, orc, cuda, workload)
 
 def test_tuner_picks_a_path_and_keeps_results(lpm, orc, cuda):
     torch = cuda
-    for workload in ("C1", "C3b"):
+    for workload in ("C1", "C2", "C3b"):
         info = lpm.workload_info(workload)
         fib = lpm.workload_fib(info.fib_kind)
         dev = lpm.Fib.build(fib)
@@ -56,9 +57,9 @@ def test_tuner_picks_a_path_and_keeps_results(lpm, orc, cuda):
         d = torch.empty((n, 16), dtype=torch.uint8, device="cuda")
         gen.run(0, n, d)
         base = dev.lookup_batch(d).clone()
-        chosen = dev.tune_leaf_path(d)
-        assert chosen in (0, 1, 2)
-        assert dev.kernel_config()["leaf_path"] == chosen
+        chosen = dev.tune_line_path(d)
+        assert chosen in (0, 1, 2, 3)
+        assert dev.kernel_config()["line_path"] == chosen
         again = dev.lookup_batch(d)
         torch.cuda.synchronize()
         assert torch.equal(base, again)
@@ -71,22 +72,22 @@ def test_tuner_on_checked_and_leaf_image_fibs_stays_on_lsu(lpm, cuda):
     fib = lpm.workload_fib(lpm.workload_info("C0").fib_kind)  # leaf-image tree
     dev = lpm.Fib.build(fib)
     a = torch.zeros((4096, 16), dtype=torch.uint8, device="cuda")
-    assert dev.tune_leaf_path(a) == 0
+    assert dev.tune_line_path(a) == 0
     big = lpm.Fib.build(lpm.workload_fib(1))
     big.set_checked(True)
-    assert big.tune_leaf_path(a) == 0
+    assert big.tune_line_path(a) == 0
     big.lookup_batch(a)
     torch.cuda.synchronize()
     assert big.violations() == 0
     big.set_checked(False)
 
 
-def test_leaf_path_argument_errors(lpm, cuda):
+def test_line_path_argument_errors(lpm, cuda):
     torch = cuda
     dev = lpm.Fib.build(lpm.workload_fib(1))
     with pytest.raises(lpm.Lpm6Error):
-        dev.set_kernel_config(leaf_path=3)
+        dev.set_kernel_config(line_path=4)
     with pytest.raises(lpm.Lpm6Error):
-        dev.tune_leaf_path(np.zeros((16, 16), np.uint8))  # host buffers
+        dev.tune_line_path(np.zeros((16, 16), np.uint8))  # host buffers
     with pytest.raises(lpm.Lpm6Error):
-        dev.tune_leaf_path(torch.zeros((0, 16), dtype=torch.uint8, device="cuda"))
+        dev.tune_line_path(torch.zeros((0, 16), dtype=torch.uint8, device="cuda"))

@@ -1,7 +1,7 @@
 """Randomised parity stress: random FIBs (0–60,000 rules, nesting, minimum
 lengths, default route on/off, merge on/off, 1/2/4-byte next hops, host or
 device build) through every kernel mode the FIB admits — every shared-memory
-split incl. the leaf image, both leaf paths, checked and unchecked, address / key /
+split incl. the leaf image, every line path, checked and unchecked, address / key /
 search_batch inputs — against the CPU oracle on every boundary ±1 and random keys."""
 import numpy as np
 import pytest
@@ -35,8 +35,8 @@ def test_random_fibs_every_mode(lpm, orc, cuda):
         dk = torch.from_numpy(keys.view(np.int64)).cuda()
         view = {1: np.uint8, 2: np.uint16, 4: np.uint32}[g.value_bytes]
         for t in [None] + list(range(g.depth + g.leaf_image + 1)):
-            for lp in (0, 1, 2):  # leaf lines through the LSU / the texture pipe / half each
-                dev.set_kernel_config(smem_levels=t, leaf_path=lp)
+            for lp in (0, 1, 2, 3):  # line paths: which L1TEX pipe carries the L2 lines
+                dev.set_kernel_config(smem_levels=t, line_path=lp)
                 for checked in (False, True):
                     dev.set_checked(checked)
                     for mode, got in (("addr", dev.lookup_batch(da)), ("keys", dev.lookup_keys(dk)),
