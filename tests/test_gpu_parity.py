@@ -187,24 +187,14 @@ def test_checked_mode_flags_corrupted_tree(lpm, orc, cuda):
     assert good.violations() == 0
 
 
+LINE_PATHS = (0, 1, 2, 3)  # lpm6cu_kernel_config.line_path: every plan the tuner can pick
+
+
 def test_c1_full_size(lpm, orc, cuda):
-    """C1 at BASELINE size: 268,435,456 queries, every one checked against the oracle."""
-    torch = cuda
-    info = lpm.workload_info("C1")
-    fib = lpm.workload_fib(info.fib_kind)
-    imap = lpm.build_intervals(fib)
-    dev = lpm.Fib.build(fib)
-    gen = lpm.QueryGen("C1", fib)
-    chunk = 1 << 26
-    d = torch.empty((chunk, 16), dtype=torch.uint8, device="cuda")
-    mism = 0
-    for c in range(info.n_queries // chunk):
-        gen.run(c * chunk, chunk, d)
-        out = dev.lookup_batch(d)
-        host_addrs = d.cpu().numpy().view(np.uint64).reshape(-1, 2)
-        want = oracle_next_hops(orc, imap.boundaries, imap.next_hops, host_addrs)
-        mism += int(np.count_nonzero(out.cpu().numpy().astype(np.uint32) != want))
-    assert mism == 0
+    """C1 at BASELINE size: 268,435,456 queries, every one checked against the oracle,
+    on every line path."""
+    mism, checked = _check_chunks(lpm, orc, cuda, "C1", range(4), 1 << 26)
+    assert checked == 1 << 28 and mism == 0
 
 
 def _check_chunks(lpm, orc, cuda, workload, chunks, chunk):
@@ -219,17 +209,20 @@ def _check_chunks(lpm, orc, cuda, workload, chunks, chunk):
     mism = checked = 0
     for c in chunks:
         gen.run(c * chunk, chunk, d)
-        out = dev.lookup_batch(d)
         host_addrs = d.cpu().numpy().view(np.uint64).reshape(-1, 2)
         want = oracle_next_hops(orc, imap.boundaries, imap.next_hops, host_addrs)
-        got = out.cpu().numpy().view(vdt).astype(np.uint32)
-        mism += int(np.count_nonzero(got != want))
+        for lp in LINE_PATHS:  # one oracle pass, every line path
+            dev.set_kernel_config(line_path=lp)
+            out = dev.lookup_batch(d)
+            got = out.cpu().numpy().view(vdt).astype(np.uint32)
+            mism += int(np.count_nonzero(got != want))
         checked += chunk
     return mism, checked
 
 
 def test_c2_full_size(lpm, orc, cuda):
-    """C2 at BASELINE size: 1,073,741,824 queries over the 1M-prefix FIB, every one checked."""
+    """C2 at BASELINE size: 1,073,741,824 queries over the 1M-prefix FIB, every one checked
+    on every line path."""
     mism, checked = _check_chunks(lpm, orc, cuda, "C2", range(16), 1 << 26)
     assert checked == 1 << 30 and mism == 0
 
