@@ -213,9 +213,11 @@ int lpm6cu_fib_node_visits(lpm6cu_fib* fib, uint64_t* visits, int reset);
 
 /* n next hops for n addresses. With device pointers: one kernel launch on
  * `stream` (a cudaStream_t; NULL = legacy default), asynchronous, no host sync,
- * no allocation. With host pointers (pinned or pageable): chunked host->device
- * copy / lookup / device->host copy pipeline on internal streams ordered after
- * `stream`; returns when `out` holds the results. */
+ * no allocation — when `out` is 4*value_bytes-byte aligned; at any other byte
+ * offset the results go through a stream-ordered scratch buffer and one
+ * device-to-device copy. With host pointers (pinned or pageable): chunked
+ * host->device copy / lookup / device->host copy pipeline on internal streams
+ * ordered after `stream`; returns when `out` holds the results. */
 int lpm6cu_lookup_batch(const lpm6cu_fib* fib, const void* addrs, uint64_t n, void* out,
                         void* stream);
 

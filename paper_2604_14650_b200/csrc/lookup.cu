@@ -203,6 +203,24 @@ struct PacketInput {
 void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, void* d_out, cudaStream_t stream,
                    int input = kInAddr, const PacketInput* pk = nullptr, unsigned* d_ord = nullptr) {
   if (n == 0) return;
+  // The kernels store a 4-query group's next hops with one 4*vb-byte store, so the
+  // result buffer must be 4*vb-byte aligned. A caller's pointer at any other byte
+  // offset (a slice of a byte buffer) gets a stream-ordered aligned scratch buffer
+  // and a device-to-device copy; the aligned fast path is unchanged.
+  const unsigned long long vb_out = f->g.value_bytes;
+  if (d_out && reinterpret_cast<uintptr_t>(d_out) % (4 * vb_out) != 0) {
+    void* tmp = nullptr;
+    check_cuda(cudaMallocAsync(&tmp, n * vb_out, stream), "cudaMallocAsync (unaligned result buffer)");
+    try {
+      launch_lookup(f, d_in, n, tmp, stream, input, pk, d_ord);
+      check_cuda(cudaMemcpyAsync(d_out, tmp, n * vb_out, cudaMemcpyDeviceToDevice, stream), "copy results");
+    } catch (...) {
+      cudaFreeAsync(tmp, stream);
+      throw;
+    }
+    check_cuda(cudaFreeAsync(tmp, stream), "cudaFreeAsync");
+    return;
+  }
   const bool dflt = input != kInAddr;
   const unsigned tiles = dflt ? 1 : f->cfg.queries_per_lane;
   const unsigned threads_cta = dflt ? 1024 : f->cfg.threads_per_cta;
