@@ -294,6 +294,26 @@ int lpm6cu_store_commit(lpm6cu_store* s, uint64_t* epoch) {
     // pending ops untouched.
     lpm6cu_snapshot* next = s->build(std::move(rules), cur + 1);
     {
+      // The new FIB inherits the active one's kernel config (shape and the tuned
+      // line path, lpm6cu_fib_tune_line_path); the staged levels are re-resolved
+      // for the new tree. Only commits retire the active snapshot, and this one
+      // holds commit_mu, so reading it here is safe.
+      const lpm6cu_fib* prev = nullptr;
+      {
+        std::lock_guard<std::mutex> lk(s->mu);
+        prev = s->active->fib;
+      }
+      lpm6cu_kernel_config c{};
+      if (lpm6cu_fib_kernel_config(prev, &c) == LPM6CU_OK) {
+        c.smem_levels = 0xFF;
+        if (lpm6cu_fib_set_kernel_config(next->fib, &c) != LPM6CU_OK) {
+          lpm6cu_kernel_config d{};
+          d.smem_levels = 0xFF;
+          lpm6cu_fib_set_kernel_config(next->fib, &d);  // shape not available for this tree: defaults
+        }
+      }
+    }
+    {
       std::lock_guard<std::mutex> lk(s->stage_mu);
       s->pending.erase(s->pending.begin(), s->pending.begin() + static_cast<std::ptrdiff_t>(taken));
     }

@@ -188,6 +188,27 @@ def test_value_width_follows_commits(lpm, orc, cuda, st):
     store.close()
 
 
+def test_commit_keeps_the_tuned_kernel_config(lpm, orc, cuda, st):
+    """A new snapshot inherits the active FIB's kernel config (the tuned line path),
+    with the staged levels re-resolved for the new tree; lookups stay exact."""
+    from paper_2604_14650_b200.fib import Prefix
+    rng = np.random.default_rng(6)
+    fib = lpm.workload_fib(1)
+    store = st.FibStore(fib)
+    with store.acquire() as snap:
+        snap.fib.set_kernel_config(line_path=2)
+    ops = [st.UpdateOp(st.ANNOUNCE, Prefix((0x2001 << 112) | (i << 64), 64, 7)) for i in range(50)]
+    store.stage(ops)
+    store.commit()
+    view, _, _ = st.apply_updates(fib, ops)
+    with store.acquire() as snap:
+        cfg = snap.fib.kernel_config()
+        assert cfg["line_path"] == 2 and cfg["smem_levels"] == snap.fib.geometry.image_levels
+        addrs = probe_addrs(lpm, view, rng)
+        np.testing.assert_array_equal(lookup(cuda, snap, addrs), expected(lpm, orc, view, addrs))
+    store.close()
+
+
 def test_epoch_monotonic_over_1000_commits(lpm, cuda, st):
     """Epoch monotonicity across >= 10^3 commits; memory is reclaimed as it goes."""
     from paper_2604_14650_b200.fib import PREFIX_DTYPE, Prefix
