@@ -215,9 +215,11 @@ int lpm6cu_fib_node_visits(lpm6cu_fib* fib, uint64_t* visits, int reset);
  * `stream` (a cudaStream_t; NULL = legacy default), asynchronous, no host sync,
  * no allocation — when `out` is 4*value_bytes-byte aligned; at any other byte
  * offset the results go through a stream-ordered scratch buffer and one
- * device-to-device copy. With host pointers (pinned or pageable): chunked
- * host->device copy / lookup / device->host copy pipeline on internal streams
- * ordered after `stream`; returns when `out` holds the results. */
+ * device-to-device copy. With host pointers: page-locked buffers of up to 2^20
+ * queries are read and written by the kernel over PCIe (zero-copy: one launch,
+ * one sync); larger or pageable buffers go through a chunked host->device copy /
+ * lookup / device->host copy pipeline. Either way the work is ordered after
+ * `stream` and the call returns when `out` holds the results. */
 int lpm6cu_lookup_batch(const lpm6cu_fib* fib, const void* addrs, uint64_t n, void* out,
                         void* stream);
 
