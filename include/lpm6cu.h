@@ -29,6 +29,8 @@
  *     change how later lookups run and must not race with lookups on the handle.
  *   - There is no CPU fallback: a lookup without a usable CUDA device fails with
  *     LPM6CU_E_CUDA.
+ *   - Device buffers must live on the FIB's own device (InvalidArgument otherwise:
+ *     a kernel touching another GPU's memory would poison the CUDA context).
  */
 #ifndef LPM6CU_H
 #define LPM6CU_H

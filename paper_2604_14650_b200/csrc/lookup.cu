@@ -359,12 +359,18 @@ void load_root(lpm6cu_fib* f) {
   f->root_ready = true;
 }
 
-bool is_device_ptr(const void* p) {
+// True for device (or managed) memory. Device memory must be on the FIB's own
+// device: the kernel would fault on another GPU's allocation (no peer mapping is
+// assumed), which poisons the whole CUDA context, so that is rejected here.
+bool is_device_ptr(const void* p, int device) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
+  if (a.type == cudaMemoryTypeDevice && a.device != device)
+    throw Error(Errc::InvalidArgument, "buffer is on CUDA device " + std::to_string(a.device) +
+                                           ", the FIB on device " + std::to_string(device));
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
@@ -567,7 +573,7 @@ int lpm6cu_fib_tune_line_path(lpm6cu_fib* f, const void* d_addrs, uint64_t n, vo
     if (!f || !d_addrs || !d_out) throw Error(Errc::InvalidArgument, "NULL argument");
     if (n == 0) throw Error(Errc::InvalidArgument, "empty tuning batch");
     DeviceGuard dg(f->device);
-    if (!is_device_ptr(d_addrs) || !is_device_ptr(d_out))
+    if (!is_device_ptr(d_addrs, f->device) || !is_device_ptr(d_out, f->device))
       throw Error(Errc::InvalidArgument, "lpm6cu_fib_tune_line_path takes device buffers");
     if (reinterpret_cast<uintptr_t>(d_addrs) % 16 != 0)
       throw Error(Errc::InvalidArgument, "addresses must be 16-byte aligned");
@@ -669,7 +675,7 @@ int lpm6cu_lookup_batch(const lpm6cu_fib* fib, const void* addrs, uint64_t n, vo
     if (n == 0) return;
     if (!addrs || !out) throw Error(Errc::InvalidArgument, "NULL buffer");
     DeviceGuard dg(fib->device);
-    const bool da = is_device_ptr(addrs), dout = is_device_ptr(out);
+    const bool da = is_device_ptr(addrs, fib->device), dout = is_device_ptr(out, fib->device);
     if (da != dout)
       throw Error(Errc::InvalidArgument, "addresses and results must both be device or both be host memory");
     if (reinterpret_cast<uintptr_t>(addrs) % 16 != 0)
@@ -687,7 +693,7 @@ int lpm6cu_lookup_keys(const lpm6cu_fib* fib, const uint64_t* keys, uint64_t n, 
     if (n == 0) return;
     if (!keys || !out) throw Error(Errc::InvalidArgument, "NULL buffer");
     DeviceGuard dg(fib->device);
-    const bool dk = is_device_ptr(keys), dout = is_device_ptr(out);
+    const bool dk = is_device_ptr(keys, fib->device), dout = is_device_ptr(out, fib->device);
     if (dk != dout) throw Error(Errc::InvalidArgument, "keys and results must both be device or both be host memory");
     if (reinterpret_cast<uintptr_t>(keys) % 8 != 0) throw Error(Errc::InvalidArgument, "keys must be 8-byte aligned");
     if (dk)
@@ -704,7 +710,8 @@ int lpm6cu_search_batch(const lpm6cu_fib* fib, const uint64_t* keys, uint64_t n,
     if (n == 0) return;
     if (!keys || !ordinals) throw Error(Errc::InvalidArgument, "NULL buffer");
     DeviceGuard dg(fib->device);
-    if (!is_device_ptr(keys) || !is_device_ptr(ordinals) || (next_hops && !is_device_ptr(next_hops)))
+    if (!is_device_ptr(keys, fib->device) || !is_device_ptr(ordinals, fib->device) ||
+        (next_hops && !is_device_ptr(next_hops, fib->device)))
       throw Error(Errc::InvalidArgument, "lpm6cu_search_batch takes device buffers");
     if (reinterpret_cast<uintptr_t>(keys) % 8 != 0 || reinterpret_cast<uintptr_t>(ordinals) % 4 != 0)
       throw Error(Errc::InvalidArgument, "keys must be 8-byte and ordinals 4-byte aligned");
@@ -720,7 +727,7 @@ int lpm6cu_lookup_packets(const lpm6cu_fib* fib, const void* frames, uint64_t n,
     if (!frames || !out) throw Error(Errc::InvalidArgument, "NULL buffer");
     if (stride < dst_offset + 16ull) throw Error(Errc::InvalidArgument, "stride must cover dst_offset + 16 bytes");
     DeviceGuard dg(fib->device);
-    if (!is_device_ptr(frames) || !is_device_ptr(out))
+    if (!is_device_ptr(frames, fib->device) || !is_device_ptr(out, fib->device))
       throw Error(Errc::InvalidArgument, "lpm6cu_lookup_packets takes device buffers");
     PacketInput pk;
     pk.stride = stride;
