@@ -191,8 +191,9 @@ int lpm6cu_fib_device_lines(const lpm6cu_fib* fib, const void** d_lines);
 int lpm6cu_fib_copy_lines(const lpm6cu_fib* fib, uint64_t* host_lines, uint64_t words);
 int lpm6cu_fib_set_kernel_config(lpm6cu_fib* fib, const lpm6cu_kernel_config* cfg);
 int lpm6cu_fib_kernel_config(const lpm6cu_fib* fib, lpm6cu_kernel_config* cfg);
-/* Times the line paths on a representative batch (device buffers, `reps` timed
- * launches each after one untimed, on `stream`; synchronizes it), keeps the
+/* Times the line paths on a representative batch (device buffers; two interleaved
+ * rounds of `reps` timed launches per path after one untimed, the faster round
+ * kept; on `stream`, which it synchronizes), keeps the
  * fastest in the kernel config and returns it in *line_path (0..3, see
  * lpm6cu_kernel_config; 3 only when the tree has internal L2 levels). Results are
  * identical on every path; like the other tuning calls it must not race with

@@ -32,19 +32,21 @@
 // 0xFFFF...FFFE) (types.hpp:25), internal child = node * 16 + rank, leaf
 // ordinal = rank - 1, next hop = the value of that leaf slot.
 //
-// Included once, by lookup.cu; everything here is in an anonymous namespace.
+// Included by lookup_vb{1,2,4}.cu (one next-hop width each); the kernels are in an
+// anonymous namespace, the launch interface in lookup_params.hpp.
 #pragma once
 
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "capi_internal.hpp"
+#include "lookup_params.hpp"
 
 namespace {
 
 using namespace lpm6;
+using namespace lpm6::kern;
 
-constexpr int kMaxKernelDepth = 7;
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
 // ---- PTX helpers ------------------------------------------------------------
@@ -68,8 +70,6 @@ __device__ __forceinline__ uint4 ld_stream_v4(const uint4* p, uint64_t pol) {
 }
 
 
-// Input formats of the lookup kernel.
-enum : int { kInAddr = 0, kInKey = 1, kInPacket = 2, kInKeyOrd = 3 };  // kInKeyOrd: keys in, ordinals out too
 
 template <class T>
 __device__ __forceinline__ T ld_stream(const void* p, uint64_t pol);
@@ -199,27 +199,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 
 // ---- kernel -----------------------------------------------------------------
 
-struct LookupParams {
-  const unsigned long long* lines;                     // the tree, 16 u64 words per line
-  unsigned long long level_start[LPM6CU_MAX_LEVELS];  // word offset of each level
-  const uint4* addrs;               // kInAddr: 16-byte addresses (lookup_batch), or
-  const unsigned long long* keys;   // kInKey / kInKeyOrd: 8-byte keys (search_batch's input), or
-  unsigned int* ord;                // kInKeyOrd: interval ordinal per query (SearchResult::interval_ordinal)
-  const unsigned char* pkts;        // kInPacket: frames, destination address at pkt_off of each
-  unsigned long long pkt_stride;    //   bytes between frames
-  unsigned int pkt_off;             //   byte offset of the IPv6 destination address in a frame
-  unsigned int pkt_align;           //   16, 8, 4, 2 or 1: alignment of every frame start
-  unsigned char* out;
-  unsigned long long n;
-  const unsigned long long* image;  // packed 15-key copy of internal levels 0.. (layout.hpp)
-  unsigned int smem_levels;  // phase A levels [0, smem_levels), <= depth
-  unsigned int smem_bytes;   // image bytes staged for those levels (+ the leaf image when LEAFS)
-  unsigned int leaf_image_off;  // LEAFS: word offset of the leaf image in shared memory
-  unsigned long long level_nodes[LPM6CU_MAX_LEVELS];  // checked mode: node-index bounds
-  unsigned int* err;         // checked mode: OR of violation bits (1 smem level, 2 line level, 4 leaf rank)
-  unsigned long long root[16];  // the root's 15 separators (+ sentinel), read from the constant bank
-  unsigned long long tex;       // texture object over the line array (int4 texels), 0 = none
-};
+
 
 // Count of the 15 separators of node n of a shared-memory image level that are
 // <= q: a branch-free 4-probe binary search (16 outcomes). The probe positions
@@ -577,10 +557,10 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
   }
 }
 
-using KernelFn = void (*)(const LookupParams);
 
-// Instantiated shapes: (queries per lane, min CTAs per SM) for every depth and
-// value width; the tuning grid below is measured by bench.py --sweep.
+// Instantiated shapes: (queries per lane, min CTAs per SM) for every depth; one
+// next-hop width per translation unit (lookup_vb{1,2,4}.cu), so the ~150 kernels
+// of each width compile in parallel. bench.py --sweep measures the shapes.
 template <int VB, int INPUT, int TEXL, int LEAFTEX>
 KernelFn pick_depth_texl(int depth) {
   switch (depth) {
@@ -595,24 +575,14 @@ KernelFn pick_depth_texl(int depth) {
   }
 }
 
-template <int INPUT, int TEXL = 1, int LEAFTEX = 0>
-KernelFn pick_vb_texl(int vb, int depth) {
-  switch (vb) {
-    case 1: return pick_depth_texl<1, INPUT, TEXL, LEAFTEX>(depth);
-    case 2: return pick_depth_texl<2, INPUT, TEXL, LEAFTEX>(depth);
-    case 4: return pick_depth_texl<4, INPUT, TEXL, LEAFTEX>(depth);
-    default: return nullptr;
-  }
-}
-
 // Leaf lines through the texture pipe (default shape, unchecked, address / key input).
 // texl: internal-level mode (0 LSU, 1 texture, 2 split); mode: leaf mode (1 texture,
 // 2 split). Instantiated: texl 0/1 with either leaf mode, texl 2 with texture leaves.
-template <int INPUT>
-KernelFn pick_leaftex(int vb, int depth, int texl, int mode) {
-  if (texl == 2) return mode == 1 ? pick_vb_texl<INPUT, 2, 1>(vb, depth) : nullptr;
-  if (mode == 2) return texl ? pick_vb_texl<INPUT, 1, 2>(vb, depth) : pick_vb_texl<INPUT, 0, 2>(vb, depth);
-  return texl ? pick_vb_texl<INPUT, 1, 1>(vb, depth) : pick_vb_texl<INPUT, 0, 1>(vb, depth);
+template <int VB, int INPUT>
+KernelFn pick_leaftex(int depth, int texl, int mode) {
+  if (texl == 2) return mode == 1 ? pick_depth_texl<VB, INPUT, 2, 1>(depth) : nullptr;
+  if (mode == 2) return texl ? pick_depth_texl<VB, INPUT, 1, 2>(depth) : pick_depth_texl<VB, INPUT, 0, 2>(depth);
+  return texl ? pick_depth_texl<VB, INPUT, 1, 1>(depth) : pick_depth_texl<VB, INPUT, 0, 1>(depth);
 }
 
 template <int VB, bool CHECKED>
@@ -626,7 +596,7 @@ KernelFn pick_depth_leafs(int depth) {
   }
 }
 
-template <int VB, int TILES, int THREADS, int MINB, bool CHECKED, int INPUT>
+template <int VB, int TILES, int THREADS, int MINB, bool CHECKED = false, int INPUT = kInAddr>
 KernelFn pick_depth(int depth) {
   switch (depth) {
     case 0: return lpm6_lookup_kernel<0, VB, TILES, THREADS, MINB, CHECKED, INPUT>;
@@ -641,64 +611,51 @@ KernelFn pick_depth(int depth) {
   }
 }
 
-template <int TILES, int THREADS, int MINB, bool CHECKED = false, int INPUT = kInAddr>
-KernelFn pick_vb(int vb, int depth) {
-  switch (vb) {
-    case 1: return pick_depth<1, TILES, THREADS, MINB, CHECKED, INPUT>(depth);
-    case 2: return pick_depth<2, TILES, THREADS, MINB, CHECKED, INPUT>(depth);
-    case 4: return pick_depth<4, TILES, THREADS, MINB, CHECKED, INPUT>(depth);
-    default: return nullptr;
-  }
-}
-
-// Instantiated shapes (queries per lane, threads per CTA, min CTAs per SM);
-// bench.py --sweep measures them. The checked variant exists for the default shape.
-KernelFn pick_kernel(int vb, int depth, int tiles, int threads, int minb, bool checked = false,
-                     int input = kInAddr, bool leafs = false, int texl = 0, int leaftex = 0) {
-  if (leaftex) {  // default shape, unchecked, no leaf image, depth >= 1
-    if (leafs || checked || tiles != 1 || threads != 1024 || minb != 1) return nullptr;
-    switch (input) {
-      case kInAddr: return pick_leaftex<kInAddr>(vb, depth, texl, leaftex);
-      case kInKey: return pick_leaftex<kInKey>(vb, depth, texl, leaftex);
+// The kernel for one next-hop width (see pick_kernel in lookup_params.hpp). The
+// checked variant exists for the default shape.
+template <int VB>
+KernelFn pick_kernel_t(const PickArgs& a) {
+  const int depth = a.depth;
+  const bool dflt = a.tiles == 1 && a.threads == 1024 && a.minb == 1;
+  if (a.leaftex) {  // default shape, unchecked, no leaf image, depth >= 1
+    if (a.leafs || a.checked || !dflt) return nullptr;
+    switch (a.input) {
+      case kInAddr: return pick_leaftex<VB, kInAddr>(depth, a.texl, a.leaftex);
+      case kInKey: return pick_leaftex<VB, kInKey>(depth, a.texl, a.leaftex);
       default: return nullptr;
     }
   }
-  if (texl) {  // internal L2 levels via the texture pipe: default shape, unchecked
-    if (leafs || checked || tiles != 1 || threads != 1024 || minb != 1) return nullptr;
-    switch (input) {
-      case kInAddr: return pick_vb_texl<kInAddr>(vb, depth);
-      case kInKey: return pick_vb_texl<kInKey>(vb, depth);
-      case kInPacket: return pick_vb_texl<kInPacket>(vb, depth);
+  if (a.texl) {  // internal L2 levels via the texture pipe: default shape, unchecked
+    if (a.leafs || a.checked || !dflt) return nullptr;
+    switch (a.input) {
+      case kInAddr: return pick_depth_texl<VB, kInAddr, 1, 0>(depth);
+      case kInKey: return pick_depth_texl<VB, kInKey, 1, 0>(depth);
+      case kInPacket: return pick_depth_texl<VB, kInPacket, 1, 0>(depth);
       default: return nullptr;  // kInKeyOrd: LSU loads
     }
   }
-  if (leafs) {  // leaf image: address input, default shape, depth <= kMaxLeafImageDepth
-    if (input != kInAddr || tiles != 1 || threads != 1024 || minb != 1) return nullptr;
-    switch (vb) {
-      case 1: return checked ? pick_depth_leafs<1, true>(depth) : pick_depth_leafs<1, false>(depth);
-      case 2: return checked ? pick_depth_leafs<2, true>(depth) : pick_depth_leafs<2, false>(depth);
-      case 4: return checked ? pick_depth_leafs<4, true>(depth) : pick_depth_leafs<4, false>(depth);
-      default: return nullptr;
-    }
+  if (a.leafs) {  // leaf image: address input, default shape, depth <= kMaxLeafImageDepth
+    if (a.input != kInAddr || !dflt) return nullptr;
+    return a.checked ? pick_depth_leafs<VB, true>(depth) : pick_depth_leafs<VB, false>(depth);
   }
-  if (input != kInAddr) {  // key / packet input: the default shape, unchecked and checked
-    if (tiles != 1 || threads != 1024 || minb != 1) return nullptr;
-    if (input == kInKey)
-      return checked ? pick_vb<1, 1024, 1, true, kInKey>(vb, depth) : pick_vb<1, 1024, 1, false, kInKey>(vb, depth);
-    if (input == kInPacket)
-      return checked ? pick_vb<1, 1024, 1, true, kInPacket>(vb, depth)
-                     : pick_vb<1, 1024, 1, false, kInPacket>(vb, depth);
-    if (input == kInKeyOrd)
-      return checked ? pick_vb<1, 1024, 1, true, kInKeyOrd>(vb, depth)
-                     : pick_vb<1, 1024, 1, false, kInKeyOrd>(vb, depth);
+  if (a.input != kInAddr) {  // key / packet input: the default shape, unchecked and checked
+    if (!dflt) return nullptr;
+    if (a.input == kInKey)
+      return a.checked ? pick_depth<VB, 1, 1024, 1, true, kInKey>(depth) : pick_depth<VB, 1, 1024, 1, false, kInKey>(depth);
+    if (a.input == kInPacket)
+      return a.checked ? pick_depth<VB, 1, 1024, 1, true, kInPacket>(depth)
+                       : pick_depth<VB, 1, 1024, 1, false, kInPacket>(depth);
+    if (a.input == kInKeyOrd)
+      return a.checked ? pick_depth<VB, 1, 1024, 1, true, kInKeyOrd>(depth)
+                       : pick_depth<VB, 1, 1024, 1, false, kInKeyOrd>(depth);
     return nullptr;
   }
-  if (checked) return (tiles == 1 && threads == 1024 && minb == 1) ? pick_vb<1, 1024, 1, true>(vb, depth) : nullptr;
-  if (tiles == 1 && threads == 256 && minb == 0) return pick_vb<1, 256, 0>(vb, depth);
-  if (tiles == 1 && threads == 256 && minb == 4) return pick_vb<1, 256, 4>(vb, depth);
-  if (tiles == 2 && threads == 256 && minb == 0) return pick_vb<2, 256, 0>(vb, depth);
-  if (tiles == 1 && threads == 512 && minb == 2) return pick_vb<1, 512, 2>(vb, depth);
-  if (tiles == 1 && threads == 1024 && minb == 1) return pick_vb<1, 1024, 1>(vb, depth);
+  if (a.checked) return dflt ? pick_depth<VB, 1, 1024, 1, true>(depth) : nullptr;
+  if (a.tiles == 1 && a.threads == 256 && a.minb == 0) return pick_depth<VB, 1, 256, 0>(depth);
+  if (a.tiles == 1 && a.threads == 256 && a.minb == 4) return pick_depth<VB, 1, 256, 4>(depth);
+  if (a.tiles == 2 && a.threads == 256 && a.minb == 0) return pick_depth<VB, 2, 256, 0>(depth);
+  if (a.tiles == 1 && a.threads == 512 && a.minb == 2) return pick_depth<VB, 1, 512, 2>(depth);
+  if (dflt) return pick_depth<VB, 1, 1024, 1>(depth);
   return nullptr;
 }
 

@@ -1,0 +1,6 @@
+// Lookup kernels for 2-byte next hops (instantiated from lookup_kernel.cuh).
+#include "lookup_kernel.cuh"
+
+namespace lpm6::kern {
+KernelFn pick_kernel_vb2(const PickArgs& a) { return pick_kernel_t<2>(a); }
+}  // namespace lpm6::kern
