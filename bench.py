@@ -623,7 +623,7 @@ def main():
     torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(dev_index) as clk:
-        if use_graph:
+        if use_graph and hasattr(torch.cuda, "_sleep"):
             # Launch-bound steps (~12 us): hold the stream in an untimed device sleep
             # while the host enqueues all K replays, so host submission gaps never
             # land between the timing events (the sleep itself is before ev[0]).
