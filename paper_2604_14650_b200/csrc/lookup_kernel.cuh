@@ -42,10 +42,6 @@
 #include "capi_internal.hpp"
 #include "lookup_params.hpp"
 
-#ifndef LPM6_ROOT_VARIANT
-#define LPM6_ROOT_VARIANT 0
-#endif
-
 namespace {
 
 using namespace lpm6;
@@ -407,21 +403,10 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
             // same node, so the probes are (nearly) uniform LDCs and keep the
             // shared-memory data pipe free for the deeper levels.
             const unsigned long long q = key[t];
-#if LPM6_ROOT_VARIANT == 1
-            unsigned c = 0;
-#pragma unroll
-            for (int i = 0; i < 15; ++i) c += (p.root[i] <= q) ? 1u : 0u;
-#elif LPM6_ROOT_VARIANT == 2
-            const bool b7 = p.root[7] <= q, b3 = p.root[3] <= q, b11 = p.root[11] <= q;
-            unsigned c = b7 ? (b11 ? 12u : 8u) : (b3 ? 4u : 0u);
-            c |= (p.root[c | 1u] <= q) ? 2u : 0u;
-            c |= (p.root[c] <= q) ? 1u : 0u;
-#else
             unsigned c = (p.root[7] <= q) ? 8u : 0u;
             c |= (p.root[c | 3u] <= q) ? 4u : 0u;
             c |= (p.root[c | 1u] <= q) ? 2u : 0u;
             c |= (p.root[c] <= q) ? 1u : 0u;
-#endif
             node[t] = c;
           } else {
             const uint32_t lvl = s_base + static_cast<uint32_t>(p.level_start[l] >> 4) * 120u;
