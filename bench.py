@@ -436,6 +436,16 @@ def run_reference(args):
     return 0
 
 
+def gather_per_rank(ms, dist):
+    """Every rank's summed device time of the timed steps (rank order), for the
+    balance check in multi-GPU lines; [ms] at one rank."""
+    if dist is None:
+        return [ms]
+    allv = [None] * dist.get_world_size()
+    dist.all_gather_object(allv, float(ms))
+    return allv
+
+
 def choose_line_path(args, fdev, addrs, out, stream):
     """Leaf path for the timed steps: fixed by --line-path, or measured on this batch
     (untimed, before the warm-up) by the library's tuner. Returns the kernel config."""
@@ -494,6 +504,7 @@ def run_chunked(args, lpm, dispatch, fdev, fib, info, geom, cfg, ws, rank, dev_i
     with ClockSampler(dev_index) as clk:
         step_ms = [one_pass() for _ in range(args.steps)]
     total_ms = dispatch.max_over_ranks(sum(step_ms), dist, "cuda")
+    per_rank_ms = gather_per_rank(sum(step_ms), dist)
     value = info.n_queries * args.steps / (total_ms * 1e-3) / 1e9
     parity = None
     if rank == 0:  # CPU-baseline leg: the oracle checks a sample of chunk c0's output
@@ -531,7 +542,7 @@ def run_chunked(args, lpm, dispatch, fdev, fib, info, geom, cfg, ws, rank, dev_i
         "gpu_launches": 2 * nc * args.steps,
         "clocks": clk.summary(), "parity_sample": parity,
         "fib_build_ms": build_ms, "fib_build_device_ms": device_build_ms(lpm, fib, dev_index, vb),
-        "fib_broadcast_ms": bcast_ms, "step_ms": step_ms,
+        "fib_broadcast_ms": bcast_ms, "step_ms": step_ms, "per_rank_total_ms": per_rank_ms,
     }
     if ws > 1 and shared_gpu_mode():
         line["harness_check"] = "LPM6_BENCH_SHARED_GPU: ranks shared GPUs over gloo; not a bench value"
@@ -637,6 +648,7 @@ def main():
         dist.barrier()
     step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     total_ms = dispatch.max_over_ranks(sum(step_ms), dist, "cuda")
+    per_rank_ms = gather_per_rank(sum(step_ms), dist)
     ms_per_step = total_ms / args.steps
     value = ws * n * args.steps / (total_ms * 1e-3) / 1e9  # aggregate G lookups/s
     lps_gpu = n / (ms_per_step * 1e-3)
@@ -768,6 +780,7 @@ def main():
         "fib_broadcast_ms": bcast_ms,
         "step_ms": step_ms,
         "ms_per_step_median": float(np.median(step_ms)),
+        "per_rank_total_ms": per_rank_ms,
     }
     if sweep is not None:
         line["sweep"] = sweep
