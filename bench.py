@@ -403,6 +403,23 @@ def time_restated_planb(fib, addrs, threads):
     return dt, {2: "avx512_batch16", 1: "branchfree_scalar"}[ran]
 
 
+def single_thread_baselines(fib, addrs, n1=1 << 22):
+    """SURVEY §8d asks for the CPU baselines on one thread as well as on all cores:
+    the reference's lookup_interval_oracle and the restated PlanB search on the first
+    n1 queries of the sample, one thread each."""
+    a = addrs[:n1]
+    out = {"sample": f"first {len(a)} queries, 1 thread"}
+    times, kind, _ = time_reference_cpu(fib, a, 1, repeats=1)
+    out["reference_oracle"] = {"value": len(a) / times[0] / 1e9, "unit": UNIT, "cores": 1, "kind": kind}
+    try:
+        dt, variant = time_restated_planb(fib, a, 1)
+        out["restated_planb"] = {"value": len(a) / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "port",
+                                 "variant": variant}
+    except Exception as e:  # extra context only
+        out["restated_planb"] = {"error": str(e)}
+    return out
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -432,6 +449,7 @@ def run_reference(args):
                                       "variant": variant, "sample": f"{n} queries"}
     except Exception as e:  # the restatement is extra context only
         line["restated_planb_cpu"] = {"error": str(e)}
+    line["single_thread"] = single_thread_baselines(fib, addrs)
     print(json.dumps(line), flush=True)
     return 0
 
@@ -739,6 +757,7 @@ def main():
                                      "variant": variant}
         except Exception as e:
             cpu["restated_planb"] = {"error": str(e)}
+        cpu["single_thread"] = single_thread_baselines(fib, ha)
 
     if rank != 0:
         if dist is not None:
