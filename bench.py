@@ -32,7 +32,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "IPv6 lookups/sec (G/s) per B200 and at 1/2/4/8 GPUs; % of roofline"
 UNIT = "G lookups/s"
 HBM_FALLBACK_GBS = 6650.0
-CPU_SAMPLE = 1 << 25  # bounded CPU-baseline sample (33.5M queries)
+CPU_SAMPLE = 1 << 26  # bounded CPU-baseline sample (67.1M queries; SURVEY §8d asks >= 64M)
 
 
 def parse_args():
