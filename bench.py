@@ -454,6 +454,30 @@ def run_reference(args):
     return 0
 
 
+def output_digest(torch, gen, fdev, addrs, out, c0, nc, chunk, stream, dist):
+    """sha256 over (chunk index, per-chunk hash) for all chunks in order; the per-chunk
+    hash is a position-weighted wrapping sum of the chunk's next-hop bytes taken as
+    int64 words, computed on the device."""
+    import hashlib
+    words = out.numel() // 8
+    weights = (torch.arange(words, dtype=torch.int64, device=out.device) * 0x9E3779B97F4A7C1 + 0x632BE5AB) | 1
+    mine = {}
+    for c in range(c0, c0 + nc):
+        gen.run(c * chunk, chunk, addrs, stream)
+        fdev.lookup_batch(addrs, out, stream)
+        w = out[: words * 8].view(torch.int64)
+        mine[c] = int((w * weights).sum().item())
+    if dist is not None:
+        parts = [None] * dist.get_world_size()
+        dist.all_gather_object(parts, mine)
+        for part in parts:
+            mine.update(part)
+    h = hashlib.sha256()
+    for c in sorted(mine):
+        h.update(c.to_bytes(8, "little") + (mine[c] & (2**64 - 1)).to_bytes(8, "little"))
+    return {"sha256": h.hexdigest(), "chunks": len(mine)}
+
+
 def gather_per_rank(ms, dist):
     """Every rank's summed device time of the timed steps (rank order), for the
     balance check in multi-GPU lines; [ms] at one rank."""
@@ -524,6 +548,9 @@ def run_chunked(args, lpm, dispatch, fdev, fib, info, geom, cfg, ws, rank, dev_i
     total_ms = dispatch.max_over_ranks(sum(step_ms), dist, "cuda")
     per_rank_ms = gather_per_rank(sum(step_ms), dist)
     value = info.n_queries * args.steps / (total_ms * 1e-3) / 1e9
+    # Output digest (untimed pass): a hash of every chunk's next hops, combined in chunk
+    # order over all ranks — identical for every GPU count if sharding changes nothing.
+    digest = output_digest(torch, gen, fdev, addrs, out, c0, nc, chunk, stream, dist)
     parity = None
     if rank == 0:  # CPU-baseline leg: the oracle checks a sample of chunk c0's output
         gen.run(c0 * chunk, 1 << 20, addrs, stream)
@@ -561,6 +588,7 @@ def run_chunked(args, lpm, dispatch, fdev, fib, info, geom, cfg, ws, rank, dev_i
         "clocks": clk.summary(), "parity_sample": parity,
         "fib_build_ms": build_ms, "fib_build_device_ms": device_build_ms(lpm, fib, dev_index, vb),
         "fib_broadcast_ms": bcast_ms, "step_ms": step_ms, "per_rank_total_ms": per_rank_ms,
+        "output_digest": digest,
     }
     if ws > 1 and shared_gpu_mode():
         line["harness_check"] = "LPM6_BENCH_SHARED_GPU: ranks shared GPUs over gloo; not a bench value"
