@@ -459,14 +459,11 @@ def output_digest(torch, gen, fdev, addrs, out, c0, nc, chunk, stream, dist):
     hash is a position-weighted wrapping sum of the chunk's next-hop bytes taken as
     int64 words, computed on the device."""
     import hashlib
-    words = out.numel() // 8
-    weights = (torch.arange(words, dtype=torch.int64, device=out.device) * 0x9E3779B97F4A7C1 + 0x632BE5AB) | 1
     mine = {}
     for c in range(c0, c0 + nc):
         gen.run(c * chunk, chunk, addrs, stream)
         fdev.lookup_batch(addrs, out, stream)
-        w = out[: words * 8].view(torch.int64)
-        mine[c] = int((w * weights).sum().item())
+        mine[c] = chunk_hash(torch, out)
     if dist is not None:
         parts = [None] * dist.get_world_size()
         dist.all_gather_object(parts, mine)
@@ -476,6 +473,22 @@ def output_digest(torch, gen, fdev, addrs, out, c0, nc, chunk, stream, dist):
     for c in sorted(mine):
         h.update(c.to_bytes(8, "little") + (mine[c] & (2**64 - 1)).to_bytes(8, "little"))
     return {"sha256": h.hexdigest(), "chunks": len(mine)}
+
+
+def chunk_hash(torch, out):
+    """Position-weighted wrapping int64 sum of a result buffer's 8-byte words (device)."""
+    words = out.numel() // 8
+    weights = (torch.arange(words, dtype=torch.int64, device=out.device) * 0x9E3779B97F4A7C1 + 0x632BE5AB) | 1
+    return int((out[: words * 8].view(torch.int64) * weights).sum().item()) & (2**64 - 1)
+
+
+def gather_block_hashes(torch, out, dist):
+    h = f"{chunk_hash(torch, out):016x}"
+    if dist is None:
+        return [h]
+    parts = [None] * dist.get_world_size()
+    dist.all_gather_object(parts, h)
+    return parts
 
 
 def gather_per_rank(ms, dist):
@@ -695,6 +708,8 @@ def main():
     step_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
     total_ms = dispatch.max_over_ranks(sum(step_ms), dist, "cuda")
     per_rank_ms = gather_per_rank(sum(step_ms), dist)
+    # Rank r always resolves queries [r*n, (r+1)*n): its block's hash is the same at any GPU count.
+    block_hashes = gather_block_hashes(torch, out, dist)
     ms_per_step = total_ms / args.steps
     value = ws * n * args.steps / (total_ms * 1e-3) / 1e9  # aggregate G lookups/s
     lps_gpu = n / (ms_per_step * 1e-3)
@@ -828,6 +843,8 @@ def main():
         "step_ms": step_ms,
         "ms_per_step_median": float(np.median(step_ms)),
         "per_rank_total_ms": per_rank_ms,
+        "output_digest": {"per_rank_block_hash": block_hashes,
+                          "note": "rank r's block = queries [r*n, (r+1)*n); equal across GPU counts"},
     }
     if sweep is not None:
         line["sweep"] = sweep
