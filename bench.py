@@ -2,10 +2,12 @@
 """bench.py — batched IPv6 LPM throughput on B200 (BASELINE.json metric).
 
 A step = one pass of the lookup over one batch of synthetic queries (default:
-workload C1 = the 200K-prefix backbone FIB and 268,435,456 queries per GPU,
-BASELINE.json configs[1]). Prints ONE JSON line (rank 0).
+workload C2 = the 1M-prefix projected FIB, 1,073,741,824 queries per GPU and
+16-bit next hops, BASELINE.json configs[2] — the largest configuration that fits
+one GPU; BASELINE quotes its metric on no single config). Prints ONE JSON line
+(rank 0).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C1]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2]
   python bench.py --impl reference ...   # the reference's CPU lookup on host cores
 
 Multi-GPU (N > 1) is launched by torchrun: rank 0 builds the FIB on the host,
@@ -41,7 +43,9 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", default="C1")
+    ap.add_argument("--workload", default="C2",
+                    help="BASELINE config: C0..C4; default C2, the largest single-GPU config (1M-prefix FIB, "
+                         "1,073,741,824 queries, 16-bit next hops)")
     ap.add_argument("--lanes", type=int, default=0, help="lanes per query (4/8/16), 0 = auto")
     ap.add_argument("--smem-levels", type=int, default=None, help="levels staged in smem, default auto")
     ap.add_argument("--ctas-per-sm", type=int, default=0)
@@ -341,37 +345,24 @@ def cpu_model():
     return f"{name}, {os.cpu_count()} CPUs, avx512f {'yes' if avx512 else 'no'}"
 
 
-def reference_sample(lpm, workload, n):
-    info = lpm.workload_info(workload)
-    fib = lpm.workload_fib(info.fib_kind)
-    addrs = lpm.workload_queries_host(workload, fib, 0, n, threads=cpu_threads())
-    return info, fib, addrs
-
-
 def time_reference_cpu(fib, addrs, threads, repeats=1):
     """The reference's own lpm6::lookup_interval_oracle (oracle/_ref, intervals.cpp:142-145)
-    on `threads` std::threads, or the C restatement when _ref was not built."""
-    from oracle.oracle import REF_SO, Oracle, RefOracle
+    on `threads` std::threads over one shared IntervalMap (SURVEY §8d baseline A). No
+    fallback: without oracle/_ref (built from /root/reference) this raises."""
+    from oracle.oracle import REF_SO, RefOracle
+    if not REF_SO.exists():
+        raise FileNotFoundError(f"{REF_SO} is not built; build() compiles it from /root/reference")
     keys = np.ascontiguousarray(addrs[:, 1])
-    if REF_SO.exists():
-        r = RefOracle()
-        st, rmap = r.build_intervals(fib.rules, fib.default_next_hop)
-        assert st == 0, r.error()
-        rmap.lookup(keys[: 1 << 16], threads)  # warm-up
-        times = []
-        for _ in range(repeats):
-            t0 = time.perf_counter()
-            rmap.lookup(keys, threads)
-            times.append(time.perf_counter() - t0)
-        return times, "reference", "oracle/_ref lpm6::lookup_interval_oracle (reference fib.cpp+intervals.cpp)"
-    o = Oracle()
-    st, b, nh = o.build_intervals(fib.rules, fib.default_next_hop)
+    r = RefOracle()
+    st, rmap = r.build_intervals(fib.rules, fib.default_next_hop)
+    assert st == 0, r.error()
+    rmap.lookup(keys[: 1 << 16], threads)  # warm-up
     times = []
     for _ in range(repeats):
         t0 = time.perf_counter()
-        o.lookup_batch(0, b, nh, addrs, threads)
+        rmap.lookup(keys, threads)
         times.append(time.perf_counter() - t0)
-    return times, "port", "oracle/lpm6_oracle.c orc_lookup_interval (restatement)"
+    return times, "reference", "oracle/_ref lpm6::lookup_interval_oracle (reference fib.cpp+intervals.cpp)"
 
 
 def oracle_check(fib, host_addrs, gpu_out, vb, threads, extra=None):
@@ -420,36 +411,85 @@ def single_thread_baselines(fib, addrs, n1=1 << 22):
     return out
 
 
+def shared_config(info, fib_len, n_per_gpu, ws):
+    """The `config` object of both arms (identical keys and values for the same
+    workload and GPU count; each arm's own details live outside it)."""
+    if info.chunk and n_per_gpu == info.n_queries:
+        return {"workload": info.name, "fib_prefixes": fib_len, "queries_total": info.n_queries,
+                "chunk": info.chunk, "value_bytes": info.value_bytes, "parallelism": f"dp{ws}",
+                "scaling": "strong"}
+    return {"workload": info.name, "fib_prefixes": fib_len, "queries_per_gpu": n_per_gpu,
+            "value_bytes": info.value_bytes, "parallelism": f"dp{ws}", "scaling": "weak"}
+
+
+def product_mapped():
+    """Product-library mappings of this process (the reference arm must have none)."""
+    try:
+        return sorted({ln.split()[-1] for ln in open("/proc/self/maps")
+                       if "paper_2604_14650_b200" in ln or "liblpm6cu" in ln})
+    except OSError:
+        return []
+
+
 def run_reference(args):
+    """--impl reference: the reference's own CPU lookup (lookup_interval_oracle from
+    oracle/_ref, compiled from /root/reference's fib.cpp + intervals.cpp) on every host
+    thread, over the same workload and config as our arm. Each step looks up a bounded,
+    different slice of the workload's query stream (CPU_SAMPLE queries: slice i of the
+    stream for step i), generated before its timer starts. The FIB and queries come
+    from oracle/liblpm6work.so (our generator compiled alone), so this process never
+    maps the product library; rank 0 alone runs under torchrun."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    import paper_2604_14650_b200 as lpm
+    from oracle.oracle import REF_SO, RefOracle
+    from oracle.workload import Workloads
+    if not REF_SO.exists():
+        raise FileNotFoundError(f"{REF_SO} is not built; build() compiles it from /root/reference")
+    wl = Workloads()
     threads = cpu_threads()
-    info, fib, addrs = reference_sample(lpm, args.workload, CPU_SAMPLE)
-    n = len(addrs)
-    times, kind, what = time_reference_cpu(fib, addrs, threads, repeats=args.warmup + args.steps)
-    timed = times[args.warmup:]
-    total = sum(timed)
-    value = n * len(timed) / total / 1e9
+    info = wl.info(args.workload)
+    fib = wl.fib(info.fib_kind)
+    n_full = args.queries or info.n_queries
+    sample = min(n_full, CPU_SAMPLE)
+    r = RefOracle()
+    t0 = time.perf_counter()
+    st, rmap = r.build_intervals(fib.rules, fib.default_next_hop)
+    build_s = time.perf_counter() - t0
+    assert st == 0, r.error()
+    step_s = []
+    first_q = wl.queries(args.workload, fib, 0, 1 << 16, threads)
+    rmap.lookup(np.ascontiguousarray(first_q[:, 1]), threads)  # warm-up pass (S:470)
+    for i in range(args.warmup + args.steps):
+        first = (i * sample) % max(n_full - sample + 1, 1)
+        keys = np.ascontiguousarray(wl.queries(args.workload, fib, first, sample, threads)[:, 1])
+        t0 = time.perf_counter()
+        rmap.lookup(keys, threads)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            step_s.append(dt)
+    total = sum(step_s)
+    value = sample * len(step_s) / total / 1e9
+    mapped = product_mapped()
+    assert not mapped, f"reference arm mapped the product library: {mapped}"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": total / len(timed) * 1e3, "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": total / len(step_s) * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64", "impl": "reference",
-        "data": f"synthetic seeded {info.name} workload, first {n} queries per step (bounded CPU sample)",
-        "config": {"workload": info.name, "fib_prefixes": len(fib), "queries_per_step": n,
-                   "full_workload_queries": info.n_queries},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"{n} queries of {info.name} per step", "what": what, "cpu": cpu_model()},
+        "data": f"synthetic seeded {info.name} workload (oracle/liblpm6work.so, bit-identical to our arm's "
+                f"generator); step i looks up queries [i*{sample}, (i+1)*{sample}) of the stream",
+        "config": shared_config(info, len(fib), n_full, args.gpus),
+        "sample": {"queries_per_step": sample, "of_workload_queries": n_full,
+                   "why": "bounded CPU sample per step so the run ends within minutes"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{sample} queries of {info.name} per step ({len(step_s)} steps)",
+                         "what": "oracle/_ref lpm6::lookup_interval_oracle (reference fib.cpp+intervals.cpp)",
+                         "cpu": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "build_intervals_ms": build_s * 1e3,
+        "step_ms": [x * 1e3 for x in step_s],
+        "product_library_mapped": mapped,
     }
-    try:
-        dt, variant = time_restated_planb(fib, addrs, threads)
-        line["restated_planb_cpu"] = {"value": n / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
-                                      "variant": variant, "sample": f"{n} queries"}
-    except Exception as e:  # the restatement is extra context only
-        line["restated_planb_cpu"] = {"error": str(e)}
-    line["single_thread"] = single_thread_baselines(fib, addrs)
     print(json.dumps(line), flush=True)
     return 0
 
@@ -585,11 +625,11 @@ def run_chunked(args, lpm, dispatch, fdev, fib, info, geom, cfg, ws, rank, dev_i
         "dtype": "u64",
         "data": f"synthetic: seeded {info.name} FIB ({len(fib)} prefixes); {info.n_queries} queries in "
                 f"{total_chunks} chunks of {chunk}, chunk c seeded by c, generated on device (untimed)",
-        "config": {"workload": info.name, "fib_prefixes": len(fib), "intervals": geom.num_keys,
-                   "tree_depth": geom.depth, "queries_total": info.n_queries, "chunk": chunk,
-                   "chunks_per_gpu": nc, "value_bytes": vb, "kernel": cfg,
-                   "l2_flush": f"not needed: each chunk streams {chunk * 16 / 1e9:.1f} GB of addresses",
-                   "parallelism": f"dp{ws} (contiguous chunk ranges; FIB replicated by NCCL broadcast)"},
+        "config": shared_config(info, len(fib), info.n_queries, ws),
+        "layout": {"intervals": geom.num_keys, "tree_depth": geom.depth, "chunks_per_gpu": nc,
+                   "sharding": "contiguous chunk ranges; FIB replicated by NCCL broadcast"},
+        "kernel": cfg,
+        "l2_flush": f"not needed: each chunk streams {chunk * 16 / 1e9:.1f} GB of addresses (> 126 MB L2)",
         "roofline": {"bound": rl["bound"], "achieved": lps_gpu * bpq / 1e9, "peak": peak, "unit": "GB/s",
                      "frac": lps_gpu * bpq / 1e9 / peak, "traffic": measured_traffic(info.name, chunk),
                      "lps_achieved_per_gpu": lps_gpu / 1e9,
@@ -817,12 +857,12 @@ def main():
         "dtype": "u64",
         "data": f"synthetic: seeded {info.name} FIB ({len(fib)} prefixes) and query generator, "
                 f"{n} queries per GPU generated on device",
-        "config": {"workload": info.name, "fib_prefixes": len(fib), "intervals": geom.num_keys,
-                   "tree_depth": geom.depth, "node_keys": geom.k, "leaf_keys": geom.leaf_keys,
-                   "tree_bytes": tree_bytes,
-                   "queries_per_gpu": n, "value_bytes": vb, "kernel": cfg,
-                   "l2_flush": f"not needed: each step streams {n * 16 / 1e9:.1f} GB of addresses (> 126 MB L2)",
-                   "parallelism": f"dp{ws} (query batches; FIB replicated by NCCL broadcast)"},
+        "config": shared_config(info, len(fib), n, ws),
+        "layout": {"intervals": geom.num_keys, "tree_depth": geom.depth, "node_keys": geom.k,
+                   "leaf_keys": geom.leaf_keys, "tree_bytes": tree_bytes,
+                   "sharding": "query batches; FIB replicated by NCCL broadcast"},
+        "kernel": cfg,
+        "l2_flush": f"not needed: each step streams {n * 16 / 1e9:.1f} GB of addresses (> 126 MB L2)",
         "roofline": {"bound": rl["bound"], "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": measured_traffic(info.name, n),
                      "lps_achieved_per_gpu": lps_gpu / 1e9, "lps_roofline_per_gpu": rl["lps"] / 1e9,

@@ -49,6 +49,12 @@ using namespace lpm6::kern;
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
+// Phase B node ranking: 1 = lane-local packed counts + XOR shuffles (group_ranks),
+// 0 = one ballot + popc per key slot (group_rank). Build-time switch for A/B runs.
+#ifndef LPM6_RANK_MODE
+#define LPM6_RANK_MODE 1
+#endif
+
 // ---- PTX helpers ------------------------------------------------------------
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -239,6 +245,41 @@ __device__ __forceinline__ unsigned group_rank(unsigned long long q, const unsig
 #pragma unroll
   for (int t = 0; t < 4; ++t) r += __popc(__ballot_sync(kFull, (t < static_cast<int>(nvalid)) && q >= w[t]) & gmask);
   return r;
+}
+
+// Phase B ranks of all NS queries a 4-lane group carries, without ballots: each
+// lane counts its own keys <= q per query into one byte of a packed counter
+// (query s -> byte s % 4 of acc[s / 4]; a count is at most 16), then two XOR
+// shuffles inside the 4-lane group sum the four lanes' bytes. Per compare this is
+// a 64-bit setp and one predicated add (3 SASS instructions) against the
+// ballot form's compare + VOTE + LOP + POPC + add (6); the reduction costs two
+// SHFL + two adds per four queries. Lane j's key slots t < 2 / t >= 2 count only
+// when lo / hi is all-ones (leaf lines: slots past kL hold next hops, not keys).
+template <int NS, bool MASKED>
+__device__ __forceinline__ void group_ranks(const unsigned long long (&qk)[NS], const unsigned long long (&w)[NS][4],
+                                            unsigned lo, unsigned hi, unsigned (&r)[NS]) {
+  constexpr int NA = (NS + 3) / 4;
+  unsigned acc[NA], acc_hi[NA];
+#pragma unroll
+  for (int a = 0; a < NA; ++a) acc[a] = acc_hi[a] = 0u;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      unsigned& dst = (MASKED && t >= 2) ? acc_hi[s / 4] : acc[s / 4];
+      asm("{\n\t.reg .pred p;\n\tsetp.ge.u64 p, %1, %2;\n\t@p add.u32 %0, %0, %3;\n\t}"
+          : "+r"(dst)
+          : "l"(qk[s]), "l"(w[s][t]), "r"(1u << (8 * (s % 4))));
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < NA; ++a) {
+    if (MASKED) acc[a] = (acc[a] & lo) + (acc_hi[a] & hi);
+    acc[a] += __shfl_xor_sync(kFull, acc[a], 1);
+    acc[a] += __shfl_xor_sync(kFull, acc[a], 2);
+  }
+#pragma unroll
+  for (int s = 0; s < NS; ++s) r[s] = __byte_perm(acc[s / 4], 0u, 0x4440u | (s % 4));
 }
 
 template <int VB>
@@ -487,8 +528,17 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
         for (int t = 0; t < TILES; ++t)
           if ((st * TILES + t) * 32ull + lane < p.n) ++visits;
       }
+#if LPM6_RANK_MODE == 1
+      {
+        unsigned r[NS];
+        group_ranks<NS, false>(qk, w, ~0u, ~0u, r);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) nd[s] = nd[s] * 16u + r[s];
+      }
+#else
 #pragma unroll
       for (int s = 0; s < NS; ++s) nd[s] = nd[s] * 16u + group_rank(qk[s], w[s], 4u, gmask);
+#endif
     }
     unsigned leafn[INPUT == kInKeyOrd ? NS : 1];  // kInKeyOrd: leaf node of each query
     {  // the leaf line: ordinal = rank - 1
@@ -519,12 +569,24 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
         for (int t = 0; t < TILES; ++t)
           if ((st * TILES + t) * 32ull + lane < p.n) ++visits;
       }
+#if LPM6_RANK_MODE == 1
+      {
+        unsigned r[NS];
+        group_ranks<NS, true>(qk, w, leaf_valid >= 2 ? ~0u : 0u, leaf_valid >= 4 ? ~0u : 0u, r);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          if (CHECKED && r[s] == 0) violations |= 4u;
+          nd[s] = CHECKED && r[s] == 0 ? 0u : r[s] - 1u;
+        }
+      }
+#else
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
         const unsigned r = group_rank(qk[s], w[s], leaf_valid, gmask);
         if (CHECKED && r == 0) violations |= 4u;
         nd[s] = CHECKED && r == 0 ? 0u : r - 1u;
       }
+#endif
     }
 
     if constexpr (INPUT == kInKeyOrd) {  // lane j stores the ordinal of its own query (4t + j of the group)

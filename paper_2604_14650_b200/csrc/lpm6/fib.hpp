@@ -3,11 +3,11 @@
 // Mirrors the reference's fib-model surface (fib.hpp:17-121) that a caller of
 // the batched lookup needs: Prefix (same memory layout as lpm6::Prefix,
 // fib.hpp:22-29, so a reference FibTable's entries can be handed over as-is),
-// prefix_to_range (fib.cpp:66-70), parse_prefix / load_fib (fib.cpp:72-195) and
-// FibTable (fib.hpp:74-105).
+// prefix_to_range (fib.cpp:66-70), parse_prefix (fib.cpp:72-105) and FibTable
+// (fib.hpp:74-105). Text FIB files are read by the caller (the reference's own
+// load_fib, or fib.py's load_fib over parse_prefix).
 #pragma once
 
-#include <istream>
 #include <string>
 #include <string_view>
 #include <unordered_map>
@@ -79,13 +79,5 @@ class FibTable {
   std::unordered_map<std::pair<u64, int>, size_t, KeyHash> index_;
   u32 default_next_hop_ = 0;
 };
-
-struct LoadStats {
-  u64 lines = 0, rules = 0, duplicates = 0, masked = 0, too_long = 0;
-};
-
-// Text FIB: '#' comments, blank lines ignored, last duplicate wins, /65+ counted and
-// skipped (fib.cpp:165-195).
-FibTable load_fib(std::istream& in, LoadStats* stats = nullptr);
 
 }  // namespace lpm6

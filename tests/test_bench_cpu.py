@@ -27,6 +27,14 @@ def test_reference_arm_json_line():
     assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["value"] == d["value"]
     assert "sample" in cb
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    # the reference arm never maps the product library, and its config is our arm's
+    assert d["product_library_mapped"] == []
+    assert cb["kind"] == "reference"
+    sys.path.insert(0, str(ROOT))
+    import bench
+    from oracle.workload import Workloads
+    info = Workloads().info("C0")
+    assert d["config"] == bench.shared_config(info, 1001, info.n_queries, 1)
 
 
 def test_reference_arm_other_ranks_exit_quietly():

@@ -114,3 +114,87 @@ def test_update_parser_never_crashes(lpm, line):
         assert e.code in ("MalformedAddress", "UnsupportedPrefixLength", "MissingNextHop", "ReservedNextHop")
         return
     assert op.kind in (store.ANNOUNCE, store.DELETE) and 0 <= op.prefix.length <= 64
+
+
+# ---- rule text: our parser against libc inet_pton (the reference's parser, fib.cpp:47) ----
+
+_HEX = "0123456789abcdefABCDEF"
+
+
+@st.composite
+def address_texts(draw):
+    """Valid RFC 4291 forms (full, '::'-compressed, embedded dotted quads) and near-misses."""
+    groups = [draw(st.integers(0, 0xFFFF)) for _ in range(8)]
+    style = draw(st.integers(0, 5))
+    g = [format(x, "x") if draw(st.booleans()) else format(x, "04X") for x in groups]
+    if style == 0:
+        return ":".join(g)
+    if style == 1:  # compress a run
+        a = draw(st.integers(0, 8))
+        b = draw(st.integers(a, 8))
+        return ":".join(g[:a]) + "::" + ":".join(g[b:])
+    if style == 2:  # dotted-quad tail
+        quad = ".".join(str(draw(st.integers(0, 255))) for _ in range(4))
+        if draw(st.booleans()):
+            return ":".join(g[:6]) + ":" + quad
+        a = draw(st.integers(0, 6))
+        return ":".join(g[:a]) + "::" + quad
+    # near-misses: random short strings over the address alphabet
+    return draw(st.text(alphabet=_HEX + ":.x/ ", min_size=0, max_size=20))
+
+
+@SETTINGS
+@given(text=address_texts(), length=st.integers(0, 130), hop=st.integers(0, (1 << 32) + 5))
+def test_parse_prefix_matches_inet_pton(lpm, text, length, hop):
+    """lpm6_parse_prefix accepts exactly the addresses libc's inet_pton accepts (the
+    reference parses with inet_pton, fib.cpp:47) and yields the same 128-bit value."""
+    import socket
+    try:
+        raw = socket.inet_pton(socket.AF_INET6, text)
+    except (OSError, ValueError):
+        raw = None
+    rule = f"{text}/{length} {hop}"
+    if raw is None or " " in text or "/" in text or text == "":
+        if raw is None:
+            with pytest.raises(lpm.Lpm6Error):
+                lpm.parse_prefix(rule)
+        return
+    value = int.from_bytes(raw, "big")
+    if length > 128:
+        with pytest.raises(lpm.Lpm6Error) as e:
+            lpm.parse_prefix(rule)
+        assert e.value.code == "MalformedAddress"
+        return
+    if length > 64:
+        with pytest.raises(lpm.Lpm6Error) as e:
+            lpm.parse_prefix(rule)
+        assert e.value.code == "UnsupportedPrefixLength"
+        return
+    if hop > 0xFFFFFFFF:
+        with pytest.raises(lpm.Lpm6Error) as e:
+            lpm.parse_prefix(rule)
+        assert e.value.code == "MissingNextHop"
+        return
+    if hop == 0xFFFFFFFF:
+        with pytest.raises(lpm.Lpm6Error) as e:
+            lpm.parse_prefix(rule)
+        assert e.value.code == "ReservedNextHop"
+        return
+    p, masked = lpm.parse_prefix(rule)
+    keep = ((1 << 128) - 1) ^ ((1 << (128 - length)) - 1)
+    assert p.value == value & keep and p.length == length and p.next_hop == hop
+    assert masked == ((value & keep) != value)
+
+
+@pytest.mark.parametrize("text", ["2001:db8::/32 1", "::/0 7", "::ffff:10.0.0.1/64 9", "1:2:3:4:5:6:7::/48 2",
+                                  "::1:2:3:4:5:6:7/64 3", "2001:DB8:0:0:1::/64 5"])
+def test_parse_prefix_matches_reference(lpm, ref, text):
+    """Against the reference's own parse_prefix (oracle/_ref, fib.cpp:72-105)."""
+    import ctypes
+    buf = np.zeros(1, lpm.fib.PREFIX_DTYPE)
+    masked = ctypes.c_int(0)
+    st_ = ref.L.ref_parse_prefix(text.encode(), buf.ctypes.data, ctypes.byref(masked))
+    assert st_ == 0
+    p, m = lpm.parse_prefix(text)
+    assert p.value == (int(buf["value_hi"][0]) << 64 | int(buf["value_lo"][0]))
+    assert p.length == int(buf["length"][0]) and p.next_hop == int(buf["next_hop"][0]) and m == bool(masked.value)
