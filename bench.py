@@ -495,35 +495,21 @@ def run_reference(args):
 
 
 def output_digest(torch, gen, fdev, addrs, out, c0, nc, chunk, stream, dist):
-    """sha256 over (chunk index, per-chunk hash) for all chunks in order; the per-chunk
-    hash is a position-weighted wrapping sum of the chunk's next-hop bytes taken as
-    int64 words, computed on the device."""
-    import hashlib
+    """sha256 over (chunk index, per-chunk hash) for all chunks in order
+    (dispatch.combine_digests); the per-chunk hash is computed on the device
+    (dispatch.chunk_hash)."""
+    from paper_2604_14650_b200 import dispatch
     mine = {}
     for c in range(c0, c0 + nc):
         gen.run(c * chunk, chunk, addrs, stream)
         fdev.lookup_batch(addrs, out, stream)
-        mine[c] = chunk_hash(torch, out)
-    if dist is not None:
-        parts = [None] * dist.get_world_size()
-        dist.all_gather_object(parts, mine)
-        for part in parts:
-            mine.update(part)
-    h = hashlib.sha256()
-    for c in sorted(mine):
-        h.update(c.to_bytes(8, "little") + (mine[c] & (2**64 - 1)).to_bytes(8, "little"))
-    return {"sha256": h.hexdigest(), "chunks": len(mine)}
-
-
-def chunk_hash(torch, out):
-    """Position-weighted wrapping int64 sum of a result buffer's 8-byte words (device)."""
-    words = out.numel() // 8
-    weights = (torch.arange(words, dtype=torch.int64, device=out.device) * 0x9E3779B97F4A7C1 + 0x632BE5AB) | 1
-    return int((out[: words * 8].view(torch.int64) * weights).sum().item()) & (2**64 - 1)
+        mine[c] = dispatch.chunk_hash(out)
+    return dispatch.combine_digests(mine, dist)
 
 
 def gather_block_hashes(torch, out, dist):
-    h = f"{chunk_hash(torch, out):016x}"
+    from paper_2604_14650_b200 import dispatch
+    h = f"{dispatch.chunk_hash(out):016x}"
     if dist is None:
         return [h]
     parts = [None] * dist.get_world_size()

@@ -331,6 +331,7 @@ typedef struct {
   uint64_t commits;       /* effective commits */
   double last_build_ms;   /* wall time of the last device rebuild */
   double last_publish_us; /* time the active-pointer swap was held */
+  uint64_t fences;        /* outstanding release fences over all snapshots (<= reader streams each) */
 } lpm6cu_store_stats;
 
 typedef struct lpm6cu_store lpm6cu_store;

@@ -68,7 +68,7 @@ class UpdateOp_t(C.Structure):
 class StoreStats_t(C.Structure):
     _fields_ = [("epoch", C.c_uint64), ("pending_ops", C.c_uint64), ("active_rules", C.c_uint64),
                 ("retired", C.c_uint64), ("reclaimed", C.c_uint64), ("commits", C.c_uint64),
-                ("last_build_ms", C.c_double), ("last_publish_us", C.c_double)]
+                ("last_build_ms", C.c_double), ("last_publish_us", C.c_double), ("fences", C.c_uint64)]
 
 
 class Footprint_t(C.Structure):

@@ -258,8 +258,12 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
                                 static_cast<int>(tiles), threads, static_cast<int>(minb), f->d_err != nullptr, input,
                                 leafs, texl_mode, leaftex);
       if (!fn) throw Error(Errc::InvalidArgument, "no kernel instantiated for this configuration");
+      // The attribute belongs to the kernel, which every FIB of this depth and
+      // next-hop width shares: always set it to the device's opt-in maximum, never
+      // to this FIB's own image size, so that no FIB can lower it under another.
       if (smem > 48 * 1024)
-        check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+        check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(f->max_smem_optin)),
                    "cudaFuncSetAttribute");
       int per_sm = 0;
       check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem), "occupancy");
@@ -295,6 +299,12 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
   p.err = f->d_err;
   std::memcpy(p.root, f->root, sizeof p.root);
   p.tex = f->tex;
+  {
+    auto off = [&](unsigned l) { return static_cast<unsigned>((f->g.level_start[l] / kLineWords) * kNodeKeys * 8); };
+    const unsigned ta = p.smem_levels;
+    p.img_step[0] = ta >= 2 ? off(1) : 0u;
+    for (unsigned l = 1; l < ta; ++l) p.img_step[l] = l + 1 < ta ? off(l + 1) - 16u * off(l) : 0u - 16u * off(l);
+  }
   const unsigned long long ntiles = (n + 32ull * tiles - 1) / (32ull * tiles);
   const unsigned long long warps_per_cta = threads / 32;
   unsigned long long grid = static_cast<unsigned long long>(f->num_sms) * plan.per_sm;

@@ -227,7 +227,7 @@ __device__ __forceinline__ unsigned node_rank_smem(const unsigned long long* lvl
 // Returns the byte offset of the final position, 8 * rank.
 __device__ __forceinline__ unsigned node_rank_saddr(uint32_t a, unsigned long long q) {
   const uint32_t a0 = a;
-  asm("{\n\t.reg .pred p;\n\t.reg .b64 k;\n\t"
+  asm volatile("{\n\t.reg .pred p;\n\t.reg .b64 k;\n\t"
       "ld.shared.u64 k, [%0+56];\n\tsetp.le.u64 p, k, %1;\n\t@p add.u32 %0, %0, 64;\n\t"
       "ld.shared.u64 k, [%0+24];\n\tsetp.le.u64 p, k, %1;\n\t@p add.u32 %0, %0, 32;\n\t"
       "ld.shared.u64 k, [%0+8];\n\tsetp.le.u64 p, k, %1;\n\t@p add.u32 %0, %0, 16;\n\t"
@@ -289,14 +289,29 @@ struct LeafFmt {
   static constexpr int kValueOff = kL * 8 - kValueLane * 32;   // their byte offset in that lane's 32 B
 };
 
+__device__ __forceinline__ unsigned long long sel64(bool p, unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\tselp.b64 %0, %1, %2, q;\n\t}"
+      : "=l"(r)
+      : "l"(a), "l"(b), "r"(static_cast<unsigned>(p)));
+  return r;
+}
+
+// Next hop of leaf ordinal `ord` from the value lane's 32 bytes: a branch-free
+// select of the 8-byte word holding it (only the words the value bytes occupy
+// are candidates) and one funnel shift. Values never straddle a word.
 template <int VB>
 __device__ __forceinline__ unsigned leaf_value(const unsigned long long (&w)[4], unsigned ord) {
-  const unsigned o = LeafFmt<VB>::kValueOff + ord * VB;  // byte offset within the lane's quarter
+  constexpr unsigned kOff = LeafFmt<VB>::kValueOff;
+  constexpr unsigned kFirst = kOff / 8;
+  constexpr unsigned kLast = (kOff + LeafFmt<VB>::kL * VB - 1) / 8;
+  const unsigned o = kOff + ord * VB;  // byte offset within the lane's quarter
   const unsigned wi = o >> 3;
-  const unsigned long long x = wi == 0 ? w[0] : wi == 1 ? w[1] : wi == 2 ? w[2] : w[3];
-  const unsigned long long v = x >> ((o & 7u) * 8u);
-  return VB == 1 ? static_cast<unsigned>(v & 0xFFu) : VB == 2 ? static_cast<unsigned>(v & 0xFFFFu)
-                                                              : static_cast<unsigned>(v & 0xFFFFFFFFu);
+  unsigned long long x = w[kFirst];
+#pragma unroll
+  for (unsigned i = kFirst + 1; i <= kLast; ++i) x = sel64(wi == i, w[i], x);
+  const unsigned v = static_cast<unsigned>(x >> ((o & 7u) * 8u));
+  return VB == 1 ? (v & 0xFFu) : VB == 2 ? (v & 0xFFFFu) : v;
 }
 
 template <int VB>
@@ -434,6 +449,40 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
     }
 
     // Phase A: this thread's own queries through the shared-memory levels.
+    if constexpr (!CHECKED) {
+      // As a walk over shared-memory byte addresses: with a = the address of node
+      // n of level l and a' = a + 8 * rank after the four probes, the child's
+      // address in level l + 1 is img(l+1) + (16 n + rank) * 120 =
+      // a + 15 a' + (img(l+1) - 16 img(l)) — one IMAD and one add per level (the
+      // constants come with the launch, LookupParams::img_step); after the last
+      // staged level the same step with img(l+1) := 0 leaves s_base + 120 x the
+      // child's node index (an exact division by 120 recovers it).
+#pragma unroll
+      for (int t = 0; t < TILES; ++t) {
+        if (TA == 0) break;
+        const unsigned long long q = key[t];
+        // Root from the kernel-parameter constant bank: all lanes start at the
+        // same node, so the probes are (nearly) uniform LDCs and keep the
+        // shared-memory data pipe free for the deeper levels.
+        unsigned c = (p.root[7] <= q) ? 8u : 0u;
+        c |= (p.root[c | 3u] <= q) ? 4u : 0u;
+        c |= (p.root[c | 1u] <= q) ? 2u : 0u;
+        c |= (p.root[c] <= q) ? 1u : 0u;
+        if (TA == 1) {
+          node[t] = c;
+          continue;
+        }
+        uint32_t a = s_base + p.img_step[0] + c * 120u;
+#pragma unroll
+        for (int l = 1; l < DEPTH; ++l) {
+          if (static_cast<unsigned>(l) >= TA) break;
+          const uint32_t af = a + node_rank_saddr(a, q);
+          a = a + 15u * af + (p.img_step[l] - 15u * s_base);  // img_step: see LookupParams
+        }
+        // a - s_base = 120 x node: exact division (0xEEEEEEEF = 15^-1 mod 2^32)
+        node[t] = ((a - s_base) >> 3) * 0xEEEEEEEFu;
+      }
+    } else
 #pragma unroll
     for (int l = 0; l < DEPTH; ++l)
       if (static_cast<unsigned>(l) < TA) {

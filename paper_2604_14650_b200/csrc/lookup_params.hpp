@@ -34,6 +34,10 @@ struct LookupParams {
   unsigned int* err;         // checked mode: OR of violation bits (1 smem level, 2 line level, 4 leaf rank)
   unsigned long long root[16];  // the root's 15 separators (+ sentinel), read from the constant bank
   unsigned long long tex;       // texture object over the line array (int4 texels), 0 = none
+  // Phase A address walk (lookup_kernel.cuh), with off(l) = byte offset of level l
+  // in the shared-memory image: img_step[0] = off(1); img_step[l] = off(l+1) -
+  // 16 off(l) for 1 <= l < smem_levels - 1; img_step[smem_levels - 1] = -16 off(l).
+  unsigned int img_step[LPM6CU_MAX_LEVELS];
 };
 
 using KernelFn = void (*)(const LookupParams);

@@ -98,9 +98,14 @@ struct lpm6cu_snapshot {
   uint64_t epoch = 0;
   lpm6cu_fib* fib = nullptr;
   std::vector<Prefix> rules;
-  // Guarded by store->mu.
+  // Guarded by store->mu. At most one fence per reader stream: events on one
+  // stream complete in order, so a release re-records that stream's fence.
+  struct Fence {
+    cudaStream_t stream;
+    cudaEvent_t event;
+  };
   uint64_t refs = 0;
-  std::vector<cudaEvent_t> fences;
+  std::vector<Fence> fences;
 
   ~lpm6cu_snapshot() {
     if (fib) lpm6cu_fib_destroy(fib);
@@ -125,17 +130,6 @@ struct lpm6cu_store {
   std::vector<cudaEvent_t> event_pool;
   lpm6cu_store_stats stats{};
 
-  cudaEvent_t take_event() {  // under mu
-    if (!event_pool.empty()) {
-      cudaEvent_t e = event_pool.back();
-      event_pool.pop_back();
-      return e;
-    }
-    cudaEvent_t e = nullptr;
-    ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
-    return e;
-  }
-
   // Detach retired snapshots that no reader holds and whose fences completed.
   std::vector<lpm6cu_snapshot*> collect(bool wait) {  // under mu
     std::vector<lpm6cu_snapshot*> dead;
@@ -143,7 +137,7 @@ struct lpm6cu_store {
       lpm6cu_snapshot* s = retired[i];
       bool done = s->refs == 0;
       for (size_t f = 0; done && f < s->fences.size(); ++f) {
-        const cudaError_t q = wait ? cudaEventSynchronize(s->fences[f]) : cudaEventQuery(s->fences[f]);
+        const cudaError_t q = wait ? cudaEventSynchronize(s->fences[f].event) : cudaEventQuery(s->fences[f].event);
         if (q == cudaErrorNotReady) done = false;
         else if (q != cudaSuccess) cudaGetLastError();  // a failed fence cannot become ready; treat as done
       }
@@ -151,7 +145,7 @@ struct lpm6cu_store {
         ++i;
         continue;
       }
-      for (cudaEvent_t e : s->fences) event_pool.push_back(e);
+      for (const auto& f : s->fences) event_pool.push_back(f.event);
       s->fences.clear();
       dead.push_back(s);
       retired[i] = retired.back();
@@ -351,15 +345,38 @@ int lpm6cu_store_release(lpm6cu_snapshot* snap, void* stream) {
     {
       std::lock_guard<std::mutex> lk(s->mu);
       if (snap->refs == 0) throw Error(Errc::InvalidArgument, "snapshot released more often than acquired");
-      cudaEvent_t e = s->take_event();
-      const cudaError_t r = cudaEventRecord(e, static_cast<cudaStream_t>(stream));
-      if (r != cudaSuccess) {
-        s->event_pool.push_back(e);
-        ck(r, "cudaEventRecord (release fence)");
-      }
-      snap->fences.push_back(e);
-      --snap->refs;
+      --snap->refs;  // before anything that can fail: a failed fence must not pin the snapshot
       retired = snap != s->active;
+      const auto st = static_cast<cudaStream_t>(stream);
+      // Recycle fences that have completed; re-record this stream's fence if it has one.
+      bool mine = false;
+      cudaEvent_t e = nullptr;
+      for (size_t i = 0; i < snap->fences.size();) {
+        auto& f = snap->fences[i];
+        if (f.stream == st) {
+          mine = true;
+          e = f.event;
+        } else if (cudaEventQuery(f.event) == cudaSuccess) {
+          s->event_pool.push_back(f.event);
+          f = snap->fences.back();
+          snap->fences.pop_back();
+          continue;
+        }
+        ++i;
+      }
+      cudaGetLastError();  // a query of a failed stream's event reports its error; it stays a fence
+      if (!e) {
+        e = s->event_pool.empty() ? nullptr : s->event_pool.back();
+        if (e) s->event_pool.pop_back();
+        else if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) e = nullptr;
+      }
+      if (!e || cudaEventRecord(e, st) != cudaSuccess) {
+        // No fence available: wait for this reader's stream instead (rare; never unsafe).
+        if (e && !mine) s->event_pool.push_back(e);
+        ck(cudaStreamSynchronize(st), "cudaStreamSynchronize (release without a fence)");
+      } else if (!mine) {
+        snap->fences.push_back({st, e});
+      }
     }
     if (retired) s->reclaim(false);
   });
@@ -409,6 +426,8 @@ int lpm6cu_store_stats_get(lpm6cu_store* s, lpm6cu_store_stats* out) {
     {
       std::lock_guard<std::mutex> lk(s->mu);
       *out = s->stats;
+      out->fences = s->active->fences.size();
+      for (const lpm6cu_snapshot* r : s->retired) out->fences += r->fences.size();
     }
     std::lock_guard<std::mutex> lk(s->stage_mu);
     out->pending_ops = s->pending.size();

@@ -92,3 +92,28 @@ def max_over_ranks(value: float, dist, device=None) -> float:
     t = torch.tensor([value], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def chunk_hash(out) -> int:
+    """Position-weighted wrapping int64 sum of a result buffer's 8-byte words (a torch
+    uint8 tensor, computed where it lives — on the device for GPU results)."""
+    import torch
+    words = out.numel() // 8
+    weights = (torch.arange(words, dtype=torch.int64, device=out.device) * 0x9E3779B97F4A7C1 + 0x632BE5AB) | 1
+    return int((out[: words * 8].view(torch.int64) * weights).sum().item()) & (2**64 - 1)
+
+
+def combine_digests(mine: dict, dist) -> dict:
+    """sha256 over (chunk index, chunk hash) for every chunk of every rank, in chunk
+    order: a checksum of checksums that does not depend on how chunks were sharded."""
+    import hashlib
+    allh = dict(mine)
+    if dist is not None:
+        parts = [None] * dist.get_world_size()
+        dist.all_gather_object(parts, mine)
+        for part in parts:
+            allh.update(part)
+    h = hashlib.sha256()
+    for c in sorted(allh):
+        h.update(int(c).to_bytes(8, "little") + (allh[c] & (2**64 - 1)).to_bytes(8, "little"))
+    return {"sha256": h.hexdigest(), "chunks": len(allh)}

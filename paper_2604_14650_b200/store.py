@@ -139,6 +139,7 @@ class StoreStats:
     commits: int
     last_build_ms: float
     last_publish_us: float
+    fences: int = 0
 
 
 class FibStore:
@@ -190,7 +191,7 @@ class FibStore:
         s = StoreStats_t()
         check(lib().lpm6cu_store_stats_get(self._h, C.byref(s)))
         return StoreStats(s.epoch, s.pending_ops, s.active_rules, s.retired, s.reclaimed, s.commits,
-                          s.last_build_ms, s.last_publish_us)
+                          s.last_build_ms, s.last_publish_us, s.fences)
 
     @property
     def epoch(self) -> int:

@@ -64,3 +64,37 @@ def random_fib_rules(rng, n, dtype, with_default: bool, nest_p: float = 0.3, min
         tops.append((top, ln))
         rules.append((top << 64, ln, int(rng.integers(1, 2**16))))
     return rules_array(rules, dtype)
+
+
+def sha(a: np.ndarray) -> str:
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a).view(np.uint8).tobytes()).hexdigest()
+
+
+def large_fixture_rules(source: str):
+    """Regenerate the rules of a hash-pinned golden fixture (make_golden.make_large)
+    from its recorded source string -> (rules, default next hop)."""
+    from paper_2604_14650_b200.fib import PREFIX_DTYPE
+    kind, _, arg = source.partition(":")
+    if kind == "random_nested":  # random_fib_rules(default_rng(seed), n, ..., with_default=True, nest_p=0.5)
+        n, seed = (int(x) for x in arg.split(","))
+        return random_fib_rules(np.random.default_rng(seed), n, PREFIX_DTYPE, True, nest_p=0.5), 7
+    if kind == "ref_synth":  # the reference's synth_fib(n, seed) (fib.cpp:237-273)
+        import pytest
+        from oracle.oracle import REF_SO, RefOracle
+        if not REF_SO.exists():
+            pytest.skip("oracle/_ref not built: the reference's synth_fib regenerates this fixture")
+        n, seed = (int(x) for x in arg.split(","))
+        return RefOracle().synth_fib(n, seed, PREFIX_DTYPE), 0
+    if kind == "workload":  # our seeded workload FIB (csrc/lpm6/workload.cpp)
+        from oracle.workload import Workloads
+        f = Workloads().fib(int(arg))
+        return f.rules, f.default_next_hop
+    raise ValueError(source)
+
+
+def large_rules(d):
+    """Rules of a loaded large fixture, checked against the recorded sha256."""
+    rules, dflt = large_fixture_rules(str(d["source"]))
+    assert len(rules) == int(d["n_rules"][0]) and sha(rules) == str(d["rules_sha256"]), "fixture rules changed"
+    return rules, dflt

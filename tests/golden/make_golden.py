@@ -22,7 +22,7 @@ ROOT = HERE.parents[1]
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(HERE.parent))
 
-from _util import MASK64, random_fib_rules  # noqa: E402
+from _util import MASK64, large_fixture_rules, random_fib_rules, sha  # noqa: E402
 from oracle.oracle import RefOracle  # noqa: E402
 from paper_2604_14650_b200.fib import PREFIX_DTYPE  # noqa: E402
 
@@ -53,6 +53,34 @@ def make(ref, name, rules, default_nh, rng, n_random=2000, linear=True):
     print(name, len(rules), "rules ->", len(out["boundaries_m1"]), "intervals,", len(out["keys"]), "keys")
 
 
+def make_large(ref, name, rules, default_nh, rng, source, n_interval=60000, n_linear=20000):
+    """Fixtures for FIBs too large to commit: the rules are regenerated at test time
+    from `source` (and checked against their sha256); the reference's interval map is
+    pinned by its size and sha256 (merge on and off), and its answers by sampled keys:
+    boundaries / boundary+-1 / random keys through lookup_interval_oracle, and a
+    subset through the brute-force linear oracle (SPEC S:486 asks 10^5 rules against
+    the linear oracle)."""
+    out = {"source": np.array(source), "rules_sha256": np.array(sha(rules)), "n_rules": np.array([len(rules)]),
+           "default_nh": np.array([default_nh], np.uint32)}
+    for merge in (1, 0):
+        st, m = ref.build_intervals(rules, default_nh, bool(merge))
+        assert st == 0, ref.error()
+        out[f"m_m{merge}"] = np.array([len(m.boundaries)])
+        out[f"boundaries_sha256_m{merge}"] = np.array(sha(m.boundaries))
+        out[f"next_hops_sha256_m{merge}"] = np.array(sha(m.next_hops))
+        if merge:
+            allk = sample_keys(rng, m.boundaries, n_interval // 4)
+            keys = np.unique(rng.choice(allk, size=min(n_interval, len(allk)), replace=False))
+            out["keys"] = keys
+            out["interval_oracle"] = m.lookup(keys, 8)
+            lk = np.unique(rng.choice(keys, size=min(n_linear, len(keys)), replace=False))
+            out["linear_keys"] = lk
+            out["linear_oracle"] = ref.linear_keys(rules, default_nh, lk, 8)
+    np.savez_compressed(HERE / f"{name}.npz", **out)
+    print(name, len(rules), "rules ->", int(out["m_m1"][0]), "intervals,", len(out["keys"]), "keys,",
+          len(out["linear_keys"]), "linear")
+
+
 def main():
     ref = RefOracle()
     rng = np.random.default_rng(20260101)
@@ -67,7 +95,22 @@ def main():
     for n, dflt in ((300, True), (2000, False)):
         rules = random_fib_rules(rng, n, PREFIX_DTYPE, dflt, nest_p=0.5)
         make(ref, f"nested_{n}", rules, 9, rng)
+    # SPEC S:486 acceptance size (10^5 rules) and the deepest tree (the 1M-prefix C2
+    # FIB: depth 5 in the B200 layout, 16-bit next hops)
+    for name, src in (("large_random_nested_100000", "random_nested:100000,100000"),
+                      ("large_ref_synth_100000", "ref_synth:100000,4"),
+                      ("large_workload_c2_fib", "workload:2")):
+        rules, dflt = large_fixture_rules(src)
+        make_large(ref, name, rules, dflt, rng, src)
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["large"]:  # only the large (hash-pinned) fixtures
+        ref_, rng_ = RefOracle(), np.random.default_rng(20261020)
+        for name, src in (("large_random_nested_100000", "random_nested:100000,100000"),
+                          ("large_ref_synth_100000", "ref_synth:100000,4"),
+                          ("large_workload_c2_fib", "workload:2")):
+            r, d = large_fixture_rules(src)
+            make_large(ref_, name, r, d, rng_, src)
+    else:
+        main()

@@ -7,7 +7,7 @@ oracle/_ref is present the reference's own lookup_interval_oracle is checked too
 import numpy as np
 import pytest
 
-from _util import addrs_from_keys, boundary_probe_keys, random_fib_rules
+from _util import addrs_from_keys, boundary_probe_keys, large_rules, random_fib_rules
 
 pytestmark = pytest.mark.gpu
 
@@ -354,7 +354,8 @@ def test_golden_fixtures_on_gpu(lpm, cuda):
     fixture key looked up on the GPU equals the reference's own interval oracle and
     linear (brute-force) oracle, every kernel mode."""
     from pathlib import Path
-    files = sorted((Path(__file__).resolve().parent / "golden").glob("*.npz"))
+    files = sorted(f for f in (Path(__file__).resolve().parent / "golden").glob("*.npz")
+                   if not f.stem.startswith("large_"))
     assert files
     for f in files:
         d = np.load(f)
@@ -449,3 +450,110 @@ print("ABI-OK" if not bad else bad)
     root = Path(__file__).resolve().parents[1]
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ABI-OK" in r.stdout, (r.returncode, r.stdout[-2000:], r.stderr[-3000:])
+
+
+@pytest.mark.parametrize("name", ["large_random_nested_100000", "large_ref_synth_100000", "large_workload_c2_fib"])
+def test_golden_large_fixtures_on_gpu(lpm, cuda, name):
+    """The hash-pinned reference fixtures (SPEC S:486's 10^5 rules; the 1M-prefix C2 FIB,
+    a depth-5 tree with 16-bit next hops): every sampled key's next hop from the GPU
+    equals the reference's own lookup_interval_oracle and linear-oracle answers, at
+    every smem_levels and on every line path, for the host-built and the device-built
+    FIB."""
+    from pathlib import Path
+    d = np.load(Path(__file__).resolve().parent / "golden" / f"{name}.npz")
+    rules, dflt = large_rules(d)
+    fib = lpm.FibTable(dflt, rules)
+    keys = d["keys"].astype(np.uint64)
+    addrs = addrs_from_keys(keys, np.random.default_rng(1))
+    pos = np.searchsorted(d["keys"], d["linear_keys"])
+    for dev in (lpm.Fib.build(fib), lpm.Fib.build_device(fib, 0)):
+        geo = dev.geometry
+        if name == "large_workload_c2_fib":
+            assert geo.depth == 5 and geo.value_bytes == 2
+        for t in [None] + list(range(geo.depth + geo.leaf_image + 1)):
+            for lp in (0, 1, 2, 3):
+                dev.set_kernel_config(smem_levels=t, line_path=lp)
+                got = run_lookup(cuda, dev, addrs).astype(np.uint32)
+                np.testing.assert_array_equal(got, d["interval_oracle"], err_msg=f"{name} T={t} lp={lp}")
+                np.testing.assert_array_equal(got[pos], d["linear_oracle"], err_msg=f"{name} T={t} lp={lp}")
+        dev.close()
+
+
+def test_c2_against_reference_library(lpm, ref, cuda):
+    """2^26 C2 queries (the 1M-prefix FIB, depth 5, 16-bit next hops) looked up on the
+    GPU and by the reference's own build_intervals + lookup_interval_oracle
+    (oracle/_ref, intervals.cpp:33-93,142-145), on every host thread."""
+    import os
+    torch = cuda
+    info = lpm.workload_info("C2")
+    fib = lpm.workload_fib(info.fib_kind)
+    dev = lpm.Fib.build(fib)
+    gen = lpm.QueryGen("C2", fib)
+    n = 1 << 26
+    d = torch.empty((n, 16), dtype=torch.uint8, device="cuda")
+    gen.run(0, n, d)
+    st, rmap = ref.build_intervals(fib.rules, fib.default_next_hop)
+    assert st == 0
+    keys = np.ascontiguousarray(d.cpu().numpy().view(np.uint64).reshape(-1, 2)[:, 1])
+    want = rmap.lookup(keys, os.cpu_count() or 8)
+    got = dev.lookup_batch(d).cpu().numpy().view(np.uint16).astype(np.uint32)
+    assert int(np.count_nonzero(got != want)) == 0
+
+
+@pytest.mark.slow
+def test_c4_every_chunk(lpm, orc, cuda):
+    """C4 in full: all 128 chunks of 64M queries (8,589,934,592 lookups) on the tuned
+    line path, every next hop compared with the oracle (chunk c is seeded by c, so this
+    is exactly the stream bench.py's C4 line and its output digest cover)."""
+    import os
+    torch = cuda
+    info = lpm.workload_info("C4")
+    fib = lpm.workload_fib(info.fib_kind)
+    imap = lpm.build_intervals(fib)
+    dev = lpm.Fib.build(fib)
+    gen = lpm.QueryGen("C4", fib)
+    chunk = info.chunk
+    d = torch.empty((chunk, 16), dtype=torch.uint8, device="cuda")
+    gen.run(0, chunk, d)
+    dev.tune_line_path(d)
+    threads = os.cpu_count() or 8
+    mism = 0
+    for c in range(info.n_queries // chunk):
+        gen.run(c * chunk, chunk, d)
+        got = dev.lookup_batch(d).cpu().numpy().view(np.uint16).astype(np.uint32)
+        host_addrs = d.cpu().numpy().view(np.uint64).reshape(-1, 2)
+        want = oracle_next_hops_threads(orc, imap.boundaries, imap.next_hops, host_addrs, threads)
+        mism += int(np.count_nonzero(got != want))
+    assert mism == 0
+
+
+def oracle_next_hops_threads(orc, b, nh, addrs, threads):
+    out, _ = orc.lookup_batch(0, b, nh, addrs, threads=threads)
+    return out
+
+
+def test_kernel_smem_attribute_shared_across_fibs(lpm, orc, cuda):
+    """FIBs of equal depth and next-hop width share one kernel, whose
+    max-dynamic-shared-memory attribute used to be set to each FIB's own image size. A
+    FIB with a smaller image (> 48 KB) resolving its plan then lowered it under a FIB
+    with a larger one, whose later launches failed. Launch larger, smaller, larger."""
+    from paper_2604_14650_b200.fib import PREFIX_DTYPE
+    rng = np.random.default_rng(77)
+    big = lpm.workload_fib(1)  # C1: depth 4, u8, 221 KB image
+    rules = random_fib_rules(rng, 60000, PREFIX_DTYPE, True, nest_p=0.3)
+    rules["next_hop"] = (rules["next_hop"] % 255) + 1  # u8 next hops like C1
+    small = lpm.FibTable(0, rules)  # depth 4, 64 KB image
+    db, ds = lpm.Fib.build(big), lpm.Fib.build(small)
+    gb, gs = db.geometry, ds.geometry
+    assert gb.depth == gs.depth and gb.value_bytes == gs.value_bytes == 1
+    img = lambda dev: dev.kernel_config()["smem_levels"]
+    keys = rng.integers(0, 2**64, 1 << 16, dtype=np.uint64)
+    addrs = addrs_from_keys(keys, rng)
+    wants = {}
+    for name, fib in (("big", big), ("small", small)):
+        st, b, nhs = orc.build_intervals(fib.rules, fib.default_next_hop)
+        wants[name] = oracle_next_hops(orc, b, nhs, addrs)
+    for name, dev in (("big", db), ("small", ds), ("big", db), ("small", ds), ("big", db)):
+        got = run_lookup(cuda, dev, addrs).astype(np.uint32)
+        np.testing.assert_array_equal(got, wants[name], err_msg=name)
+    assert img(db) >= 1 and img(ds) >= 1

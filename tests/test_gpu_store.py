@@ -337,3 +337,24 @@ def test_1m_prefix_rebuild_under_5s(lpm, cuda, st):
     assert dt < 5.0, dt
     assert store.stats.last_build_ms < 1000
     store.close()
+
+
+def test_release_fences_stay_bounded(lpm, cuda, st):
+    """every release used to add a CUDA event to the active snapshot. Now a
+    snapshot keeps at most one fence per reader stream (re-recorded on each release)
+    and recycles completed ones, however many acquire/release pairs run."""
+    torch = cuda
+    fib = lpm.workload_fib(0)
+    store = st.FibStore(fib)
+    rng = np.random.default_rng(9)
+    a = torch.from_numpy(addrs_from_keys(rng.integers(0, 2**64, 4096, dtype=np.uint64), rng)
+                         .view(np.uint8).reshape(-1, 16)).cuda()
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    for i in range(3000):
+        s = streams[i % 3]
+        snap = store.acquire()
+        snap.lookup_batch(a, stream=s)
+        snap.release(s)
+        assert store.stats.fences <= 3
+    torch.cuda.synchronize()
+    store.close()

@@ -1,4 +1,4 @@
-"""World-size-2 tests of the multi-GPU dispatcher's host logic on CPU (gloo).
+"""World-size 2/4/8 tests of the multi-GPU dispatcher's host logic on CPU (gloo).
 
 The GPU path runs the same code with NCCL (bench.py under torchrun): FIB built
 once on rank 0, the line array broadcast to every rank, contiguous query
@@ -54,22 +54,93 @@ def _worker(rank, world, port, q):
         q.put((rank, repr(e)))
 
 
-def test_dispatch_world2_gloo():
+def _run(target, world, *extra):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=target, args=(r, world, port, q) + extra) for r in range(world)]
     for p in procs:
         p.start()
-    res = sorted(q.get(timeout=300) for _ in procs)
+    res = sorted((q.get(timeout=600) for _ in procs), key=lambda r: r[0])
     for p in procs:
         p.join(timeout=60)
+    return res
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_dispatch_gloo(world):
+    """FIB built once on rank 0 and broadcast: every rank holds rank 0's exact line
+    array and geometry; weak-scaling shards reassemble the single-process stream;
+    the device-time reduction is the max over ranks."""
+    res = _run(_worker, world)
     for r in res:
         assert len(r) == 5, r
         rank, ok_lines, ok_geom, ok_shards, mx = r
         assert ok_lines and ok_geom and ok_shards
-        assert mx == 3.0
+        assert mx == 1.5 * world
+
+
+C4_TEST_CHUNK = 4096
+C4_TEST_CHUNKS = 27  # uneven over 2, 4 and 8 ranks
+
+
+def _digest_worker(rank, world, port, q):
+    """bench.py's C4 strong-scaling path on CPU: contiguous uneven chunk shards
+    (dispatch.shard with a total), each chunk's queries from the C4 generator (chunk c
+    seeded by c), next hops from the line array this rank received by broadcast —
+    resolved with the oracle in place of the kernel — hashed per chunk
+    (dispatch.chunk_hash) and combined over ranks (dispatch.combine_digests)."""
+    sys.path.insert(0, str(ROOT))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    import torch
+
+    import paper_2604_14650_b200 as lpm
+    from oracle.oracle import Oracle
+    from paper_2604_14650_b200 import dispatch
+    try:
+        dist = None
+        if world > 1:
+            import torch.distributed as tdist
+            tdist.init_process_group("gloo", rank=rank, world_size=world)
+            dist = tdist
+        fib = lpm.workload_fib(0)  # small FIB: the digest logic, not the FIB, is under test
+        tree = dispatch.build_on_root(fib, rank, 2)
+        geom, lines = dispatch.replicate_tree(tree, dist, torch.device("cpu"))
+        # the received layout's leaves carry the interval map: rebuild it from the lines
+        imap = lpm.build_intervals(fib)
+        ok = bool(np.array_equal(lines.numpy().view(np.uint64), lpm.build_tree(imap, 2).lines))
+        c0, nc = dispatch.shard(rank, world, 0, total=C4_TEST_CHUNKS)
+        o = Oracle()
+        st, b, nh = o.build_intervals(fib.rules, fib.default_next_hop)
+        mine = {}
+        for c in range(c0, c0 + nc):
+            a = lpm.workload_queries_host("C4", fib, c * C4_TEST_CHUNK, C4_TEST_CHUNK)
+            hops, _ = o.lookup_batch(0, b, nh, a, threads=1)
+            out = torch.from_numpy(hops.astype(np.uint16).view(np.uint8).copy())
+            mine[c] = dispatch.chunk_hash(out)
+        dig = dispatch.combine_digests(mine, dist)
+        q.put((rank, ok, nc, dig["sha256"], dig["chunks"]))
+        if dist is not None:
+            dist.destroy_process_group()
+    except Exception as e:
+        q.put((rank, repr(e)))
+
+
+def test_c4_digest_independent_of_world_size():
+    """The C4 line's output digest (a checksum of per-chunk checksums in chunk order)
+    is identical at world sizes 1, 2, 4 and 8 with uneven contiguous shards."""
+    digests = {}
+    for world in (1, 2, 4, 8):
+        res = _run(_digest_worker, world)
+        for r in res:
+            assert len(r) == 5, r
+        assert all(r[1] for r in res)
+        assert sum(r[2] for r in res) == C4_TEST_CHUNKS
+        assert len({r[2] for r in res}) <= 2  # near-equal shards
+        assert len({r[3] for r in res}) == 1 and res[0][4] == C4_TEST_CHUNKS
+        digests[world] = res[0][3]
+    assert len(set(digests.values())) == 1, digests
 
 
 def _update_worker(rank, world, port, q):

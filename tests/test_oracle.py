@@ -11,10 +11,11 @@ from pathlib import Path
 import numpy as np
 import pytest
 
-from _util import MASK64, addrs_from_keys, boundary_probe_keys, random_fib_rules, rules_array
+from _util import MASK64, addrs_from_keys, boundary_probe_keys, large_rules, random_fib_rules, rules_array, sha
 
 GOLDEN = Path(__file__).resolve().parent / "golden"
-FIXTURES = sorted(p.stem for p in GOLDEN.glob("*.npz"))
+FIXTURES = sorted(p.stem for p in GOLDEN.glob("*.npz") if not p.stem.startswith("large_"))
+LARGE_FIXTURES = sorted(p.stem for p in GOLDEN.glob("large_*.npz"))
 
 A = 0x20010DB800000000        # 2001:db8::
 B = 0x20010DB800010000        # 2001:db8:1::
@@ -161,9 +162,33 @@ def test_golden_oracle(orc, lpm, name):
         np.testing.assert_array_equal(got, d["interval_oracle"])
 
 
+@pytest.mark.parametrize("name", LARGE_FIXTURES)
+def test_golden_large_oracle(orc, lpm, name):
+    """Hash-pinned reference fixtures at SPEC acceptance size (10^5 rules) and
+    the deepest tree (the 1M-prefix C2 FIB): the rules are regenerated from their
+    recorded source and must match their sha256; the restatement's and the product's
+    interval maps must hash to the reference's (merge on and off); sampled keys must
+    get the reference's interval-oracle and linear-oracle answers."""
+    d = np.load(GOLDEN / f"{name}.npz")
+    rules, dflt = large_rules(d)
+    for merge in (1, 0):
+        st, b, nh = orc.build_intervals(rules, dflt, bool(merge))
+        assert st == 0 and len(b) == int(d[f"m_m{merge}"][0])
+        assert sha(b) == str(d[f"boundaries_sha256_m{merge}"]) and sha(nh) == str(d[f"next_hops_sha256_m{merge}"])
+        im = lpm.build_intervals(lpm.FibTable(dflt, rules), merge_adjacent=bool(merge))
+        assert sha(im.boundaries) == str(d[f"boundaries_sha256_m{merge}"])
+        assert sha(im.next_hops) == str(d[f"next_hops_sha256_m{merge}"])
+    st, b, nh = orc.build_intervals(rules, dflt, True)
+    out, _ = orc.lookup_batch(0, b, nh, addrs_from_keys(d["keys"]), threads=8)
+    np.testing.assert_array_equal(out, d["interval_oracle"])
+    pos = np.searchsorted(d["keys"], d["linear_keys"])
+    np.testing.assert_array_equal(out[pos], d["linear_oracle"])
+
+
 def test_reference_agrees_with_restatement(ref, orc, lpm):
-    """Live check against the compiled reference on the workload FIBs."""
-    for kind in (0, 1):
+    """Live check against the compiled reference on the workload FIBs (C0, C1 and the
+    1M-prefix C2 FIB)."""
+    for kind in (0, 1, 2):
         fib = lpm.workload_fib(kind)
         st, m = ref.build_intervals(fib.rules, fib.default_next_hop)
         assert st == 0
