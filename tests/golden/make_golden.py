@@ -105,12 +105,4 @@ def main():
 
 
 if __name__ == "__main__":
-    if sys.argv[1:] == ["large"]:  # only the large (hash-pinned) fixtures
-        ref_, rng_ = RefOracle(), np.random.default_rng(20261020)
-        for name, src in (("large_random_nested_100000", "random_nested:100000,100000"),
-                          ("large_ref_synth_100000", "ref_synth:100000,4"),
-                          ("large_workload_c2_fib", "workload:2")):
-            r, d = large_fixture_rules(src)
-            make_large(ref_, name, r, d, rng_, src)
-    else:
-        main()
+    main()
