@@ -226,6 +226,14 @@ int lpm6cu_fib_node_visits(lpm6cu_fib* fib, uint64_t* visits, int reset);
 int lpm6cu_lookup_batch(const lpm6cu_fib* fib, const void* addrs, uint64_t n, void* out,
                         void* stream);
 
+/* The serving-size fast path of lpm6cu_lookup_batch for buffers the caller knows
+ * are device memory on the FIB's device (the reference's search_batch over keys
+ * already in memory): no pointer-kind queries, no host pipeline — the
+ * launch only (plus the device switch when the calling thread is on another
+ * device). Host pointers here are undefined behaviour (the kernel faults). */
+int lpm6cu_lookup_batch_device(const lpm6cu_fib* fib, const void* d_addrs, uint64_t n, void* d_out,
+                               void* stream);
+
 /* 8-byte keys instead of 16-byte addresses — the input of the reference's
  * search_batch(t, keys[B]) and of its PBTR traces. Keys are clamped
  * like address keys. Device buffers: one kernel launch on `stream`; host buffers:

@@ -6,7 +6,10 @@
  * key, one 8x64-bit unsigned >= compare per 64-byte node, popcount, descend with
  * i = (k+1) i + (c+1) k) combined with batching (B = 16
  * interleaved descents) and depth-templated full unrolling.
- * Ordinal = leaf rank - 1. Compiled with -mavx512f/dq/bw only in this TU
+ * Ordinal = leaf rank - 1. Nodes are 64-byte aligned (one cache line,
+ * tree.hpp:42-74; oracle.py allocates the key array so), and the next batch's
+ * trace records are prefetched while the current batch descends.
+ * Compiled with -mavx512f/dq/bw only in this TU
  * and selected at run time, as CMakeLists.txt:18-46 does for the reference. */
 #include <immintrin.h>
 
@@ -19,6 +22,8 @@
                          const uint64_t* addrs, uint32_t* out) {                           \
     int64_t i[B], c[B];                                                                     \
     __m512i q[B];                                                                           \
+    /* the next batch's trace records are fetched ahead of use */            \
+    for (int b = 0; b < B; b += 4) _mm_prefetch((const char*)(addrs + 2 * (B + b)), _MM_HINT_T0); \
     for (int b = 0; b < B; ++b) {                                                           \
       uint64_t key = addrs[2 * b + 1];                                                      \
       if (key > ORC_MAX_QUERY) key = ORC_MAX_QUERY;                                         \

@@ -106,7 +106,12 @@ class Oracle:
 
     def build_tree(self, b: np.ndarray, nh: np.ndarray, k: int = 8):
         g = self.plan_geometry(len(b), k)
-        keys = np.empty(self.L.orc_total_key_slots(C.byref(g)) + 16, np.uint64)  # +16: SIMD over-read slack
+        # KeyArray is 64-byte aligned (tree.hpp:42-74): one node = one cache line.
+        slots = self.L.orc_total_key_slots(C.byref(g)) + 16  # +16: SIMD over-read slack
+        raw = np.empty(slots + 8, np.uint64)
+        off = (-raw.ctypes.data // 8) % 8
+        keys = raw[off: off + slots]
+        assert keys.ctypes.data % 64 == 0
         keys[:] = 0xFFFFFFFFFFFFFFFF
         values = np.empty(g.allocated_leaf_nodes * k, np.uint32)
         self.L.orc_build_tree(b.ctypes.data, nh.ctypes.data, len(b), k, C.byref(g), keys.ctypes.data,

@@ -109,6 +109,7 @@ SIGNATURES = {
     "lpm6cu_fib_violations": (I32, [P, C.POINTER(U32), I32]),
     "lpm6cu_fib_node_visits": (I32, [P, C.POINTER(U64), I32]),
     "lpm6cu_lookup_batch": (I32, [P, P, U64, P, P]),
+    "lpm6cu_lookup_batch_device": (I32, [P, P, U64, P, P]),
     "lpm6_workload_info_get": (I32, [I32, C.POINTER(WorkloadInfo_t)]),
     "lpm6_workload_fib": (I32, [I32, P, U64, C.POINTER(U64), C.POINTER(U32)]),
     "lpm6_workload_queries_host": (I32, [I32, P, U64, U64, U64, P, I32]),

@@ -704,6 +704,24 @@ int lpm6cu_lookup_batch(const lpm6cu_fib* fib, const void* addrs, uint64_t n, vo
   });
 }
 
+int lpm6cu_lookup_batch_device(const lpm6cu_fib* fib, const void* d_addrs, uint64_t n, void* d_out, void* stream) {
+  return guard([&] {
+    if (!fib) throw Error(Errc::InvalidArgument, "NULL fib");
+    if (n == 0) return;
+    if (!d_addrs || !d_out) throw Error(Errc::InvalidArgument, "NULL buffer");
+    if (reinterpret_cast<uintptr_t>(d_addrs) % 16 != 0)
+      throw Error(Errc::InvalidArgument, "addresses must be 16-byte aligned");
+    int cur = -1;
+    check_cuda(cudaGetDevice(&cur), "cudaGetDevice");
+    if (cur == fib->device) {
+      launch_lookup(fib, d_addrs, n, d_out, static_cast<cudaStream_t>(stream));
+    } else {
+      DeviceGuard dg(fib->device);
+      launch_lookup(fib, d_addrs, n, d_out, static_cast<cudaStream_t>(stream));
+    }
+  });
+}
+
 int lpm6cu_lookup_keys(const lpm6cu_fib* fib, const uint64_t* keys, uint64_t n, void* out, void* stream) {
   return guard([&] {
     if (!fib) throw Error(Errc::InvalidArgument, "NULL fib");

@@ -238,8 +238,10 @@ class Fib:
             raise Lpm6Error(9, f"out holds {nout} next hops, need {n}")
         if adev != odev:
             raise Lpm6Error(9, "addrs and out must both be device or both be host buffers")
-        s = _stream_handle(stream) if adev else None
-        check(lib().lpm6cu_lookup_batch(self._h, aptr, n, optr, s))
+        if adev:  # known device buffers: the launch-only entry point
+            check(lib().lpm6cu_lookup_batch_device(self._h, aptr, n, optr, _stream_handle(stream)))
+        else:
+            check(lib().lpm6cu_lookup_batch(self._h, aptr, n, optr, None))
         return out
 
 
