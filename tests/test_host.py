@@ -28,7 +28,7 @@ def header_functions():
 def test_library_exports_every_declared_symbol(lpm):
     from paper_2604_14650_b200._lib import LIB_PATH, SIGNATURES
     names = header_functions()
-    assert len(names) == len(SIGNATURES) == 59
+    assert len(names) == len(SIGNATURES) == 60
     dll = C.CDLL(str(LIB_PATH))
     for name in names:
         assert hasattr(dll, name), f"{name} declared in include/lpm6cu.h but not exported"
