@@ -287,27 +287,67 @@ def time_extras(lpm, torch, fdev, fib, addrs, n, vb, stream, device):
     return out
 
 
-def measured_traffic(workload, n):
-    """DRAM bytes per lookup launch of n queries, scaled from the committed ncu capture
-    (profiles/r01_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum of one launch)."""
-    p = ROOT / "profiles" / "r01_traffic.json"
+NCU_METRICS = ROOT / "profiles" / "r02_ncu_metrics.json"
+
+
+def ncu_metrics(workload):
+    """Per-query figures of the committed `ncu --set full` capture of this workload's
+    bench kernel (profiles/r02_ncu_metrics.json, tools/ncu_metrics.py); C3a/C3b fall
+    back to C1's and C4 to C2's (same FIB and kernel)."""
     try:
-        t = json.loads(p.read_text())
-        key = {"C3a": "C1", "C3b": "C1", "C4": "C2"}.get(workload, workload)
-        e = t[key]
-        return (e["dram_read_bytes"] + e["dram_write_bytes"]) / e["queries"] * n
+        t = json.loads(NCU_METRICS.read_text())
     except Exception:
         return None
+    return t.get(workload) or t.get({"C3a": "C1", "C3b": "C1", "C4": "C2"}.get(workload, workload))
 
 
-def roofline(geom, w, l2_gbs, smem_gbs, hbm_gbs, smem_cap=232448):
-    """roofline_lps = max_T min(HBM/(16+w), SMEM/(128 T), L2/(128 (d+1-T) + w))."""
+def roofline_object(geom, vb, cfg, lps, l2_gbs, smem_gbs, hbm_gbs, hbm_src, workload, n_per_launch, sm_mhz):
+    """The bench line's `roofline`: SURVEY §8d's model evaluated at the shared-memory
+    split the kernel actually runs (T = its staged levels) — `bound`, `achieved`,
+    `peak`, `frac` — plus the max-over-T form §8d states (`frac_best_T`), the HBM
+    fraction, the DRAM traffic of one launch from the committed ncu capture, and the
+    kernel's own ceiling from that capture: one L1 data-pipe wavefront per SM per
+    clock divided by the measured wavefronts per query."""
+    T = min(int(cfg["smem_levels"]), geom.depth + 1)
+    at = roofline(geom, vb, l2_gbs, smem_gbs, hbm_gbs, only_T=T)
+    best = roofline(geom, vb, l2_gbs, smem_gbs, hbm_gbs)
+    bpq = at["bytes_per_query"][at["bound"]]
+    peak = {"hbm": hbm_gbs, "smem": smem_gbs, "l2": l2_gbs}[at["bound"]]
+    m = ncu_metrics(workload)
+    obj = {"bound": at["bound"], "achieved": lps * bpq / 1e9, "peak": peak, "unit": "GB/s",
+           "frac": lps * bpq / 1e9 / peak,
+           "traffic": m["dram_bytes_per_query"] * n_per_launch if m else None,
+           "model": "SURVEY §8d at the kernel's split: bytes/query hbm 16+w, smem 128*T, l2 128*(d+1-T)+w",
+           "T": T, "lps_achieved_per_gpu": lps / 1e9, "lps_roofline_per_gpu": at["lps"] / 1e9,
+           "terms_glps": at["terms_glps"], "bytes_per_query": at["bytes_per_query"],
+           "frac_best_T": lps / best["lps"], "best_T": best["T"], "lps_roofline_best_T": best["lps"] / 1e9,
+           "hbm_frac": lps * (16 + vb) / 1e9 / hbm_gbs,
+           "peak_sources": {"hbm": hbm_src,
+                            "smem": "probe in this run: shared-memory read kernel on this device (not in MEASURED_PEAKS.json)",
+                            "l2": "probe in this run: random 128-B line gathers over a tree-sized buffer (not in MEASURED_PEAKS.json)"},
+           "measured": {"l2_gather_gbs": l2_gbs, "smem_gbs": smem_gbs, "hbm_gbs": hbm_gbs}}
+    if m:
+        clk = sm_mhz or m["sm_clock_mhz"]
+        ceil = 148 * clk * 1e6 / m["lsu_wavefronts_per_query"] / 1e9
+        obj.update({"limiter_ncu": f"L1 LSU data pipe {m['lsu_data_pipe_pct']:.1f}% of peak, texture data pipe "
+                                   f"{m['tex_data_pipe_pct']:.1f}%, issue {m['issue_active_pct']:.1f}% ({m['capture']})",
+                    "l1_wavefront_ceiling_glps": ceil, "frac_of_l1_ceiling": lps / 1e9 / ceil,
+                    "lsu_wavefronts_per_query": m["lsu_wavefronts_per_query"],
+                    "traffic_per_query": m["dram_bytes_per_query"], "ncu_capture": m["capture"]})
+    return obj
+
+
+def roofline(geom, w, l2_gbs, smem_gbs, hbm_gbs, smem_cap=232448, only_T=None):
+    """roofline_lps = max_T min(HBM/(16+w), SMEM/(128 T), L2/(128 (d+1-T) + w)) (SURVEY §8d);
+    with only_T, the term at that split alone."""
     d = geom.depth
     levels = d + 1
     best = None
     for T in range(0, levels + 1):
+        if only_T is not None and T != only_T:
+            continue
         staged = (geom.total_words if T >= levels else geom.level_start[T]) * 8 if T else 0
-        if staged > smem_cap:
+        if staged > smem_cap and only_T is None:
             break
         terms = {"hbm": hbm_gbs * 1e9 / (16 + w)}
         if T:
@@ -602,9 +642,7 @@ def run_chunked(args, lpm, dispatch, fdev, fib, info, geom, cfg, ws, rank, dev_i
             dist.barrier()
         return 0
     lps_gpu = nc * chunk * args.steps / (sum(step_ms) * 1e-3)
-    rl = roofline(geom, vb, l2_gbs, smem_gbs, hbm_gbs)
-    bpq = rl["bytes_per_query"][rl["bound"]]
-    peak = {"hbm": hbm_gbs, "smem": smem_gbs, "l2": l2_gbs}[rl["bound"]]
+    clocks = clk.summary()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -616,15 +654,11 @@ def run_chunked(args, lpm, dispatch, fdev, fib, info, geom, cfg, ws, rank, dev_i
                    "sharding": "contiguous chunk ranges; FIB replicated by NCCL broadcast"},
         "kernel": cfg,
         "l2_flush": f"not needed: each chunk streams {chunk * 16 / 1e9:.1f} GB of addresses (> 126 MB L2)",
-        "roofline": {"bound": rl["bound"], "achieved": lps_gpu * bpq / 1e9, "peak": peak, "unit": "GB/s",
-                     "frac": lps_gpu * bpq / 1e9 / peak, "traffic": measured_traffic(info.name, chunk),
-                     "lps_achieved_per_gpu": lps_gpu / 1e9,
-                     "lps_roofline_per_gpu": rl["lps"] / 1e9, "terms_glps": rl["terms_glps"],
-                     "measured": {"l2_gather_gbs": l2_gbs, "smem_gbs": smem_gbs, "hbm_gbs": hbm_gbs,
-                                  "hbm_source": hbm_src}},
+        "roofline": roofline_object(geom, vb, cfg, lps_gpu, l2_gbs, smem_gbs, hbm_gbs, hbm_src, info.name, chunk,
+                                    clocks.get("sm_mhz")),
         "cpu_baseline": None, "e2e": None,
         "gpu_launches": 2 * nc * args.steps,
-        "clocks": clk.summary(), "parity_sample": parity,
+        "clocks": clocks, "parity_sample": parity,
         "fib_build_ms": build_ms, "fib_build_device_ms": device_build_ms(lpm, fib, dev_index, vb),
         "fib_broadcast_ms": bcast_ms, "step_ms": step_ms, "per_rank_total_ms": per_rank_ms,
         "output_digest": digest,
@@ -788,12 +822,14 @@ def main():
                                            min_ctas_per_sm=minb)
                 except Exception:
                     continue
+                # launch() directly, never the captured graph: a graph replays the kernel
+                # and parameters captured before the sweep changed the config
                 for _ in range(2):
-                    step()
+                    launch()
                 a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a0.record(stream)
                 for _ in range(3):
-                    step()
+                    launch()
                 a1.record(stream)
                 torch.cuda.synchronize()
                 ms = a0.elapsed_time(a1) / 3
@@ -833,10 +869,7 @@ def main():
             dist.barrier()
         return 0
 
-    rl = roofline(geom, vb, l2_gbs, smem_gbs, hbm_gbs)
-    bpq = rl["bytes_per_query"][rl["bound"]]
-    peak = {"hbm": hbm_gbs, "smem": smem_gbs, "l2": l2_gbs}[rl["bound"]]
-    achieved = lps_gpu * bpq / 1e9
+    clocks = clk.summary()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -849,19 +882,13 @@ def main():
                    "sharding": "query batches; FIB replicated by NCCL broadcast"},
         "kernel": cfg,
         "l2_flush": f"not needed: each step streams {n * 16 / 1e9:.1f} GB of addresses (> 126 MB L2)",
-        "roofline": {"bound": rl["bound"], "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": measured_traffic(info.name, n),
-                     "lps_achieved_per_gpu": lps_gpu / 1e9, "lps_roofline_per_gpu": rl["lps"] / 1e9,
-                     "smem_levels_for_roofline": rl["T"], "terms_glps": rl["terms_glps"],
-                     "bytes_per_query": rl["bytes_per_query"],
-                     "measured": {"l2_gather_gbs": l2_gbs, "smem_gbs": smem_gbs, "hbm_gbs": hbm_gbs,
-                                  "hbm_source": hbm_src},
-                     "hbm_frac": lps_gpu * (16 + vb) / 1e9 / hbm_gbs},
+        "roofline": roofline_object(geom, vb, cfg, lps_gpu, l2_gbs, smem_gbs, hbm_gbs, hbm_src, info.name, n,
+                                    clocks.get("sm_mhz")),
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": args.steps,
         "cuda_graph": use_graph,
-        "clocks": clk.summary(),
+        "clocks": clocks,
         "parity_sample": parity,
         "fib_build_ms": build_ms,
         "fib_build_device_ms": device_build_ms(lpm, fib, dev_index, vb),

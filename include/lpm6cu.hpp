@@ -107,6 +107,10 @@ class Fib {
   void lookup_batch(const void* addrs, uint64_t n, void* out_next_hops, void* stream = nullptr) const {
     lpm6cu::check(lpm6cu_lookup_batch(h_, addrs, n, out_next_hops, stream));
   }
+  // Device buffers known to be on this FIB's GPU: the launch only (serving-size batches).
+  void lookup_batch_device(const void* d_addrs, uint64_t n, void* d_out, void* stream = nullptr) const {
+    lpm6cu::check(lpm6cu_lookup_batch_device(h_, d_addrs, n, d_out, stream));
+  }
 
   // One address (the reference's lookup(t, addr)): a batch of one through
   // the host path — correct but latency-bound; batch where throughput matters.

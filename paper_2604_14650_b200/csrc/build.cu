@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "capi_internal.hpp"
@@ -39,15 +40,38 @@ void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw Error(Errc::CudaError, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-// Device buffer owned for the duration of one build, from the stream-ordered
-// allocator (the pool keeps freed blocks, so repeated builds do not pay
-// cudaMalloc/cudaFree).
+// The build's temporaries come from a library-private stream-ordered memory pool
+// per device whose release threshold keeps up to 2 GiB reserved between builds.
+// (The device's default pool releases its memory at every synchronization, so
+// each rebuild of a FibStore commit would map its ~10^8 bytes of temporaries
+// again.) The pool is created once per device and lives as long as the process.
+cudaMemPool_t build_pool(int device) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  if (device < 0 || device >= 64) throw Error(Errc::CudaError, "device index out of range");
+  std::lock_guard<std::mutex> lk(mu);
+  if (!pools[device]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    ck(cudaMemPoolCreate(&pools[device], &props), "cudaMemPoolCreate (device build)");
+    uint64_t keep = 2ull << 30;
+    ck(cudaMemPoolSetAttribute(pools[device], cudaMemPoolAttrReleaseThreshold, &keep), "cudaMemPoolSetAttribute");
+  }
+  return pools[device];
+}
+
+// Device buffer owned for the duration of one build (stream-ordered, build_pool).
 struct DBuf {
   void* p = nullptr;
   cudaStream_t s = nullptr;
   DBuf() = default;
   DBuf(size_t bytes, cudaStream_t stream) : s(stream) {
-    if (bytes) ck(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync (device build)");
+    if (!bytes) return;
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    ck(cudaMallocFromPoolAsync(&p, bytes, build_pool(dev), s), "cudaMallocFromPoolAsync (device build)");
   }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;

@@ -54,6 +54,20 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 #ifndef LPM6_RANK_MODE
 #define LPM6_RANK_MODE 1
 #endif
+// Phase A as a shared-memory address walk (1) or the node-index form (0); the
+// leaf's next hop by a branch-free word select (1) or the compiler's lowering of
+// an indexed pick (0). Build-time switches for A/B runs (tools/build_variant.sh).
+#ifndef LPM6_PHASEA_WALK
+#define LPM6_PHASEA_WALK 1
+#endif
+#ifndef LPM6_LEAF_SEL
+#define LPM6_LEAF_SEL 1
+#endif
+// Phase B's key/node hand-over through a per-warp shared-memory slot (1) or
+// shuffles (0); the slot area follows the image (LookupParams::xchg_off).
+#ifndef LPM6_XCHG
+#define LPM6_XCHG 0
+#endif
 
 // ---- PTX helpers ------------------------------------------------------------
 
@@ -307,9 +321,13 @@ __device__ __forceinline__ unsigned leaf_value(const unsigned long long (&w)[4],
   constexpr unsigned kLast = (kOff + LeafFmt<VB>::kL * VB - 1) / 8;
   const unsigned o = kOff + ord * VB;  // byte offset within the lane's quarter
   const unsigned wi = o >> 3;
+#if LPM6_LEAF_SEL
   unsigned long long x = w[kFirst];
 #pragma unroll
   for (unsigned i = kFirst + 1; i <= kLast; ++i) x = sel64(wi == i, w[i], x);
+#else
+  const unsigned long long x = wi == 0 ? w[0] : wi == 1 ? w[1] : wi == 2 ? w[2] : w[3];
+#endif
   const unsigned v = static_cast<unsigned>(x >> ((o & 7u) * 8u));
   return VB == 1 ? (v & 0xFFu) : VB == 2 ? (v & 0xFFFFu) : v;
 }
@@ -449,7 +467,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
     }
 
     // Phase A: this thread's own queries through the shared-memory levels.
-    if constexpr (!CHECKED) {
+    if constexpr (!CHECKED && LPM6_PHASEA_WALK) {
       // As a walk over shared-memory byte addresses: with a = the address of node
       // n of level l and a' = a + 8 * rank after the four probes, the child's
       // address in level l + 1 is img(l+1) + (16 n + rank) * 120 =
@@ -534,6 +552,26 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
     // Phase B: the group's queries, one 128-byte line per query per level.
     unsigned long long qk[NS];
     unsigned nd[NS];
+#if LPM6_XCHG
+    if constexpr (TILES == 1) {
+      // Through a per-warp shared-memory slot instead of 12 shuffles: group g's four
+      // keys at 48 g (+8 s) and its four nodes at 48 g + 32 (+4 s). The 48-byte group
+      // stride puts the 8 groups' 16-byte chunks in 8 distinct bank quads, so the
+      // STS.64 (2 wavefronts), STS.32 (1) and the three broadcast LDS.128 (1 each)
+      // are conflict-free: 6 wavefronts against 12.
+      const uint32_t slot = s_base + p.xchg_off + (threadIdx.x >> 5) * kXchgBytes + (lane >> 2) * 48u;
+      __syncwarp();  // the previous tile's reads of this slot are done
+      asm volatile("st.shared.u64 [%0], %1;" ::"r"(slot + (lane & 3u) * 8u), "l"(key[0]) : "memory");
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(slot + 32u + (lane & 3u) * 4u), "r"(node[0]) : "memory");
+      __syncwarp();
+      asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(qk[0]), "=l"(qk[1]) : "r"(slot) : "memory");
+      asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(qk[2]), "=l"(qk[3]) : "r"(slot + 16u) : "memory");
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(nd[0]), "=r"(nd[1]), "=r"(nd[2]), "=r"(nd[3])
+                   : "r"(slot + 32u)
+                   : "memory");
+    } else
+#endif
 #pragma unroll
     for (int t = 0; t < TILES; ++t)
 #pragma unroll

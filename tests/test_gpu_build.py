@@ -54,7 +54,8 @@ def test_device_build_reference_fixtures(lpm, cuda):
     """The reference-generated golden fixtures (tests/golden) through the device build."""
     from pathlib import Path
     from paper_2604_14650_b200.gpu import build_intervals_device
-    for f in sorted((Path(__file__).resolve().parent / "golden").glob("*.npz")):
+    for f in sorted(p for p in (Path(__file__).resolve().parent / "golden").glob("*.npz")
+                    if not p.stem.startswith("large_")):  # large ones: test_gpu_parity
         g = np.load(f)
         fib = lpm.FibTable(int(g["default_nh"][0]), g["rules"])
         for merge in (1, 0):

@@ -40,8 +40,9 @@ def main(rep, queries):
     print(f"  instructions/query: {per_q(f(d, 'smsp__inst_executed.sum')):.2f}   "
           f"shared ld/query {per_q(f(d, 'smsp__sass_inst_executed_op_shared_ld.sum')):.3f}   "
           f"bank conflicts/query {per_q(f(d, 'l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum')):.2f}")
-    print(f"  dram bytes/query: {per_q(f(d, 'dram__bytes_read.sum') * 1e9 + f(d, 'dram__bytes_write.sum') * 1e6):.2f} "
-          f"(read {d.get('dram__bytes_read.sum', ('', ''))[0]}, write {d.get('dram__bytes_write.sum', ('', ''))[0]})")
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    dram = sum(f(d, k) * scale.get(d.get(k, ("byte", ""))[0], 1) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+    print(f"  dram bytes/query: {per_q(dram):.2f}")
     st = {k.split("stalled_")[1]: f(d, k) for k in d if k.startswith("smsp__pcsamp_warps_issue_stalled_")
           and not k.endswith("not_issued")}
     tot = sum(v for v in st.values() if v == v)
