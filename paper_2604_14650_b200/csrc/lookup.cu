@@ -246,12 +246,7 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
                           ? (plan_lp == 2 ? 2 : 1)
                           : 0;
   const int texl_mode = !texl ? 0 : (plan_lp == 3 && leaftex == 1) ? 2 : 1;
-  const size_t img_bytes = image_bytes_of(f->g, smem_levels);
-#if LPM6_XCHG
-  const size_t smem = img_bytes + (!leafs && tiles == 1 ? (threads_cta / 32) * kXchgBytes : 0);
-#else
-  const size_t smem = img_bytes;
-#endif
+  const size_t smem = image_bytes_of(f->g, smem_levels);
   const int threads = static_cast<int>(threads_cta);
   LaunchPlan plan;
   {
@@ -296,8 +291,7 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
   }
   p.out = static_cast<unsigned char*>(d_out);
   p.n = n;
-  p.smem_bytes = static_cast<unsigned>(img_bytes);
-  p.xchg_off = static_cast<unsigned>(img_bytes);
+  p.smem_bytes = static_cast<unsigned>(smem);
   p.smem_levels = std::min<unsigned>(smem_levels, f->g.depth);
   p.leaf_image_off = static_cast<unsigned>(image_bytes_of(f->g, f->g.depth) / 8);
   p.image = f->d_lines + f->g.image_start;

@@ -63,10 +63,11 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 #ifndef LPM6_LEAF_SEL
 #define LPM6_LEAF_SEL 1
 #endif
-// Phase B's key/node hand-over through a per-warp shared-memory slot (1) or
-// shuffles (0); the slot area follows the image (LookupParams::xchg_off).
-#ifndef LPM6_XCHG
-#define LPM6_XCHG 0
+// Texture fetches of 1-byte-next-hop leaf lines as two sector-disjoint halves (1)
+// or lane quarters (0); internal lines always as lane quarters (C2 level 4: the
+// halves measured 2 % slower there).
+#ifndef LPM6_TEX_SECTORS
+#define LPM6_TEX_SECTORS 1
 #endif
 
 // ---- PTX helpers ------------------------------------------------------------
@@ -167,13 +168,27 @@ __device__ __forceinline__ unsigned long long load_dst_key(const unsigned char* 
   return bswap64(le);  // network order: first byte is the most significant
 }
 
-// 32 bytes of a line through the texture path (two 16-byte texels at texel index t, t+1).
-__device__ __forceinline__ void tex_line_quarter(unsigned long long tex, unsigned t, unsigned long long (&w)[4]) {
+// 32 bytes of a line through the texture path: two 16-byte texels. Line texel
+// t0 + 0..7; lane j of the 4-lane group fetches texels (2j, 2j+1) — words 4j..4j+3,
+// the same quarter an LSU lane loads — or, with SECTORS, texels (j, j+4): words
+// 2j, 2j+1, 8+2j, 9+2j. With SECTORS the group's first fetch covers sectors 0-1 of
+// the line and its second sectors 2-3, so no sector is requested twice: with
+// (2j, 2j+1) both fetches touch all four sectors and the second re-reads them from
+// L1 — which misses when the ~30 KB of L1 a 221 KB shared-memory image leaves have
+// been recycled in between (measured on C1: texture sector hit rate 25 % -> every
+// line fetched ~1.5 times from L2 when the compiler spreads a slot's two fetches
+// apart). Counting ranks does not depend on which lane holds which key; the leaf
+// formats where it matters are handled at the call site.
+template <bool SECTORS>
+__device__ __forceinline__ void tex_line_quarter(unsigned long long tex, unsigned t0, unsigned j,
+                                                 unsigned long long (&w)[4]) {
+  const unsigned ta = SECTORS ? t0 + j : t0 + 2u * j;
+  const unsigned tb = SECTORS ? ta + 4u : ta + 1u;
   int a0, a1, a2, a3, b0, b1, b2, b3;
   asm volatile("tex.1d.v4.s32.s32 {%0,%1,%2,%3}, [%4, {%5}];"
-               : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3) : "l"(tex), "r"(t));
+               : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3) : "l"(tex), "r"(ta));
   asm volatile("tex.1d.v4.s32.s32 {%0,%1,%2,%3}, [%4, {%5}];"
-               : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3) : "l"(tex), "r"(t + 1));
+               : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3) : "l"(tex), "r"(tb));
   w[0] = static_cast<unsigned>(a0) | (static_cast<unsigned long long>(static_cast<unsigned>(a1)) << 32);
   w[1] = static_cast<unsigned>(a2) | (static_cast<unsigned long long>(static_cast<unsigned>(a3)) << 32);
   w[2] = static_cast<unsigned>(b0) | (static_cast<unsigned long long>(static_cast<unsigned>(b1)) << 32);
@@ -322,6 +337,15 @@ __device__ __forceinline__ unsigned leaf_value(const unsigned long long (&w)[4],
   const unsigned o = kOff + ord * VB;  // byte offset within the lane's quarter
   const unsigned wi = o >> 3;
 #if LPM6_LEAF_SEL
+  if constexpr (VB == 1) {
+    // 1-byte next hops: the compiler's own lowering of the pick. With it, ptxas
+    // issues each texture leaf line's two fetches back to back, which L1TEX turns
+    // into one L2 request per line; with the select below it spreads them apart
+    // and a C1 leaf line costs 1.6 L2 requests (ncu, lts__t_requests_srcunit_tex:
+    // 440 M vs 322 M per 268 M queries; C1 on texture leaves 56 vs 85 G/s).
+    const unsigned long long x = wi == 0 ? w[0] : wi == 1 ? w[1] : wi == 2 ? w[2] : w[3];
+    return static_cast<unsigned>(x >> ((o & 7u) * 8u)) & 0xFFu;
+  }
   unsigned long long x = w[kFirst];
 #pragma unroll
   for (unsigned i = kFirst + 1; i <= kLast; ++i) x = sel64(wi == i, w[i], x);
@@ -552,26 +576,6 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
     // Phase B: the group's queries, one 128-byte line per query per level.
     unsigned long long qk[NS];
     unsigned nd[NS];
-#if LPM6_XCHG
-    if constexpr (TILES == 1) {
-      // Through a per-warp shared-memory slot instead of 12 shuffles: group g's four
-      // keys at 48 g (+8 s) and its four nodes at 48 g + 32 (+4 s). The 48-byte group
-      // stride puts the 8 groups' 16-byte chunks in 8 distinct bank quads, so the
-      // STS.64 (2 wavefronts), STS.32 (1) and the three broadcast LDS.128 (1 each)
-      // are conflict-free: 6 wavefronts against 12.
-      const uint32_t slot = s_base + p.xchg_off + (threadIdx.x >> 5) * kXchgBytes + (lane >> 2) * 48u;
-      __syncwarp();  // the previous tile's reads of this slot are done
-      asm volatile("st.shared.u64 [%0], %1;" ::"r"(slot + (lane & 3u) * 8u), "l"(key[0]) : "memory");
-      asm volatile("st.shared.u32 [%0], %1;" ::"r"(slot + 32u + (lane & 3u) * 4u), "r"(node[0]) : "memory");
-      __syncwarp();
-      asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(qk[0]), "=l"(qk[1]) : "r"(slot) : "memory");
-      asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(qk[2]), "=l"(qk[3]) : "r"(slot + 16u) : "memory");
-      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                   : "=r"(nd[0]), "=r"(nd[1]), "=r"(nd[2]), "=r"(nd[3])
-                   : "r"(slot + 32u)
-                   : "memory");
-    } else
-#endif
 #pragma unroll
     for (int t = 0; t < TILES; ++t)
 #pragma unroll
@@ -590,7 +594,8 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
       if (li >= DEPTH - static_cast<int>(TA)) break;
       const unsigned l = TA + li;
       // 32-bit word offsets (the layout keeps the array below 2^32 words).
-      const unsigned base_w = static_cast<unsigned>(p.level_start[l]) + j * 4u;
+      const unsigned line_w = static_cast<unsigned>(p.level_start[l]);
+      const unsigned base_w = line_w + j * 4u;
       if (CHECKED) {
 #pragma unroll
         for (int s = 0; s < NS; ++s)
@@ -606,7 +611,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
         // +8 %); leaves through the texture pipe lose on L2-missing workloads
         // (C1 -17 %), so they stay on the LSU path.
         if (TEXL == 1 || (TEXL == 2 && s < NS / 2))
-          tex_line_quarter(p.tex, (base_w + nd[s] * 16u) >> 1, w[s]);
+          tex_line_quarter<false>(p.tex, (line_w + nd[s] * 16u) >> 1, j, w[s]);
         else
           ld_line_quarter(p.lines + (base_w + nd[s] * 16u), w[s]);
       }
@@ -629,7 +634,8 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
     }
     unsigned leafn[INPUT == kInKeyOrd ? NS : 1];  // kInKeyOrd: leaf node of each query
     {  // the leaf line: ordinal = rank - 1
-      const unsigned base_w = static_cast<unsigned>(p.level_start[DEPTH]) + j * 4u;
+      const unsigned line_w = static_cast<unsigned>(p.level_start[DEPTH]);
+      const unsigned base_w = line_w + j * 4u;
       if (CHECKED) {
 #pragma unroll
         for (int s = 0; s < NS; ++s)
@@ -643,7 +649,10 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
         // LEAFTEX 1: every slot through the texture pipe; 2: the upper half of the
         // group's slots (compile-time split, both pipes busy in one warp).
         if (LEAFTEX == 1 || (LEAFTEX == 2 && s >= NS / 2))
-          tex_line_quarter(p.tex, (base_w + nd[s] * 16u) >> 1, w[s]);
+          // sector-disjoint fetches for 1-byte next hops, whose leaf keeps the same
+          // key slots and value lane in both orders (the values are words 14-15 =
+          // lane 3's second texel either way); wider values straddle lanes then
+          tex_line_quarter<LPM6_TEX_SECTORS != 0 && VB == 1>(p.tex, (line_w + nd[s] * 16u) >> 1, j, w[s]);
         else
           ld_line_quarter(p.lines + (base_w + nd[s] * 16u), w[s]);
       }

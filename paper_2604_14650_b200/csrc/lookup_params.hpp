@@ -13,7 +13,6 @@ namespace lpm6::kern {
 enum : int { kInAddr = 0, kInKey = 1, kInPacket = 2, kInKeyOrd = 3 };  // kInKeyOrd: keys in, ordinals out too
 
 constexpr int kMaxKernelDepth = 7;
-constexpr unsigned kXchgBytes = 384;  // per warp: 8 groups x 48 bytes (lookup_kernel.cuh)
 
 struct LookupParams {
   const unsigned long long* lines;                     // the tree, 16 u64 words per line
@@ -39,7 +38,6 @@ struct LookupParams {
   // in the shared-memory image: img_step[0] = off(1); img_step[l] = off(l+1) -
   // 16 off(l) for 1 <= l < smem_levels - 1; img_step[smem_levels - 1] = -16 off(l).
   unsigned int img_step[LPM6CU_MAX_LEVELS];
-  unsigned int xchg_off;  // LPM6_XCHG: byte offset of the per-warp Phase B hand-over slots
 };
 
 using KernelFn = void (*)(const LookupParams);
