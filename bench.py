@@ -57,8 +57,8 @@ def parse_args():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also time every kernel shape (extra key)")
     ap.add_argument("--no-extras", action="store_true", help="skip the key/packet-input and store timings")
-    ap.add_argument("--line-path", choices=["tune", "lsu", "tex", "split", "tex-split"], default="tune",
-                    help="L2 lines through the LSU or the texture pipe (lpm6cu_kernel_config.line_path 0-3); tune = time all on the step's "
+    ap.add_argument("--line-path", choices=["tune", "lsu", "tex", "split", "tex-split", "tex-select"], default="tune",
+                    help="L2 lines through the LSU or the texture pipe (lpm6cu_kernel_config.line_path 0-4); tune = time all on the step's "
                          "batch before the warm-up (lpm6cu_fib_tune_line_path) and keep the faster")
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
                     help="replay each step's launch from a CUDA graph (auto: batches under 2^24 queries, "
@@ -577,7 +577,7 @@ def choose_line_path(args, fdev, addrs, out, stream):
         fdev.set_kernel_config(lanes_per_query=c["lanes_per_query"], smem_levels=c["smem_levels"],
                                ctas_per_sm=c["ctas_per_sm"], threads_per_cta=c["threads_per_cta"],
                                queries_per_lane=c["queries_per_lane"], min_ctas_per_sm=c["min_ctas_per_sm"],
-                               line_path={"lsu": 0, "tex": 1, "split": 2, "tex-split": 3}[args.line_path])
+                               line_path={"lsu": 0, "tex": 1, "split": 2, "tex-split": 3, "tex-select": 4}[args.line_path])
     cfg = fdev.kernel_config()
     cfg["line_path_choice"] = args.line_path
     return cfg

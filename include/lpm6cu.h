@@ -119,7 +119,8 @@ typedef struct {
                                 through the texture pipe too, faster when leaf lines often hit L1
                                 (skewed traffic); 2 = half of each warp's leaf lines through each
                                 pipe; 3 = as 1 with half of the internal-level lines through the
-                                LSU. Pick it on representative traffic with
+                                LSU; 4 = as 1 with another extraction of 1-byte next hops (same as 1
+                                for wider ones). Pick it on representative traffic with
                                 lpm6cu_fib_tune_line_path. */
 } lpm6cu_kernel_config;
 
@@ -194,8 +195,9 @@ int lpm6cu_fib_kernel_config(const lpm6cu_fib* fib, lpm6cu_kernel_config* cfg);
 /* Times the line paths on a representative batch (device buffers; two interleaved
  * rounds of `reps` timed launches per path after one untimed, the faster round
  * kept; on `stream`, which it synchronizes), keeps the
- * fastest in the kernel config and returns it in *line_path (0..3, see
- * lpm6cu_kernel_config; 3 only when the tree has internal L2 levels). Results are
+ * fastest in the kernel config and returns it in *line_path (0..4, see
+ * lpm6cu_kernel_config; 3 only when the tree has internal L2 levels, 4 only with
+ * 1-byte next hops). Results are
  * identical on every path; like the other tuning calls it must not race with
  * lookups on the handle. */
 int lpm6cu_fib_tune_line_path(lpm6cu_fib* fib, const void* d_addrs, uint64_t n, void* d_out, void* stream,

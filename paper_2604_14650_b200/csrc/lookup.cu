@@ -188,7 +188,7 @@ void resolve_config(lpm6cu_fib* f, const lpm6cu_kernel_config* req) {
     }
     c.smem_levels = t;
   }
-  if (c.line_path > 3) throw Error(Errc::InvalidArgument, "line_path must be 0, 1, 2 or 3");
+  if (c.line_path > 4) throw Error(Errc::InvalidArgument, "line_path must be 0..4");
   if (c.smem_levels > tmax) c.smem_levels = tmax;
   const unsigned long long staged = image_bytes_of(f->g, c.smem_levels);
   if (staged > budget)
@@ -239,11 +239,12 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
   const bool texl = f->tex && !leafs && input != kInKeyOrd && f->d_err == nullptr && smem_levels < f->g.depth &&
                     tiles == 1 && threads_cta == 1024 && minb == 1 && f->g.depth >= 2;
   // Line path plan (lpm6cu_kernel_config.line_path): 0 LSU leaves, 1 texture leaves,
-  // 2 split leaves, 3 texture leaves + split internal L2 levels.
+  // 2 split leaves, 3 texture leaves + split internal L2 levels, 4 texture leaves
+  // with the select extraction of 1-byte next hops (= 1 for wider next hops).
   const int plan_lp = static_cast<int>(f->cfg.line_path);
   const int leaftex = plan_lp != 0 && f->tex && !leafs && (input == kInAddr || input == kInKey) &&
                               f->d_err == nullptr && tiles == 1 && threads_cta == 1024 && minb == 1 && f->g.depth >= 1
-                          ? (plan_lp == 2 ? 2 : 1)
+                          ? (plan_lp == 2 ? 2 : (plan_lp == 4 && f->g.value_bytes == 1) ? 3 : 1)
                           : 0;
   const int texl_mode = !texl ? 0 : (plan_lp == 3 && leaftex == 1) ? 2 : 1;
   const size_t smem = image_bytes_of(f->g, smem_levels);
@@ -579,6 +580,16 @@ int lpm6cu_fib_kernel_config(const lpm6cu_fib* f, lpm6cu_kernel_config* cfg) {
   });
 }
 
+namespace {
+// Line paths that differ from the others for this tree: 3 only with internal L2
+// levels (it splits them), 4 only with 1-byte next hops (its extraction).
+bool plan_applies(const lpm6cu_fib* f, unsigned path) {
+  if (path == 3) return f->g.depth > f->cfg.smem_levels;
+  if (path == 4) return f->g.value_bytes == 1;
+  return path < 3;
+}
+}  // namespace
+
 int lpm6cu_fib_tune_line_path(lpm6cu_fib* f, const void* d_addrs, uint64_t n, void* d_out, void* stream,
                               uint32_t reps, uint32_t* line_path) {
   return guard([&] {
@@ -601,15 +612,15 @@ int lpm6cu_fib_tune_line_path(lpm6cu_fib* f, const void* d_addrs, uint64_t n, vo
         cudaEventDestroy(ev[0]);
         throw Error(Errc::CudaError, "cudaEventCreate");
       }
-      float ms[4] = {0.f, 0.f, 0.f, 0.f};
+      float ms[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
       try {
         const unsigned r = reps ? reps : 3;
         // Plan 3 differs from plan 1 only when the tree has internal L2 levels.
-        const unsigned plans = (f->g.depth > f->cfg.smem_levels) ? 4u : 3u;
         // Two interleaved rounds, the faster of each plan's two timings kept, so a
         // clock ramp or a neighbour's burst during one plan's turn cannot pick it.
         for (unsigned round = 0; round < 2; ++round)
-          for (unsigned path = 0; path < plans; ++path) {
+          for (unsigned path = 0; path < 5; ++path) {
+            if (!plan_applies(f, path)) continue;
             c.line_path = path;
             f->cfg = c;
             f->invalidate_plans();
@@ -632,9 +643,8 @@ int lpm6cu_fib_tune_line_path(lpm6cu_fib* f, const void* d_addrs, uint64_t n, vo
       }
       cudaEventDestroy(ev[0]);
       cudaEventDestroy(ev[1]);
-      const unsigned plans = (f->g.depth > f->cfg.smem_levels) ? 4u : 3u;
-      for (unsigned path = 1; path < plans; ++path)
-        if (ms[path] < ms[best]) best = path;
+      for (unsigned path = 1; path < 5; ++path)
+        if (plan_applies(f, path) && ms[path] < ms[best]) best = path;
     }
     c.line_path = best;
     f->cfg = c;

@@ -329,7 +329,7 @@ __device__ __forceinline__ unsigned long long sel64(bool p, unsigned long long a
 // Next hop of leaf ordinal `ord` from the value lane's 32 bytes: a branch-free
 // select of the 8-byte word holding it (only the words the value bytes occupy
 // are candidates) and one funnel shift. Values never straddle a word.
-template <int VB>
+template <int VB, bool SELECT = (VB != 1)>
 __device__ __forceinline__ unsigned leaf_value(const unsigned long long (&w)[4], unsigned ord) {
   constexpr unsigned kOff = LeafFmt<VB>::kValueOff;
   constexpr unsigned kFirst = kOff / 8;
@@ -337,12 +337,13 @@ __device__ __forceinline__ unsigned leaf_value(const unsigned long long (&w)[4],
   const unsigned o = kOff + ord * VB;  // byte offset within the lane's quarter
   const unsigned wi = o >> 3;
 #if LPM6_LEAF_SEL
-  if constexpr (VB == 1) {
-    // 1-byte next hops: the compiler's own lowering of the pick. With it, ptxas
-    // issues each texture leaf line's two fetches back to back, which L1TEX turns
-    // into one L2 request per line; with the select below it spreads them apart
-    // and a C1 leaf line costs 1.6 L2 requests (ncu, lts__t_requests_srcunit_tex:
-    // 440 M vs 322 M per 268 M queries; C1 on texture leaves 56 vs 85 G/s).
+  if constexpr (!SELECT) {
+    // 1-byte next hops (unless line path 4): the compiler's own lowering of the
+    // pick. With it, ptxas issues each texture leaf line's two fetches back to back;
+    // with the select below it spreads them apart, and on L1-missing traffic the
+    // second fetch then often misses too (C1 on texture leaves: 56 vs 85 G/s).
+    // On L1-hitting traffic the select's shorter code wins (C3a 96 vs 93 G/s):
+    // line path 4 = texture leaves with the select, for the tuner to choose.
     const unsigned long long x = wi == 0 ? w[0] : wi == 1 ? w[1] : wi == 2 ? w[2] : w[3];
     return static_cast<unsigned>(x >> ((o & 7u) * 8u)) & 0xFFu;
   }
@@ -412,7 +413,8 @@ __device__ __forceinline__ unsigned leaf_search_smem(const unsigned long long* l
 // L2 line loads and no cross-lane traffic.
 // TEXL: the internal L2 levels are read through the texture pipe (p.tex) — 1:
 // every line, 2: the lower half of each group's slots (the rest through the LSU).
-// LEAFTEX: the leaf lines too — 1: every leaf line, 2: the upper half of each
+// LEAFTEX: the leaf lines too — 1: every leaf line (3: the same with the select
+// extraction of 1-byte next hops, line path 4), 2: the upper half of each
 // group's slots. The halves are compile-time splits, so both L1TEX pipes work
 // in every warp. Texture hits return off the LSU data pipe, which pays when
 // leaf lines hit L1 often (skewed traffic: C3b +9 % with 1); on L1-missing
@@ -648,7 +650,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
       for (int s = 0; s < NS; ++s) {
         // LEAFTEX 1: every slot through the texture pipe; 2: the upper half of the
         // group's slots (compile-time split, both pipes busy in one warp).
-        if (LEAFTEX == 1 || (LEAFTEX == 2 && s >= NS / 2))
+        if (LEAFTEX == 1 || LEAFTEX == 3 || (LEAFTEX == 2 && s >= NS / 2))
           // sector-disjoint fetches for 1-byte next hops, whose leaf keeps the same
           // key slots and value lane in both orders (the values are words 14-15 =
           // lane 3's second texel either way); wider values straddle lanes then
@@ -702,7 +704,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
       for (int t = 0; t < TILES; ++t) {
         unsigned v[4];
 #pragma unroll
-        for (int s = 0; s < 4; ++s) v[s] = leaf_value<VB>(w[4 * t + s], nd[4 * t + s]);
+        for (int s = 0; s < 4; ++s) v[s] = leaf_value<VB, VB != 1 || LEAFTEX == 3>(w[4 * t + s], nd[4 * t + s]);
         store_group<VB>(p, (st * TILES + t) * 32ull + gbase, v);
       }
     }
@@ -738,6 +740,10 @@ KernelFn pick_depth_texl(int depth) {
 // 2 split). Instantiated: texl 0/1 with either leaf mode, texl 2 with texture leaves.
 template <int VB, int INPUT>
 KernelFn pick_leaftex(int depth, int texl, int mode) {
+  if (mode == 3) {  // texture leaves with the select extraction: 1-byte next hops only
+    if constexpr (VB == 1) return texl == 1 ? pick_depth_texl<VB, INPUT, 1, 3>(depth) : texl == 0 ? pick_depth_texl<VB, INPUT, 0, 3>(depth) : nullptr;
+    return nullptr;
+  }
   if (texl == 2) return mode == 1 ? pick_depth_texl<VB, INPUT, 2, 1>(depth) : nullptr;
   if (mode == 2) return texl ? pick_depth_texl<VB, INPUT, 1, 2>(depth) : pick_depth_texl<VB, INPUT, 0, 2>(depth);
   return texl ? pick_depth_texl<VB, INPUT, 1, 1>(depth) : pick_depth_texl<VB, INPUT, 0, 1>(depth);

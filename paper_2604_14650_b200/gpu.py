@@ -177,7 +177,7 @@ class Fib:
         return self.kernel_config()
 
     def tune_line_path(self, addrs, out=None, stream=None, reps: int = 3) -> int:
-        """Time the line paths (lpm6cu_kernel_config.line_path 0-3) on a representative
+        """Time the line paths (lpm6cu_kernel_config.line_path 0-4) on a representative
         device batch and keep the fastest in the kernel config; returns its number."""
         vb = self.value_bytes
         aptr, n, adev = _ptr_len(addrs, 16)

@@ -36,7 +36,7 @@ def test_texture_line_path_matches_oracle_on_workloads(lpm, orc, cuda, workload)
     da = torch.from_numpy(addrs.view(np.uint8).reshape(-1, 16)).cuda()
     dk = torch.from_numpy(np.ascontiguousarray(addrs[:, 1]).view(np.int64)).cuda()
     view = VIEW[dev.geometry.value_bytes]
-    for lp in (1, 2, 3, 0):
+    for lp in (1, 2, 3, 4, 0):
         cfg = dev.set_kernel_config(line_path=lp)
         assert cfg["line_path"] == lp
         got = dev.lookup_batch(da)
@@ -58,7 +58,7 @@ def test_tuner_picks_a_path_and_keeps_results(lpm, orc, cuda):
         gen.run(0, n, d)
         base = dev.lookup_batch(d).clone()
         chosen = dev.tune_line_path(d)
-        assert chosen in (0, 1, 2, 3)
+        assert chosen in (0, 1, 2, 3, 4)
         assert dev.kernel_config()["line_path"] == chosen
         again = dev.lookup_batch(d)
         torch.cuda.synchronize()
@@ -86,7 +86,7 @@ def test_line_path_argument_errors(lpm, cuda):
     torch = cuda
     dev = lpm.Fib.build(lpm.workload_fib(1))
     with pytest.raises(lpm.Lpm6Error):
-        dev.set_kernel_config(line_path=4)
+        dev.set_kernel_config(line_path=5)
     with pytest.raises(lpm.Lpm6Error):
         dev.tune_line_path(np.zeros((16, 16), np.uint8))  # host buffers
     with pytest.raises(lpm.Lpm6Error):

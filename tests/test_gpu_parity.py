@@ -187,7 +187,7 @@ def test_checked_mode_flags_corrupted_tree(lpm, orc, cuda):
     assert good.violations() == 0
 
 
-LINE_PATHS = (0, 1, 2, 3)  # lpm6cu_kernel_config.line_path: every plan the tuner can pick
+LINE_PATHS = (0, 1, 2, 3, 4)  # lpm6cu_kernel_config.line_path: every plan the tuner can pick
 
 
 def test_c1_full_size(lpm, orc, cuda):
@@ -471,7 +471,7 @@ def test_golden_large_fixtures_on_gpu(lpm, cuda, name):
         if name == "large_workload_c2_fib":
             assert geo.depth == 5 and geo.value_bytes == 2
         for t in [None] + list(range(geo.depth + geo.leaf_image + 1)):
-            for lp in (0, 1, 2, 3):
+            for lp in (0, 1, 2, 3, 4):
                 dev.set_kernel_config(smem_levels=t, line_path=lp)
                 got = run_lookup(cuda, dev, addrs).astype(np.uint32)
                 np.testing.assert_array_equal(got, d["interval_oracle"], err_msg=f"{name} T={t} lp={lp}")

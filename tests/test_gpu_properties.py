@@ -32,7 +32,7 @@ def test_gpu_matches_oracle_on_generated_fibs(lpm, orc, cuda, fib_def, keys, vb)
     da = torch.from_numpy(addrs_from_keys(k).view(np.uint8).reshape(-1, 16)).cuda()
     dk = torch.from_numpy(k.view(np.int64)).cuda()
     view = {1: np.uint8, 2: np.uint16, 4: np.uint32}[g.value_bytes]
-    for t, lp in [(t, lp) for t in [None] + list(range(g.depth + g.leaf_image + 1)) for lp in (0, 1, 2, 3)]:
+    for t, lp in [(t, lp) for t in [None] + list(range(g.depth + g.leaf_image + 1)) for lp in (0, 1, 2, 3, 4)]:
         dev.set_kernel_config(smem_levels=t, line_path=lp)
         for checked in (False, True):
             dev.set_checked(checked)

@@ -35,7 +35,7 @@ def test_random_fibs_every_mode(lpm, orc, cuda):
         dk = torch.from_numpy(keys.view(np.int64)).cuda()
         view = {1: np.uint8, 2: np.uint16, 4: np.uint32}[g.value_bytes]
         for t in [None] + list(range(g.depth + g.leaf_image + 1)):
-            for lp in (0, 1, 2, 3):  # line paths: which L1TEX pipe carries the L2 lines
+            for lp in (0, 1, 2, 3, 4):  # line paths: which L1TEX pipe carries the L2 lines
                 dev.set_kernel_config(smem_levels=t, line_path=lp)
                 for checked in (False, True):
                     dev.set_checked(checked)
