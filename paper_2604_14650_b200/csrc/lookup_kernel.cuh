@@ -69,6 +69,9 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 #ifndef LPM6_TEX_SECTORS
 #define LPM6_TEX_SECTORS 1
 #endif
+#ifndef LPM6_HALF_PROBE
+#define LPM6_HALF_PROBE 0
+#endif
 
 // ---- PTX helpers ------------------------------------------------------------
 
@@ -425,6 +428,10 @@ template <int DEPTH, int VB, int TILES, int THREADS, int MINB, bool CHECKED, int
           int TEXL = 0, int LEAFTEX = 0>
 __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const LookupParams p) {
   using F = LeafFmt<VB>;
+  // Texture leaf fetches as sector-disjoint halves (tex_line_quarter) for 1-byte next
+  // hops. (2-byte ones would need their values gathered from lanes 2 and 3; measured
+  // on C2: no gain on texture leaves, 56 vs 55 G/s, so they keep lane quarters.)
+  constexpr bool kLeafSectors = LPM6_TEX_SECTORS != 0 && VB == 1;
   unsigned violations = 0;
   unsigned long long visits = 0;  // CHECKED: lines visited by this lane's own queries
   constexpr int NS = 4 * TILES;  // queries in flight per 4-lane group
@@ -650,13 +657,31 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
       for (int s = 0; s < NS; ++s) {
         // LEAFTEX 1: every slot through the texture pipe; 2: the upper half of the
         // group's slots (compile-time split, both pipes busy in one warp).
+#if !LPM6_HALF_PROBE
         if (LEAFTEX == 1 || LEAFTEX == 3 || (LEAFTEX == 2 && s >= NS / 2))
-          // sector-disjoint fetches for 1-byte next hops, whose leaf keeps the same
-          // key slots and value lane in both orders (the values are words 14-15 =
-          // lane 3's second texel either way); wider values straddle lanes then
-          tex_line_quarter<LPM6_TEX_SECTORS != 0 && VB == 1>(p.tex, (line_w + nd[s] * 16u) >> 1, j, w[s]);
+#endif
+          // sector-disjoint fetches (kLeafSectors): for 1-byte next hops the leaf
+          // keeps the same key slots and value lane in both orders (the values are
+          // words 14-15 = lane 3's second texel either way)
+#if LPM6_HALF_PROBE  // timing experiment only (wrong answers): a 64-byte leaf read per query
+        {
+          if (LEAFTEX == 1 || LEAFTEX == 3 || (LEAFTEX == 2 && s >= NS / 2)) {
+            int a0, a1, a2, a3;
+            asm volatile("tex.1d.v4.s32.s32 {%0,%1,%2,%3}, [%4, {%5}];"
+                         : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3) : "l"(p.tex), "r"(((line_w + nd[s] * 16u) >> 1) + j));
+            w[s][0] = static_cast<unsigned>(a0) | (static_cast<unsigned long long>(static_cast<unsigned>(a1)) << 32);
+            w[s][1] = static_cast<unsigned>(a2) | (static_cast<unsigned long long>(static_cast<unsigned>(a3)) << 32);
+          } else {
+            asm volatile("ld.global.nc.v2.u64 {%0,%1}, [%2];"
+                         : "=l"(w[s][0]), "=l"(w[s][1]) : "l"(p.lines + line_w + nd[s] * 16u + 2u * j));
+          }
+          w[s][2] = w[s][3] = ~0ull;
+        }
+#else
+          tex_line_quarter<kLeafSectors>(p.tex, (line_w + nd[s] * 16u) >> 1, j, w[s]);
         else
           ld_line_quarter(p.lines + (base_w + nd[s] * 16u), w[s]);
+#endif
       }
       if constexpr (INPUT == kInKeyOrd) {
 #pragma unroll
