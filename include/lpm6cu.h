@@ -94,12 +94,17 @@ typedef struct {
   uint32_t leaf_image;   /* 1: small tree — the leaf lines also have a shared-memory image (16 words
                             at a 17-word stride) right after the internal image; smem_levels =
                             depth + 1 then serves the whole lookup from shared memory */
+  uint32_t leaf_words;   /* words per leaf: 16 (one 128-byte line) or 8 (half-line leaves: 6 keys in
+                            words 0-5, their 1- or 2-byte next hops in words 6-7) */
+  uint32_t reserved;
 } lpm6cu_geometry;
 
 typedef struct {
   uint32_t merge_adjacent; /* IntervalBuildOptions::merge_adjacent (intervals.hpp:28); default 1 */
   uint32_t value_bytes;    /* 0 = narrowest width holding every next hop */
-  uint32_t reserved0;
+  uint32_t leaf_format;    /* 0 = automatic (half-line leaves where they keep the depth and the
+                              shared-memory levels of a tree with an L2 internal level), 1 = full
+                              128-byte leaf lines, 2 = half-line leaves (1- or 2-byte next hops) */
   uint32_t reserved;
 } lpm6cu_build_opts;
 
@@ -140,6 +145,8 @@ int lpm6_build_intervals(const lpm6cu_prefix* rules, uint64_t n, uint32_t defaul
 
 /* Geometry for m boundaries at a next-hop width of value_bytes. */
 int lpm6_plan_layout(uint64_t m, uint32_t value_bytes, lpm6cu_geometry* g);
+/* The same with an explicit leaf format (lpm6cu_build_opts.leaf_format). */
+int lpm6_plan_layout_ex(uint64_t m, uint32_t value_bytes, uint32_t leaf_format, lpm6cu_geometry* g);
 
 /* Lay out the tree. With lines == NULL only *g is filled (to size the arrays:
  * g->total_words u64 words of lines, g->leaf_nodes * g->leaf_keys leaf values).
@@ -147,6 +154,10 @@ int lpm6_plan_layout(uint64_t m, uint32_t value_bytes, lpm6cu_geometry* g);
 int lpm6_build_tree(const uint64_t* boundaries, const uint32_t* next_hops, uint64_t m,
                     uint32_t default_next_hop, uint32_t value_bytes, lpm6cu_geometry* g,
                     uint64_t* lines, uint32_t* leaf_values);
+/* The same with an explicit leaf format (lpm6cu_build_opts.leaf_format). */
+int lpm6_build_tree_ex(const uint64_t* boundaries, const uint32_t* next_hops, uint64_t m,
+                       uint32_t default_next_hop, uint32_t value_bytes, uint32_t leaf_format,
+                       lpm6cu_geometry* g, uint64_t* lines, uint32_t* leaf_values);
 
 /* Parse "<ipv6>/<len> <next_hop>" (fib.cpp:72-105). */
 int lpm6_parse_prefix(const char* text, lpm6cu_prefix* out, int* host_bits_masked);

@@ -42,11 +42,12 @@ class Geometry_t(C.Structure):
                 ("num_keys", C.c_uint64), ("leaf_nodes", C.c_uint64), ("total_words", C.c_uint64),
                 ("image_start", C.c_uint64),
                 ("level_nodes", C.c_uint64 * MAX_LEVELS), ("level_start", C.c_uint64 * MAX_LEVELS),
-                ("default_next_hop", C.c_uint32), ("leaf_image", C.c_uint32)]
+                ("default_next_hop", C.c_uint32), ("leaf_image", C.c_uint32), ("leaf_words", C.c_uint32),
+                ("reserved", C.c_uint32)]
 
 
 class BuildOpts_t(C.Structure):
-    _fields_ = [("merge_adjacent", C.c_uint32), ("value_bytes", C.c_uint32), ("reserved0", C.c_uint32),
+    _fields_ = [("merge_adjacent", C.c_uint32), ("value_bytes", C.c_uint32), ("leaf_format", C.c_uint32),
                 ("reserved", C.c_uint32)]
 
 
@@ -90,6 +91,8 @@ SIGNATURES = {
     "lpm6_build_intervals": (I32, [P, U64, U32, I32, P, P, U64, C.POINTER(U64)]),
     "lpm6_plan_layout": (I32, [U64, U32, C.POINTER(Geometry_t)]),
     "lpm6_build_tree": (I32, [P, P, U64, U32, U32, C.POINTER(Geometry_t), P, P]),
+    "lpm6_plan_layout_ex": (I32, [U64, U32, U32, C.POINTER(Geometry_t)]),
+    "lpm6_build_tree_ex": (I32, [P, P, U64, U32, U32, U32, C.POINTER(Geometry_t), P, P]),
     "lpm6_parse_prefix": (I32, [C.c_char_p, C.POINTER(Prefix_t), C.POINTER(I32)]),
     "lpm6cu_fib_build": (I32, [I32, P, U64, U32, C.POINTER(BuildOpts_t), C.POINTER(P)]),
     "lpm6cu_fib_build_device": (I32, [I32, P, U64, U32, C.POINTER(BuildOpts_t), P, C.POINTER(P)]),

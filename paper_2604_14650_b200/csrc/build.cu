@@ -216,7 +216,7 @@ __global__ void merge_flags_kernel(const unsigned* nh, const u64d* m_raw, int me
 }
 
 struct Geo {
-  unsigned depth, kl, vb, image_levels;
+  unsigned depth, kl, vb, image_levels, leaf_words;
   u64d m, leaf_nodes, image_start;
   u64d level_start[kMaxLevels];
   u64d span[kMaxLevels];  // boundaries under one child of a level-l node
@@ -252,9 +252,8 @@ __global__ void leaf_kernel(const Geo g, const u64d* bnd, const unsigned* nh, u6
       for (unsigned b = 0; b < g.vb; ++b)
         words[(byte + b) >> 3] |= ((v >> (8 * b)) & 0xFFull) << (8 * ((byte + b) & 7u));
     }
-    u64d* line = lines + g.level_start[g.depth] + n * 16;
-#pragma unroll
-    for (int w = 0; w < 16; ++w) line[w] = words[w];
+    u64d* line = lines + g.level_start[g.depth] + n * g.leaf_words;  // 16, or 8 for half-line leaves
+    for (unsigned w = 0; w < g.leaf_words; ++w) line[w] = words[w];
   }
 }
 
@@ -404,14 +403,16 @@ namespace lpm6::capi {
 namespace {
 
 // Step 6: lay out m device-resident intervals; returns the cudaMalloc'ed line array.
-void* device_layout(const DeviceIntervals& iv, u32 vb, uint32_t default_nh, cudaStream_t s, lpm6cu_geometry* geom) {
-  TreeLayout t = plan_layout(iv.m, vb);
+void* device_layout(const DeviceIntervals& iv, u32 vb, u32 leaf_format, uint32_t default_nh, cudaStream_t s,
+                    lpm6cu_geometry* geom) {
+  TreeLayout t = plan_layout(iv.m, vb, leaf_format);
   t.default_next_hop = default_nh;
   Geo g{};
   g.depth = t.depth;
   g.kl = t.leaf_keys;
   g.vb = t.value_bytes;
   g.image_levels = t.image_levels;
+  g.leaf_words = t.leaf_words;
   g.m = t.num_keys;
   g.leaf_nodes = t.leaf_nodes;
   g.image_start = t.image_start;
@@ -467,7 +468,7 @@ void* device_build_tree(const lpm6cu_prefix* rules, uint64_t n, uint32_t default
                         cudaStream_t s, lpm6cu_geometry* geom) {
   const bool merge = opts ? opts->merge_adjacent != 0 : true;
   DeviceIntervals iv = device_intervals(rules, n, default_nh, merge, s);
-  return device_layout(iv, value_bytes_for(opts, iv.max_nh), default_nh, s, geom);
+  return device_layout(iv, value_bytes_for(opts, iv.max_nh), opts ? opts->leaf_format : 0u, default_nh, s, geom);
 }
 
 // Step 6 only, from host intervals already validated by the caller (a loaded
@@ -482,7 +483,7 @@ void* device_build_tree_from_intervals(const uint64_t* boundaries, const uint32_
   for (uint64_t i = 0; i < m; ++i) iv.max_nh = std::max(iv.max_nh, next_hops[i]);
   ck(cudaMemcpyAsync(iv.bnd.p, boundaries, m * 8, cudaMemcpyHostToDevice, s), "H2D boundaries");
   ck(cudaMemcpyAsync(iv.nh.p, next_hops, m * 4, cudaMemcpyHostToDevice, s), "H2D next hops");
-  return device_layout(iv, value_bytes_for(opts, iv.max_nh), default_nh, s, geom);
+  return device_layout(iv, value_bytes_for(opts, iv.max_nh), opts ? opts->leaf_format : 0u, default_nh, s, geom);
 }
 
 }  // namespace lpm6::capi

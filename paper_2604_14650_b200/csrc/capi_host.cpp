@@ -39,6 +39,7 @@ void export_geometry(const TreeLayout& t, lpm6cu_geometry* g) {
   g->image_levels = t.image_levels;
   g->image_start = t.image_start;
   g->leaf_image = t.leaf_image;
+  g->leaf_words = t.leaf_words;
   for (int l = 0; l < kMaxLevels; ++l) {
     g->level_nodes[l] = t.level_nodes[l];
     g->level_start[l] = t.level_start[l];
@@ -49,14 +50,15 @@ void export_geometry(const TreeLayout& t, lpm6cu_geometry* g) {
 Tree build_device_tree(const lpm6cu_prefix* rules, uint64_t n, uint32_t default_nh,
                        const lpm6cu_build_opts* opts) {
   IntervalBuildOptions io;
-  u32 vb = 0;
+  u32 vb = 0, lf = kLeafAuto;
   if (opts) {
     io.merge_adjacent = opts->merge_adjacent != 0;
     vb = opts->value_bytes;
+    lf = opts->leaf_format;
   }
   auto prefixes = to_prefixes(rules, n);
   IntervalMap map = build_intervals(std::span<const Prefix>(prefixes), default_nh, io);
-  return build_tree(map, vb);
+  return build_tree(map, vb, lf);
 }
 
 }  // namespace lpm6::capi
@@ -106,19 +108,33 @@ int lpm6_build_intervals(const lpm6cu_prefix* rules, uint64_t n, uint32_t defaul
 }
 
 int lpm6_plan_layout(uint64_t m, uint32_t value_bytes, lpm6cu_geometry* g) {
-  return guard([&] { export_geometry(plan_layout(m, value_bytes), g); });
+  return lpm6_plan_layout_ex(m, value_bytes, kLeafAuto, g);
+}
+
+int lpm6_plan_layout_ex(uint64_t m, uint32_t value_bytes, uint32_t leaf_format, lpm6cu_geometry* g) {
+  return guard([&] {
+    if (!g) throw Error(Errc::InvalidArgument, "NULL geometry");
+    export_geometry(plan_layout(m, value_bytes, leaf_format), g);
+  });
 }
 
 int lpm6_build_tree(const uint64_t* boundaries, const uint32_t* next_hops, uint64_t m,
                     uint32_t default_nh, uint32_t value_bytes, lpm6cu_geometry* g, uint64_t* lines,
                     uint32_t* leaf_values) {
+  return lpm6_build_tree_ex(boundaries, next_hops, m, default_nh, value_bytes, kLeafAuto, g, lines, leaf_values);
+}
+
+int lpm6_build_tree_ex(const uint64_t* boundaries, const uint32_t* next_hops, uint64_t m,
+                       uint32_t default_nh, uint32_t value_bytes, uint32_t leaf_format, lpm6cu_geometry* g,
+                       uint64_t* lines, uint32_t* leaf_values) {
   return guard([&] {
+    if (!g) throw Error(Errc::InvalidArgument, "NULL geometry");
     if (m < 1 || !boundaries || !next_hops) throw Error(Errc::InvalidArgument, "empty interval map");
     IntervalMap map;
     map.boundaries.assign(boundaries, boundaries + m);
     map.next_hops.assign(next_hops, next_hops + m);
     map.default_next_hop = default_nh;
-    Tree t = build_tree(map, value_bytes);
+    Tree t = build_tree(map, value_bytes, leaf_format);
     export_geometry(t.g, g);
     if (lines) std::memcpy(lines, t.lines.data(), t.lines.size() * sizeof(u64));
     if (leaf_values) std::memcpy(leaf_values, t.leaf_values.data(), t.leaf_values.size() * sizeof(u32));

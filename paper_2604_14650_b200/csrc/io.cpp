@@ -97,7 +97,7 @@ int lpm6_memory_footprint(const lpm6cu_geometry* g, lpm6cu_footprint* out) {
     if (!g || !out) throw Error(Errc::InvalidArgument, "NULL argument");
     std::memset(out, 0, sizeof *out);
     out->internal_bytes = g->level_start[g->depth] * 8;
-    out->leaf_bytes = g->leaf_nodes * 128;  // next hops are inside the leaf lines
+    out->leaf_bytes = g->leaf_nodes * (g->leaf_words ? g->leaf_words : 16) * 8;  // next hops are inside the leaves
     out->value_bytes = 0;
     out->image_bytes = (g->total_words - g->image_start) * 8;
     out->total_bytes = g->total_words * 8;

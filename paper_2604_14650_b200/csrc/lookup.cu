@@ -257,7 +257,7 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
     if (!slot.valid) {
       KernelFn fn = pick_kernel(static_cast<int>(f->g.value_bytes), static_cast<int>(f->g.depth),
                                 static_cast<int>(tiles), threads, static_cast<int>(minb), f->d_err != nullptr, input,
-                                leafs, texl_mode, leaftex);
+                                leafs, texl_mode, leaftex, f->g.leaf_words == kHalfLeafWords);
       if (!fn) throw Error(Errc::InvalidArgument, "no kernel instantiated for this configuration");
       // The attribute belongs to the kernel, which every FIB of this depth and
       // next-hop width shares: always set it to the device's opt-in maximum, never
@@ -317,12 +317,16 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
 lpm6cu_fib* new_fib(int device, const lpm6cu_geometry* g) {
   if (!g) throw Error(Errc::InvalidArgument, "geometry is NULL");
   if (g->k != kNodeKeys || g->b != kNodeKeys + 1) throw Error(Errc::InvalidArgument, "the kernels take k = 15, b = 16");
-  if (g->leaf_keys != leaf_keys_for(g->value_bytes)) throw Error(Errc::InvalidArgument, "leaf_keys mismatch");
+  const unsigned lw = g->leaf_words ? g->leaf_words : kLineWords;  // 0: a geometry from before leaf_words
+  if (lw == kLineWords ? g->leaf_keys != leaf_keys_for(g->value_bytes)
+                       : (lw != kHalfLeafWords || g->leaf_keys != kHalfLeafKeys || g->value_bytes != 2))
+    throw Error(Errc::InvalidArgument, "leaf_keys / leaf_words mismatch");
+  if (lw != kLineWords && g->leaf_image) throw Error(Errc::InvalidArgument, "a leaf image needs full leaf lines");
   if (g->depth > kMaxKernelDepth) throw Error(Errc::InvalidArgument, "tree depth above 7");
   if (g->value_bytes != 1 && g->value_bytes != 2 && g->value_bytes != 4)
     throw Error(Errc::InvalidArgument, "value_bytes must be 1, 2 or 4");
   // The geometry must describe a line array that holds what the kernels will read.
-  if (g->image_levels > g->depth || g->level_start[g->depth] + g->leaf_nodes * kLineWords > g->image_start)
+  if (g->image_levels > g->depth || g->level_start[g->depth] + g->leaf_nodes * lw > g->image_start)
     throw Error(Errc::InvalidArgument, "inconsistent geometry (levels / image offset)");
   const unsigned imaged = g->leaf_image ? g->depth + 1 : g->image_levels;
   if (g->image_start + image_bytes_of(*g, imaged) / 8 > g->total_words)
@@ -335,6 +339,7 @@ lpm6cu_fib* new_fib(int device, const lpm6cu_geometry* g) {
   auto f = std::make_unique<lpm6cu_fib>();
   f->device = device;
   f->g = *g;
+  f->g.leaf_words = lw;
   check_cuda(cudaDeviceGetAttribute(&f->num_sms, cudaDevAttrMultiProcessorCount, device), "attr");
   int optin = 0;
   check_cuda(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device), "attr");
@@ -368,7 +373,10 @@ void load_root(lpm6cu_fib* f) {
       }
     }
   }
-  check_cuda(cudaMemcpy(f->root, f->d_lines, sizeof f->root, cudaMemcpyDeviceToHost), "read root line");
+  // The root line (a half-line leaf when the whole tree is one leaf: fewer than 128 bytes).
+  std::memset(f->root, 0xFF, sizeof f->root);
+  const size_t root_bytes = std::min<size_t>(sizeof f->root, static_cast<size_t>(f->g.total_words) * 8);
+  check_cuda(cudaMemcpy(f->root, f->d_lines, root_bytes, cudaMemcpyDeviceToHost), "read root line");
   f->root_ready = true;
 }
 

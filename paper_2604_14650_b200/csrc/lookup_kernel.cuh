@@ -69,9 +69,7 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 #ifndef LPM6_TEX_SECTORS
 #define LPM6_TEX_SECTORS 1
 #endif
-#ifndef LPM6_HALF_PROBE
-#define LPM6_HALF_PROBE 0
-#endif
+
 
 // ---- PTX helpers ------------------------------------------------------------
 
@@ -198,6 +196,19 @@ __device__ __forceinline__ void tex_line_quarter(unsigned long long tex, unsigne
   w[3] = static_cast<unsigned>(b2) | (static_cast<unsigned long long>(static_cast<unsigned>(b3)) << 32);
 }
 
+// Half-line leaves: 16 bytes per lane (words 2j, 2j+1), by a 16-byte load or one
+// texture fetch; w[2..3] are not used.
+__device__ __forceinline__ void ld_half_leaf(const unsigned long long* p, unsigned long long (&w)[4]) {
+  asm volatile("ld.global.nc.v2.u64 {%0,%1}, [%2];" : "=l"(w[0]), "=l"(w[1]) : "l"(p));
+}
+__device__ __forceinline__ void tex_half_leaf(unsigned long long tex, unsigned texel, unsigned long long (&w)[4]) {
+  int a0, a1, a2, a3;
+  asm volatile("tex.1d.v4.s32.s32 {%0,%1,%2,%3}, [%4, {%5}];"
+               : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3) : "l"(tex), "r"(texel));
+  w[0] = static_cast<unsigned>(a0) | (static_cast<unsigned long long>(static_cast<unsigned>(a1)) << 32);
+  w[1] = static_cast<unsigned>(a2) | (static_cast<unsigned long long>(static_cast<unsigned>(a3)) << 32);
+}
+
 __device__ __forceinline__ void ld_line_quarter(const unsigned long long* p, unsigned long long (&w)[4]) {
   asm volatile("ld.global.nc.L2::evict_last.v4.u64 {%0,%1,%2,%3}, [%4];"
                : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
@@ -287,9 +298,11 @@ __device__ __forceinline__ unsigned group_rank(unsigned long long q, const unsig
 // ballot form's compare + VOTE + LOP + POPC + add (6); the reduction costs two
 // SHFL + two adds per four queries. Lane j's key slots t < 2 / t >= 2 count only
 // when lo / hi is all-ones (leaf lines: slots past kL hold next hops, not keys).
-template <int NS, bool MASKED>
+template <int NS, bool MASKED, int NK = 4>
 __device__ __forceinline__ void group_ranks(const unsigned long long (&qk)[NS], const unsigned long long (&w)[NS][4],
                                             unsigned lo, unsigned hi, unsigned (&r)[NS]) {
+  // NK keys per lane (4: a 128-byte line, 2: a half-line leaf, where `lo` masks
+  // the lane's whole count)
   constexpr int NA = (NS + 3) / 4;
   unsigned acc[NA], acc_hi[NA];
 #pragma unroll
@@ -297,7 +310,7 @@ __device__ __forceinline__ void group_ranks(const unsigned long long (&qk)[NS], 
 #pragma unroll
   for (int s = 0; s < NS; ++s) {
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
+    for (int t = 0; t < NK; ++t) {
       unsigned& dst = (MASKED && t >= 2) ? acc_hi[s / 4] : acc[s / 4];
       asm("{\n\t.reg .pred p;\n\tsetp.ge.u64 p, %1, %2;\n\t@p add.u32 %0, %0, %3;\n\t}"
           : "+r"(dst)
@@ -307,6 +320,7 @@ __device__ __forceinline__ void group_ranks(const unsigned long long (&qk)[NS], 
 #pragma unroll
   for (int a = 0; a < NA; ++a) {
     if (MASKED) acc[a] = (acc[a] & lo) + (acc_hi[a] & hi);
+    if (!MASKED && NK == 2) acc[a] &= lo;
     acc[a] += __shfl_xor_sync(kFull, acc[a], 1);
     acc[a] += __shfl_xor_sync(kFull, acc[a], 2);
   }
@@ -358,6 +372,15 @@ __device__ __forceinline__ unsigned leaf_value(const unsigned long long (&w)[4],
 #endif
   const unsigned v = static_cast<unsigned>(x >> ((o & 7u) * 8u));
   return VB == 1 ? (v & 0xFFu) : VB == 2 ? (v & 0xFFFFu) : v;
+}
+
+// Next hop of ordinal `ord` of a half-line leaf from lane 3's words 6-7 (w[0], w[1]).
+template <int VB>
+__device__ __forceinline__ unsigned half_leaf_value(const unsigned long long (&w)[4], unsigned ord) {
+  const unsigned o = ord * VB;  // byte offset within words 6-7
+  const unsigned long long x = sel64(o >= 8u, w[1], w[0]);
+  const unsigned v = static_cast<unsigned>(x >> ((o & 7u) * 8u));
+  return VB == 1 ? (v & 0xFFu) : (v & 0xFFFFu);
 }
 
 template <int VB>
@@ -425,7 +448,7 @@ __device__ __forceinline__ unsigned leaf_search_smem(const unsigned long long* l
 // with 2), so the host picks the line path by measurement
 // (lpm6cu_fib_tune_line_path).
 template <int DEPTH, int VB, int TILES, int THREADS, int MINB, bool CHECKED, int INPUT = kInAddr, bool LEAFS = false,
-          int TEXL = 0, int LEAFTEX = 0>
+          int TEXL = 0, int LEAFTEX = 0, bool HALF = false>
 __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const LookupParams p) {
   using F = LeafFmt<VB>;
   // Texture leaf fetches as sector-disjoint halves (tex_line_quarter) for 1-byte next
@@ -642,7 +665,42 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
 #endif
     }
     unsigned leafn[INPUT == kInKeyOrd ? NS : 1];  // kInKeyOrd: leaf node of each query
-    {  // the leaf line: ordinal = rank - 1
+    constexpr bool half = HALF;  // the FIB's leaf format (half-line leaves: 2-byte next hops)
+    if constexpr (half) {  // half-line leaves (layout.hpp): lane j reads words 2j, 2j+1 of its leaf
+      const unsigned line_w = static_cast<unsigned>(p.level_start[DEPTH]);
+      if (CHECKED) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+          if (nd[s] >= p.level_nodes[DEPTH]) {
+            violations |= 2u;
+            nd[s] = 0;
+          }
+      }
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        // 16 bytes per lane: one texture fetch, or one 16-byte load
+        if (LEAFTEX == 1 || LEAFTEX == 3 || (LEAFTEX == 2 && s >= NS / 2))
+          tex_half_leaf(p.tex, ((line_w + nd[s] * kHalfLeafWords) >> 1) + j, w[s]);
+        else
+          ld_half_leaf(p.lines + line_w + nd[s] * kHalfLeafWords + 2u * j, w[s]);
+      }
+      if constexpr (INPUT == kInKeyOrd) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) leafn[s] = nd[s];
+      }
+      if (CHECKED) {
+#pragma unroll
+        for (int t = 0; t < TILES; ++t)
+          if ((st * TILES + t) * 32ull + lane < p.n) ++visits;
+      }
+      unsigned r[NS];
+      group_ranks<NS, false, 2>(qk, w, j < 3u ? ~0u : 0u, 0u, r);  // lane 3 holds the next hops
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        if (CHECKED && r[s] == 0) violations |= 4u;
+        nd[s] = CHECKED && r[s] == 0 ? 0u : r[s] - 1u;
+      }
+    } else {  // the leaf line: ordinal = rank - 1
       const unsigned line_w = static_cast<unsigned>(p.level_start[DEPTH]);
       const unsigned base_w = line_w + j * 4u;
       if (CHECKED) {
@@ -657,31 +715,13 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
       for (int s = 0; s < NS; ++s) {
         // LEAFTEX 1: every slot through the texture pipe; 2: the upper half of the
         // group's slots (compile-time split, both pipes busy in one warp).
-#if !LPM6_HALF_PROBE
         if (LEAFTEX == 1 || LEAFTEX == 3 || (LEAFTEX == 2 && s >= NS / 2))
-#endif
           // sector-disjoint fetches (kLeafSectors): for 1-byte next hops the leaf
           // keeps the same key slots and value lane in both orders (the values are
           // words 14-15 = lane 3's second texel either way)
-#if LPM6_HALF_PROBE  // timing experiment only (wrong answers): a 64-byte leaf read per query
-        {
-          if (LEAFTEX == 1 || LEAFTEX == 3 || (LEAFTEX == 2 && s >= NS / 2)) {
-            int a0, a1, a2, a3;
-            asm volatile("tex.1d.v4.s32.s32 {%0,%1,%2,%3}, [%4, {%5}];"
-                         : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3) : "l"(p.tex), "r"(((line_w + nd[s] * 16u) >> 1) + j));
-            w[s][0] = static_cast<unsigned>(a0) | (static_cast<unsigned long long>(static_cast<unsigned>(a1)) << 32);
-            w[s][1] = static_cast<unsigned>(a2) | (static_cast<unsigned long long>(static_cast<unsigned>(a3)) << 32);
-          } else {
-            asm volatile("ld.global.nc.v2.u64 {%0,%1}, [%2];"
-                         : "=l"(w[s][0]), "=l"(w[s][1]) : "l"(p.lines + line_w + nd[s] * 16u + 2u * j));
-          }
-          w[s][2] = w[s][3] = ~0ull;
-        }
-#else
           tex_line_quarter<kLeafSectors>(p.tex, (line_w + nd[s] * 16u) >> 1, j, w[s]);
         else
           ld_line_quarter(p.lines + (base_w + nd[s] * 16u), w[s]);
-#endif
       }
       if constexpr (INPUT == kInKeyOrd) {
 #pragma unroll
@@ -715,16 +755,27 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
     if constexpr (INPUT == kInKeyOrd) {  // lane j stores the ordinal of its own query (4t + j of the group)
 #pragma unroll
       for (int t = 0; t < TILES; ++t) {
-        unsigned o = leafn[4 * t] * F::kL + nd[4 * t];
+        const unsigned kl = half ? kHalfLeafKeys : static_cast<unsigned>(F::kL);
+        unsigned o = leafn[4 * t] * kl + nd[4 * t];
 #pragma unroll
-        for (int s = 1; s < 4; ++s) o = j == static_cast<unsigned>(s) ? leafn[4 * t + s] * F::kL + nd[4 * t + s] : o;
+        for (int s = 1; s < 4; ++s) o = j == static_cast<unsigned>(s) ? leafn[4 * t + s] * kl + nd[4 * t + s] : o;
         const unsigned long long qi = (st * TILES + t) * 32ull + lane;
         if (qi < p.n) asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p.ord + qi), "r"(o));
       }
       if (p.out == nullptr) continue;  // ordinals only
     }
     // Leaf values: the value lane extracts the group's next hops and stores them.
-    if (j == static_cast<unsigned>(F::kValueLane)) {
+    if constexpr (half) {
+      if (j == 3u) {  // half-line leaves: lane 3 holds words 6-7, the next hops
+#pragma unroll
+        for (int t = 0; t < TILES; ++t) {
+          unsigned v[4];
+#pragma unroll
+          for (int s = 0; s < 4; ++s) v[s] = half_leaf_value<VB>(w[4 * t + s], nd[4 * t + s]);
+          store_group<VB>(p, (st * TILES + t) * 32ull + gbase, v);
+        }
+      }
+    } else if (j == static_cast<unsigned>(F::kValueLane)) {
 #pragma unroll
       for (int t = 0; t < TILES; ++t) {
         unsigned v[4];
@@ -746,32 +797,36 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
 // Instantiated shapes: (queries per lane, min CTAs per SM) for every depth; one
 // next-hop width per translation unit (lookup_vb{1,2,4}.cu), so the ~150 kernels
 // of each width compile in parallel. bench.py --sweep measures the shapes.
-template <int VB, int INPUT, int TEXL, int LEAFTEX>
+template <int VB, int INPUT, int TEXL, int LEAFTEX, bool HALF>
 KernelFn pick_depth_texl(int depth) {
   switch (depth) {
-    case 1: return lpm6_lookup_kernel<1, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX>;
-    case 2: return lpm6_lookup_kernel<2, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX>;
-    case 3: return lpm6_lookup_kernel<3, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX>;
-    case 4: return lpm6_lookup_kernel<4, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX>;
-    case 5: return lpm6_lookup_kernel<5, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX>;
-    case 6: return lpm6_lookup_kernel<6, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX>;
-    case 7: return lpm6_lookup_kernel<7, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX>;
+    case 1: return lpm6_lookup_kernel<1, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF>;
+    case 2: return lpm6_lookup_kernel<2, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF>;
+    case 3: return lpm6_lookup_kernel<3, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF>;
+    case 4: return lpm6_lookup_kernel<4, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF>;
+    case 5: return lpm6_lookup_kernel<5, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF>;
+    case 6: return lpm6_lookup_kernel<6, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF>;
+    case 7: return lpm6_lookup_kernel<7, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF>;
     default: return nullptr;
   }
 }
 
 // Leaf lines through the texture pipe (default shape, unchecked, address / key input).
 // texl: internal-level mode (0 LSU, 1 texture, 2 split); mode: leaf mode (1 texture,
-// 2 split). Instantiated: texl 0/1 with either leaf mode, texl 2 with texture leaves.
-template <int VB, int INPUT>
+// 2 split, 3 texture with the select extraction of 1-byte next hops). Instantiated:
+// texl 0/1 with leaf modes 1 and 2, texl 2 with texture leaves, mode 3 for VB = 1.
+template <int VB, int INPUT, bool HALF>
 KernelFn pick_leaftex(int depth, int texl, int mode) {
   if (mode == 3) {  // texture leaves with the select extraction: 1-byte next hops only
-    if constexpr (VB == 1) return texl == 1 ? pick_depth_texl<VB, INPUT, 1, 3>(depth) : texl == 0 ? pick_depth_texl<VB, INPUT, 0, 3>(depth) : nullptr;
+    if constexpr (VB == 1 && !HALF)
+      return texl == 1 ? pick_depth_texl<VB, INPUT, 1, 3, HALF>(depth)
+             : texl == 0 ? pick_depth_texl<VB, INPUT, 0, 3, HALF>(depth) : nullptr;
     return nullptr;
   }
-  if (texl == 2) return mode == 1 ? pick_depth_texl<VB, INPUT, 2, 1>(depth) : nullptr;
-  if (mode == 2) return texl ? pick_depth_texl<VB, INPUT, 1, 2>(depth) : pick_depth_texl<VB, INPUT, 0, 2>(depth);
-  return texl ? pick_depth_texl<VB, INPUT, 1, 1>(depth) : pick_depth_texl<VB, INPUT, 0, 1>(depth);
+  if (texl == 2) return mode == 1 ? pick_depth_texl<VB, INPUT, 2, 1, HALF>(depth) : nullptr;
+  if (mode == 2)
+    return texl ? pick_depth_texl<VB, INPUT, 1, 2, HALF>(depth) : pick_depth_texl<VB, INPUT, 0, 2, HALF>(depth);
+  return texl ? pick_depth_texl<VB, INPUT, 1, 1, HALF>(depth) : pick_depth_texl<VB, INPUT, 0, 1, HALF>(depth);
 }
 
 template <int VB, bool CHECKED>
@@ -785,67 +840,81 @@ KernelFn pick_depth_leafs(int depth) {
   }
 }
 
-template <int VB, int TILES, int THREADS, int MINB, bool CHECKED = false, int INPUT = kInAddr>
+template <int VB, int TILES, int THREADS, int MINB, bool CHECKED = false, int INPUT = kInAddr, bool HALF = false>
 KernelFn pick_depth(int depth) {
   switch (depth) {
-    case 0: return lpm6_lookup_kernel<0, VB, TILES, THREADS, MINB, CHECKED, INPUT>;
-    case 1: return lpm6_lookup_kernel<1, VB, TILES, THREADS, MINB, CHECKED, INPUT>;
-    case 2: return lpm6_lookup_kernel<2, VB, TILES, THREADS, MINB, CHECKED, INPUT>;
-    case 3: return lpm6_lookup_kernel<3, VB, TILES, THREADS, MINB, CHECKED, INPUT>;
-    case 4: return lpm6_lookup_kernel<4, VB, TILES, THREADS, MINB, CHECKED, INPUT>;
-    case 5: return lpm6_lookup_kernel<5, VB, TILES, THREADS, MINB, CHECKED, INPUT>;
-    case 6: return lpm6_lookup_kernel<6, VB, TILES, THREADS, MINB, CHECKED, INPUT>;
-    case 7: return lpm6_lookup_kernel<7, VB, TILES, THREADS, MINB, CHECKED, INPUT>;
+    case 0: return lpm6_lookup_kernel<0, VB, TILES, THREADS, MINB, CHECKED, INPUT, false, 0, 0, HALF>;
+    case 1: return lpm6_lookup_kernel<1, VB, TILES, THREADS, MINB, CHECKED, INPUT, false, 0, 0, HALF>;
+    case 2: return lpm6_lookup_kernel<2, VB, TILES, THREADS, MINB, CHECKED, INPUT, false, 0, 0, HALF>;
+    case 3: return lpm6_lookup_kernel<3, VB, TILES, THREADS, MINB, CHECKED, INPUT, false, 0, 0, HALF>;
+    case 4: return lpm6_lookup_kernel<4, VB, TILES, THREADS, MINB, CHECKED, INPUT, false, 0, 0, HALF>;
+    case 5: return lpm6_lookup_kernel<5, VB, TILES, THREADS, MINB, CHECKED, INPUT, false, 0, 0, HALF>;
+    case 6: return lpm6_lookup_kernel<6, VB, TILES, THREADS, MINB, CHECKED, INPUT, false, 0, 0, HALF>;
+    case 7: return lpm6_lookup_kernel<7, VB, TILES, THREADS, MINB, CHECKED, INPUT, false, 0, 0, HALF>;
     default: return nullptr;
   }
 }
 
-// The kernel for one next-hop width (see pick_kernel in lookup_params.hpp). The
-// checked variant exists for the default shape.
-template <int VB>
-KernelFn pick_kernel_t(const PickArgs& a) {
+// The kernels of one leaf format. HALF (half-line leaves, 2-byte next hops only) is
+// instantiated for the default shape: every input format, checked and unchecked,
+// every line path; the other shapes exist for full leaf lines.
+template <int VB, bool HALF>
+KernelFn pick_kernel_fmt(const PickArgs& a) {
   const int depth = a.depth;
   const bool dflt = a.tiles == 1 && a.threads == 1024 && a.minb == 1;
   if (a.leaftex) {  // default shape, unchecked, no leaf image, depth >= 1
     if (a.leafs || a.checked || !dflt) return nullptr;
     switch (a.input) {
-      case kInAddr: return pick_leaftex<VB, kInAddr>(depth, a.texl, a.leaftex);
-      case kInKey: return pick_leaftex<VB, kInKey>(depth, a.texl, a.leaftex);
+      case kInAddr: return pick_leaftex<VB, kInAddr, HALF>(depth, a.texl, a.leaftex);
+      case kInKey: return pick_leaftex<VB, kInKey, HALF>(depth, a.texl, a.leaftex);
       default: return nullptr;
     }
   }
   if (a.texl) {  // internal L2 levels via the texture pipe: default shape, unchecked
     if (a.leafs || a.checked || !dflt) return nullptr;
     switch (a.input) {
-      case kInAddr: return pick_depth_texl<VB, kInAddr, 1, 0>(depth);
-      case kInKey: return pick_depth_texl<VB, kInKey, 1, 0>(depth);
-      case kInPacket: return pick_depth_texl<VB, kInPacket, 1, 0>(depth);
+      case kInAddr: return pick_depth_texl<VB, kInAddr, 1, 0, HALF>(depth);
+      case kInKey: return pick_depth_texl<VB, kInKey, 1, 0, HALF>(depth);
+      case kInPacket: return pick_depth_texl<VB, kInPacket, 1, 0, HALF>(depth);
       default: return nullptr;  // kInKeyOrd: LSU loads
     }
   }
   if (a.leafs) {  // leaf image: address input, default shape, depth <= kMaxLeafImageDepth
-    if (a.input != kInAddr || !dflt) return nullptr;
+    if (HALF || a.input != kInAddr || !dflt) return nullptr;
     return a.checked ? pick_depth_leafs<VB, true>(depth) : pick_depth_leafs<VB, false>(depth);
   }
   if (a.input != kInAddr) {  // key / packet input: the default shape, unchecked and checked
     if (!dflt) return nullptr;
     if (a.input == kInKey)
-      return a.checked ? pick_depth<VB, 1, 1024, 1, true, kInKey>(depth) : pick_depth<VB, 1, 1024, 1, false, kInKey>(depth);
+      return a.checked ? pick_depth<VB, 1, 1024, 1, true, kInKey, HALF>(depth)
+                       : pick_depth<VB, 1, 1024, 1, false, kInKey, HALF>(depth);
     if (a.input == kInPacket)
-      return a.checked ? pick_depth<VB, 1, 1024, 1, true, kInPacket>(depth)
-                       : pick_depth<VB, 1, 1024, 1, false, kInPacket>(depth);
+      return a.checked ? pick_depth<VB, 1, 1024, 1, true, kInPacket, HALF>(depth)
+                       : pick_depth<VB, 1, 1024, 1, false, kInPacket, HALF>(depth);
     if (a.input == kInKeyOrd)
-      return a.checked ? pick_depth<VB, 1, 1024, 1, true, kInKeyOrd>(depth)
-                       : pick_depth<VB, 1, 1024, 1, false, kInKeyOrd>(depth);
+      return a.checked ? pick_depth<VB, 1, 1024, 1, true, kInKeyOrd, HALF>(depth)
+                       : pick_depth<VB, 1, 1024, 1, false, kInKeyOrd, HALF>(depth);
     return nullptr;
   }
-  if (a.checked) return dflt ? pick_depth<VB, 1, 1024, 1, true>(depth) : nullptr;
-  if (a.tiles == 1 && a.threads == 256 && a.minb == 0) return pick_depth<VB, 1, 256, 0>(depth);
-  if (a.tiles == 1 && a.threads == 256 && a.minb == 4) return pick_depth<VB, 1, 256, 4>(depth);
-  if (a.tiles == 2 && a.threads == 256 && a.minb == 0) return pick_depth<VB, 2, 256, 0>(depth);
-  if (a.tiles == 1 && a.threads == 512 && a.minb == 2) return pick_depth<VB, 1, 512, 2>(depth);
-  if (dflt) return pick_depth<VB, 1, 1024, 1>(depth);
+  if (a.checked) return dflt ? pick_depth<VB, 1, 1024, 1, true, kInAddr, HALF>(depth) : nullptr;
+  if (dflt) return pick_depth<VB, 1, 1024, 1, false, kInAddr, HALF>(depth);
+  if constexpr (!HALF) {
+    if (a.tiles == 1 && a.threads == 256 && a.minb == 0) return pick_depth<VB, 1, 256, 0>(depth);
+    if (a.tiles == 1 && a.threads == 256 && a.minb == 4) return pick_depth<VB, 1, 256, 4>(depth);
+    if (a.tiles == 2 && a.threads == 256 && a.minb == 0) return pick_depth<VB, 2, 256, 0>(depth);
+    if (a.tiles == 1 && a.threads == 512 && a.minb == 2) return pick_depth<VB, 1, 512, 2>(depth);
+  }
   return nullptr;
+}
+
+// The kernel for one next-hop width (see pick_kernel in lookup_params.hpp).
+template <int VB>
+KernelFn pick_kernel_t(const PickArgs& a) {
+  if (a.half) {
+    if constexpr (VB == 2) return pick_kernel_fmt<VB, true>(a);
+    return nullptr;
+  }
+  return pick_kernel_fmt<VB, false>(a);
 }
 
 }  // namespace

@@ -51,6 +51,7 @@ struct PickArgs {
   int input = kInAddr;
   bool leafs = false;
   int texl = 0, leaftex = 0;
+  bool half = false;  // half-line leaves (layout.hpp kHalfLeafWords; 2-byte next hops)
 };
 
 KernelFn pick_kernel_vb1(const PickArgs& a);  // lookup_vb1.cu
@@ -59,7 +60,8 @@ KernelFn pick_kernel_vb4(const PickArgs& a);  // lookup_vb4.cu
 
 // nullptr when that combination is not instantiated.
 inline KernelFn pick_kernel(int vb, int depth, int tiles, int threads, int minb, bool checked = false,
-                            int input = kInAddr, bool leafs = false, int texl = 0, int leaftex = 0) {
+                            int input = kInAddr, bool leafs = false, int texl = 0, int leaftex = 0,
+                            bool half = false) {
   PickArgs a;
   a.depth = depth;
   a.tiles = tiles;
@@ -70,6 +72,7 @@ inline KernelFn pick_kernel(int vb, int depth, int tiles, int threads, int minb,
   a.leafs = leafs;
   a.texl = texl;
   a.leaftex = leaftex;
+  a.half = half;
   switch (vb) {
     case 1: return pick_kernel_vb1(a);
     case 2: return pick_kernel_vb2(a);

@@ -4,13 +4,13 @@
 
 namespace lpm6 {
 
-TreeLayout plan_layout(u64 m, u32 value_bytes) {
-  if (m < 1) throw Error(Errc::InvalidArgument, "a tree needs at least one boundary");
-  if (value_bytes != 1 && value_bytes != 2 && value_bytes != 4)
-    throw Error(Errc::InvalidArgument, "value_bytes must be 1, 2 or 4");
+namespace {
+
+TreeLayout plan_with(u64 m, u32 value_bytes, bool half) {
   TreeLayout g;
   g.value_bytes = value_bytes;
-  g.leaf_keys = leaf_keys_for(value_bytes);
+  g.leaf_keys = half ? kHalfLeafKeys : leaf_keys_for(value_bytes);
+  g.leaf_words = half ? kHalfLeafWords : kLineWords;
   g.num_keys = m;
   u32 d = 0;
   for (unsigned __int128 cap = g.leaf_keys; cap < m; cap *= g.b) ++d;
@@ -23,7 +23,7 @@ TreeLayout plan_layout(u64 m, u32 value_bytes) {
   u64 off = 0;
   for (u32 l = 0; l <= d; ++l) {
     g.level_start[l] = off;
-    off += g.level_nodes[l] * kLineWords;
+    off += g.level_nodes[l] * (l < d ? kLineWords : g.leaf_words);
   }
   // Image of internal levels [0, S) for the largest S <= depth whose image fits the budget.
   u32 s = 0;
@@ -31,7 +31,7 @@ TreeLayout plan_layout(u64 m, u32 value_bytes) {
   g.image_levels = s;
   g.image_start = off;
   g.total_words = off + image_bytes(g, s) / 8;
-  if (s == d && d <= kMaxLeafImageDepth && image_bytes(g, d) + leaf_image_bytes(g) <= kImageMaxBytes) {
+  if (!half && s == d && d <= kMaxLeafImageDepth && image_bytes(g, d) + leaf_image_bytes(g) <= kImageMaxBytes) {
     g.leaf_image = 1;
     g.total_words = leaf_image_start(g) + leaf_image_bytes(g) / 8;
   }
@@ -40,7 +40,24 @@ TreeLayout plan_layout(u64 m, u32 value_bytes) {
   return g;
 }
 
-Tree build_tree(const IntervalMap& map, u32 value_bytes) {
+}  // namespace
+
+TreeLayout plan_layout(u64 m, u32 value_bytes, u32 leaf_format) {
+  if (m < 1) throw Error(Errc::InvalidArgument, "a tree needs at least one boundary");
+  if (value_bytes != 1 && value_bytes != 2 && value_bytes != 4)
+    throw Error(Errc::InvalidArgument, "value_bytes must be 1, 2 or 4");
+  if (leaf_format > kLeafHalf) throw Error(Errc::InvalidArgument, "leaf_format must be 0 (auto), 1 (full) or 2 (half)");
+  if (leaf_format == kLeafHalf && value_bytes != 2)
+    throw Error(Errc::InvalidArgument, "half-line leaves hold 2-byte next hops");
+  const TreeLayout full = plan_with(m, value_bytes, false);
+  if (leaf_format == kLeafFull || value_bytes != 2) return full;
+  const TreeLayout half = plan_with(m, value_bytes, true);
+  if (leaf_format == kLeafHalf) return half;
+  const bool keeps = half.depth == full.depth && half.image_levels == full.image_levels;
+  return keeps && !full.leaf_image && full.image_levels < full.depth ? half : full;
+}
+
+Tree build_tree(const IntervalMap& map, u32 value_bytes, u32 leaf_format) {
   const u64 m = map.size();
   if (m < 1) throw Error(Errc::InvalidArgument, "empty interval map");
   if (map.boundaries.front() != 0) throw Error(Errc::InvalidArgument, "interval map must start at key 0");
@@ -58,7 +75,7 @@ Tree build_tree(const IntervalMap& map, u32 value_bytes) {
                                            std::to_string(value_bytes) + " byte(s)");
 
   Tree t;
-  t.g = plan_layout(m, value_bytes);
+  t.g = plan_layout(m, value_bytes, leaf_format);
   t.g.default_next_hop = map.default_next_hop;
   const TreeLayout& g = t.g;
   const u32 kl = g.leaf_keys;
@@ -77,12 +94,12 @@ Tree build_tree(const IntervalMap& map, u32 value_bytes) {
     span *= g.b;
   }
 
-  // Leaf lines: kL keys (sentinel past m), then kL little-endian next hops
-  // (padding replicates the last real value), then zero padding.
+  // Leaf lines (or half lines): kL keys (sentinel past m), then kL little-endian
+  // next hops (padding replicates the last real value), then zero padding.
   t.leaf_values.resize(g.leaf_nodes * kl);
   u64* leaves = t.lines.data() + g.level_start[g.depth];
   for (u64 n = 0; n < g.leaf_nodes; ++n) {
-    u64* line = leaves + n * kLineWords;
+    u64* line = leaves + n * g.leaf_words;
     unsigned char bytes[128];
     std::memset(bytes, 0, sizeof bytes);
     for (u32 j = 0; j < kl; ++j) {
@@ -93,7 +110,7 @@ Tree build_tree(const IntervalMap& map, u32 value_bytes) {
       std::memcpy(bytes + 8 * j, &key, 8);
       std::memcpy(bytes + 8 * kl + value_bytes * j, &v, value_bytes);
     }
-    std::memcpy(line, bytes, sizeof bytes);
+    std::memcpy(line, bytes, g.leaf_words * 8);
   }
 
   // Shared-memory image: internal levels [0, image_levels), 15 keys per node.

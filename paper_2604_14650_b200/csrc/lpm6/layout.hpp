@@ -38,12 +38,24 @@ inline constexpr u32 kLineWords = 16;  // u64 words per line
 // Keys per leaf line for a next-hop width (leaf = kL keys + kL values <= 128 B).
 constexpr u32 leaf_keys_for(u32 value_bytes) { return value_bytes == 1 ? 14 : value_bytes == 2 ? 12 : 8; }
 
+// Half-line leaves (64 bytes, 2-byte next hops): 6 keys (words 0-5) and their
+// next hops in words 6-7 (12 bytes), so that in a lookup the fourth lane of a 4-lane group holds
+// exactly the values and the other three exactly the keys (16 bytes each). A query
+// then reads one 64-byte leaf instead of a 128-byte one: one texture fetch or one
+// 16-byte load per lane, half the L2 bytes. Used where it keeps the tree's depth and
+// its shared-memory levels (plan_layout's automatic rule), i.e. deep trees whose
+// last internal level is read from L2 anyway (the 1M-prefix C2 FIB).
+inline constexpr u32 kHalfLeafKeys = 6;
+inline constexpr u32 kHalfLeafWords = 8;
+enum LeafFormat : u32 { kLeafAuto = 0, kLeafFull = 1, kLeafHalf = 2 };
+
 struct TreeLayout {
   u32 k = kNodeKeys;    // internal keys per node
   u32 b = kNodeKeys + 1;
   u32 depth = 0;        // internal levels; a lookup visits depth + 1 lines
   u32 value_bytes = 1;  // 1, 2 or 4
   u32 leaf_keys = 14;   // kL
+  u32 leaf_words = kLineWords;  // 16: one 128-byte line per leaf; 8: half-line leaves
   u64 num_keys = 0;     // m, real boundaries
   u64 leaf_nodes = 0;   // ceil(m / kL)
   u64 level_nodes[kMaxLevels] = {};  // reachable nodes per level; level depth = leaves
@@ -101,11 +113,14 @@ struct Tree {
   std::vector<u32> leaf_values;                         // next hop per leaf slot (inspection only)
 };
 
-// Minimal depth with kL * b^depth >= m and the compact level table.
-TreeLayout plan_layout(u64 m, u32 value_bytes);
+// Minimal depth with kL * b^depth >= m and the compact level table. leaf_format:
+// kLeafFull, kLeafHalf (2-byte next hops only), or kLeafAuto = half-line
+// leaves when they leave the depth and the number of shared-memory levels unchanged
+// and the tree has an internal level in L2 (no leaf image), full lines otherwise.
+TreeLayout plan_layout(u64 m, u32 value_bytes, u32 leaf_format = kLeafAuto);
 
 // value_bytes = 0 picks the narrowest of {1, 2, 4} holding every next hop;
 // an explicit width that cannot hold one throws InvalidArgument.
-Tree build_tree(const IntervalMap& map, u32 value_bytes = 0);
+Tree build_tree(const IntervalMap& map, u32 value_bytes = 0, u32 leaf_format = kLeafAuto);
 
 }  // namespace lpm6

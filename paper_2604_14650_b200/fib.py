@@ -168,12 +168,13 @@ class Geometry:
     level_start: list[int]
     default_next_hop: int
     leaf_image: int = 0
+    leaf_words: int = 16  # 16: 128-byte leaf lines; 8: half-line leaves (layout.hpp)
 
     @classmethod
     def from_c(cls, g: Geometry_t) -> "Geometry":
         return cls(g.k, g.b, g.depth, g.value_bytes, g.leaf_keys, g.image_levels, g.num_keys, g.leaf_nodes,
                    g.total_words, g.image_start, list(g.level_nodes), list(g.level_start), g.default_next_hop,
-                   g.leaf_image)
+                   g.leaf_image, g.leaf_words or 16)
 
     def to_c(self) -> Geometry_t:
         g = Geometry_t()
@@ -185,6 +186,7 @@ class Geometry:
             g.level_start[i] = self.level_start[i]
         g.default_next_hop = self.default_next_hop
         g.leaf_image = self.leaf_image
+        g.leaf_words = self.leaf_words
         return g
 
     @property
@@ -208,9 +210,12 @@ def ref_memory_footprint(m: int, k: int = 8) -> dict:
     return {name: getattr(f, name) for name, _ in Footprint_t._fields_}
 
 
-def plan_layout(m: int, value_bytes: int = 1) -> Geometry:
+LEAF_AUTO, LEAF_FULL, LEAF_HALF = 0, 1, 2  # lpm6cu_build_opts.leaf_format
+
+
+def plan_layout(m: int, value_bytes: int = 1, leaf_format: int = LEAF_AUTO) -> Geometry:
     g = Geometry_t()
-    check(lib().lpm6_plan_layout(m, value_bytes, C.byref(g)))
+    check(lib().lpm6_plan_layout_ex(m, value_bytes, leaf_format, C.byref(g)))
     return Geometry.from_c(g)
 
 
@@ -226,21 +231,23 @@ class Tree:
         """The leaf boundary keys in slot order (sentinels past m)."""
         g = self.geometry
         start = g.level_start[g.depth]
-        leaves = self.lines[start: start + g.leaf_nodes * 16].reshape(-1, 16)
+        leaves = self.lines[start: start + g.leaf_nodes * g.leaf_words].reshape(-1, g.leaf_words)
         return leaves[:, : g.leaf_keys].reshape(-1)
 
 
-def build_tree(imap: IntervalMap, value_bytes: int = 0) -> Tree:
-    """Lay out the linearized tree for B200 (csrc/lpm6/layout.cpp; contract S:215-223)."""
+def build_tree(imap: IntervalMap, value_bytes: int = 0, leaf_format: int = LEAF_AUTO) -> Tree:
+    """Lay out the linearized tree for B200 (csrc/lpm6/layout.cpp; contract S:215-223);
+    leaf_format: LEAF_AUTO, LEAF_FULL (128-byte leaf lines) or LEAF_HALF (half-line
+    leaves, 2-byte next hops)."""
     g = Geometry_t()
     b = np.ascontiguousarray(imap.boundaries, np.uint64)
     nh = np.ascontiguousarray(imap.next_hops, np.uint32)
-    check(lib().lpm6_build_tree(b.ctypes.data, nh.ctypes.data, len(b), imap.default_next_hop, value_bytes,
-                                C.byref(g), None, None))
+    check(lib().lpm6_build_tree_ex(b.ctypes.data, nh.ctypes.data, len(b), imap.default_next_hop, value_bytes,
+                                   leaf_format, C.byref(g), None, None))
     lines = np.empty(g.total_words, np.uint64)
     vals = np.empty(g.leaf_nodes * g.leaf_keys, np.uint32)
-    check(lib().lpm6_build_tree(b.ctypes.data, nh.ctypes.data, len(b), imap.default_next_hop, value_bytes,
-                                C.byref(g), lines.ctypes.data, vals.ctypes.data))
+    check(lib().lpm6_build_tree_ex(b.ctypes.data, nh.ctypes.data, len(b), imap.default_next_hop, value_bytes,
+                                   leaf_format, C.byref(g), lines.ctypes.data, vals.ctypes.data))
     return Tree(Geometry.from_c(g), lines, vals)
 
 
@@ -337,8 +344,9 @@ def workload_queries_host(workload: int | str, fib: FibTable, first: int, n: int
     return out
 
 
-def build_opts(merge_adjacent: bool = True, value_bytes: int = 0) -> BuildOpts_t:
+def build_opts(merge_adjacent: bool = True, value_bytes: int = 0, leaf_format: int = LEAF_AUTO) -> BuildOpts_t:
     o = BuildOpts_t()
+    o.leaf_format = leaf_format
     o.merge_adjacent = int(merge_adjacent)
     o.value_bytes = value_bytes
     return o

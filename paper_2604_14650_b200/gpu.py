@@ -58,9 +58,12 @@ class Fib:
 
     # -- construction ---------------------------------------------------------
     @classmethod
-    def build(cls, fib: FibTable, device: int = 0, merge_adjacent: bool = True, value_bytes: int = 0) -> "Fib":
+    def build(cls, fib: FibTable, device: int = 0, merge_adjacent: bool = True, value_bytes: int = 0,
+              leaf_format: int = 0) -> "Fib":
+        """Host build (FibTable -> intervals -> layout) into device memory. leaf_format:
+        0 auto, 1 full 128-byte leaf lines, 2 half-line leaves (2-byte next hops)."""
         h = C.c_void_p()
-        opts = build_opts(merge_adjacent, value_bytes)
+        opts = build_opts(merge_adjacent, value_bytes, leaf_format)
         rules = fib.rules
         check(lib().lpm6cu_fib_build(device, _rules_ptr(rules), len(rules), fib.default_next_hop, C.byref(opts),
                                      C.byref(h)))
@@ -68,10 +71,10 @@ class Fib:
 
     @classmethod
     def build_device(cls, fib: FibTable, device: int = 0, merge_adjacent: bool = True, value_bytes: int = 0,
-                     stream=None) -> "Fib":
+                     stream=None, leaf_format: int = 0) -> "Fib":
         """The same build done on the GPU (csrc/build.cu); bit-identical layout."""
         h = C.c_void_p()
-        opts = build_opts(merge_adjacent, value_bytes)
+        opts = build_opts(merge_adjacent, value_bytes, leaf_format)
         rules = fib.rules
         s = _stream_handle(stream)
         check(lib().lpm6cu_fib_build_device(device, _rules_ptr(rules), len(rules), fib.default_next_hop,
@@ -79,10 +82,10 @@ class Fib:
         return cls(h.value, device)
 
     @classmethod
-    def from_intervals(cls, imap, device: int = 0, value_bytes: int = 0, stream=None) -> "Fib":
+    def from_intervals(cls, imap, device: int = 0, value_bytes: int = 0, stream=None, leaf_format: int = 0) -> "Fib":
         """Layout-only device build from an IntervalMap (build_tree(map), tree.hpp:74)."""
         h = C.c_void_p()
-        opts = build_opts(True, value_bytes)
+        opts = build_opts(True, value_bytes, leaf_format)
         b = np.ascontiguousarray(imap.boundaries, np.uint64)
         nh = np.ascontiguousarray(imap.next_hops, np.uint32)
         check(lib().lpm6cu_fib_build_from_intervals(device, b.ctypes.data, nh.ctypes.data, len(b),

@@ -7,7 +7,7 @@ oracle/_ref is present the reference's own lookup_interval_oracle is checked too
 import numpy as np
 import pytest
 
-from _util import addrs_from_keys, boundary_probe_keys, large_rules, random_fib_rules
+from _util import MASK64, addrs_from_keys, boundary_probe_keys, large_rules, random_fib_rules
 
 pytestmark = pytest.mark.gpu
 
@@ -27,14 +27,15 @@ def run_lookup(cuda, fib_dev, addrs_np):
     return out.cpu().numpy().view({1: np.uint8, 2: np.uint16, 4: np.uint32}[out.element_size()])
 
 
-def check_fib(lpm, orc, cuda, fib, addrs, lanes=LANES, smem_levels=(None, 0, 1, 2, 3, 4, 5, 6, 7)):
+def check_fib(lpm, orc, cuda, fib, addrs, lanes=LANES, smem_levels=(None, 0, 1, 2, 3, 4, 5, 6, 7), value_bytes=0,
+              leaf_format=0):
     imap = lpm.build_intervals(fib)
     st, ob, onh = orc.build_intervals(fib.rules, fib.default_next_hop)
     assert st == 0
     np.testing.assert_array_equal(imap.boundaries, ob)
     np.testing.assert_array_equal(imap.next_hops, onh)
     want = oracle_next_hops(orc, ob, onh, addrs)
-    dev = lpm.Fib.build(fib)
+    dev = lpm.Fib.build(fib, value_bytes=value_bytes, leaf_format=leaf_format)
     for g in lanes:
         for t in smem_levels:
             geo = dev.geometry
@@ -557,3 +558,48 @@ def test_kernel_smem_attribute_shared_across_fibs(lpm, orc, cuda):
         got = run_lookup(cuda, dev, addrs).astype(np.uint32)
         np.testing.assert_array_equal(got, wants[name], err_msg=name)
     assert img(db) >= 1 and img(ds) >= 1
+
+
+@pytest.mark.parametrize("n,dflt", [(1, True), (14, False), (3000, True), (60000, False)])
+def test_half_leaf_fibs_every_mode(lpm, orc, cuda, n, dflt):
+    """Half-line leaves (2-byte next hops, forced on random FIBs of every depth): every
+    smem_levels setting, checked and unchecked (node visits = depth + 1), every line
+    path, 8-byte keys and search_batch ordinals — all against the oracle."""
+    from paper_2604_14650_b200.fib import PREFIX_DTYPE
+    torch = cuda
+    rng = np.random.default_rng(n + 11)
+    rules = random_fib_rules(rng, n, PREFIX_DTYPE, dflt, nest_p=0.4)
+    fib = lpm.FibTable(5, rules)
+    imap = lpm.build_intervals(fib)
+    keys = np.concatenate([boundary_probe_keys(imap.boundaries), rng.integers(0, 2**64, 20000, dtype=np.uint64)])
+    addrs = addrs_from_keys(keys, rng)
+    dev, want = check_fib(lpm, orc, cuda, fib, addrs, value_bytes=2, leaf_format=2)
+    assert dev.geometry.leaf_words == 8
+    da = torch.from_numpy(addrs.view(np.uint8).reshape(-1, 16)).cuda()
+    dk = torch.from_numpy(np.ascontiguousarray(addrs[:, 1]).view(np.int64)).cuda()
+    for lp in (0, 1, 2, 3):
+        dev.set_kernel_config(line_path=lp)
+        got = dev.lookup_batch(da).cpu().numpy().view(np.uint16).astype(np.uint32)
+        gk = dev.lookup_keys(dk).cpu().numpy().view(np.uint16).astype(np.uint32)
+        np.testing.assert_array_equal(got, want, err_msg=f"lp={lp}")
+        np.testing.assert_array_equal(gk, want, err_msg=f"keys lp={lp}")
+    ords, nh = dev.search_batch(dk)
+    want_ord = np.searchsorted(imap.boundaries, np.minimum(keys, np.uint64(MASK64 - 1)), side="right") - 1
+    np.testing.assert_array_equal(ords.cpu().numpy().astype(np.int64), want_ord)
+    dev.close()
+
+
+def test_half_leaf_device_build_matches_host(lpm, cuda):
+    """The device build lays out half-line leaves bit-identically to the host build
+    (forced on a random FIB; automatic on the 1M-prefix C2 FIB)."""
+    from paper_2604_14650_b200.fib import PREFIX_DTYPE
+    rng = np.random.default_rng(5)
+    fibs = [(lpm.FibTable(1, random_fib_rules(rng, 20000, PREFIX_DTYPE, True, nest_p=0.3)), 2),
+            (lpm.workload_fib(2), 0)]
+    from paper_2604_14650_b200.gpu import device_lines
+    for fib, lf in fibs:
+        host = lpm.build_tree(lpm.build_intervals(fib), 2, lf)
+        devb = lpm.Fib.build_device(fib, 0, value_bytes=2, leaf_format=lf)
+        assert host.geometry == devb.geometry and host.geometry.leaf_words == 8
+        np.testing.assert_array_equal(device_lines(devb), host.lines)
+        devb.close()

@@ -28,7 +28,7 @@ def header_functions():
 def test_library_exports_every_declared_symbol(lpm):
     from paper_2604_14650_b200._lib import LIB_PATH, SIGNATURES
     names = header_functions()
-    assert len(names) == len(SIGNATURES) == 60
+    assert len(names) == len(SIGNATURES) == 62
     dll = C.CDLL(str(LIB_PATH))
     for name in names:
         assert hasattr(dll, name), f"{name} declared in include/lpm6cu.h but not exported"
@@ -64,18 +64,26 @@ def walk_layout(tree, keys):
         base = g.level_start[lvl] + node * 16
         nd = lines[base[:, None] + np.arange(g.k)]
         node = node * g.b + (nd <= q[:, None]).sum(axis=1)
-    base = g.level_start[g.depth] + node * 16
+    base = g.level_start[g.depth] + node * g.leaf_words
     lf = lines[base[:, None] + np.arange(g.leaf_keys)]
     ordinal = (lf <= q[:, None]).sum(axis=1) - 1
     assert np.all(ordinal >= 0)
     return tree.leaf_values[node * g.leaf_keys + ordinal]
 
 
-def check_layout(lpm, orc, fib, n_random=20000, seed=0):
+def check_layout(lpm, orc, fib, n_random=20000, seed=0, value_bytes=0, leaf_format=0):
     imap = lpm.build_intervals(fib)
-    tree = lpm.build_tree(imap)
+    tree = lpm.build_tree(imap, value_bytes, leaf_format)
     g = tree.geometry
     m = len(imap)
+    # leaves: 128-byte lines (kL = 14 / 12 / 8) or half lines of 6 keys + 2-byte next hops
+    assert (g.leaf_words, g.leaf_keys) in ((16, {1: 14, 2: 12, 4: 8}[g.value_bytes]), (8, 6))
+    if g.leaf_words == 8:
+        assert g.value_bytes == 2 and g.leaf_image == 0
+        lv = tree.lines[g.level_start[g.depth]: g.level_start[g.depth] + g.leaf_nodes * 8].reshape(-1, 8)
+        vals = lv[:, 6:8].copy().view(np.uint16)[:, :6].reshape(-1)  # words 6-7: the six next hops
+        np.testing.assert_array_equal(vals.astype(np.uint32), tree.leaf_values)
+        assert g.image_start == g.level_start[g.depth] + g.leaf_nodes * 8
     # geometry: 15 separators + pad per internal line, arity 16; minimal depth; compact levels
     assert (g.k, g.b) == (15, 16)
     assert g.leaf_keys * 16 ** g.depth >= m and (g.depth == 0 or g.leaf_keys * 16 ** (g.depth - 1) < m)
@@ -130,6 +138,33 @@ def test_layout_workload_fibs(lpm, orc, kind):
     tree = check_layout(lpm, orc, lpm.workload_fib(kind))
     assert tree.geometry.depth == {0: 2, 1: 4}[kind]
     assert tree.geometry.leaf_image == {0: 1, 1: 0}[kind]  # C0's whole tree fits shared memory
+
+
+def test_half_leaf_layout_c2_auto(lpm, orc):
+    """The 1M-prefix C2 FIB (2-byte next hops, a level in L2) gets half-line leaves by
+    the automatic rule: the same depth (5) and the same four shared-memory levels."""
+    tree = check_layout(lpm, orc, lpm.workload_fib(2), n_random=5000)
+    g = tree.geometry
+    assert g.leaf_words == 8 and g.leaf_keys == 6 and g.depth == 5 and g.image_levels == 4
+    full = lpm.plan_layout(g.num_keys, 2, lpm.fib.LEAF_FULL)
+    assert full.leaf_words == 16 and full.depth == g.depth and full.image_levels == g.image_levels
+    # C1 (1-byte next hops, whole internal tree staged) keeps full lines
+    assert lpm.plan_layout(387232, 1).leaf_words == 16
+    with pytest.raises(lpm.Lpm6Error):
+        lpm.plan_layout(1000, 1, lpm.fib.LEAF_HALF)  # half lines hold 2-byte next hops only
+
+
+@pytest.mark.parametrize("n,dflt", [(0, False), (1, True), (13, False), (14, True), (300, False), (5000, True),
+                                    (40000, True)])
+def test_half_leaf_layout_forced(lpm, orc, n, dflt):
+    """Half-line leaves forced on random FIBs with 2-byte next hops: the layout walk
+    (the kernel's descent restated in numpy) matches the oracle on every boundary."""
+    from paper_2604_14650_b200.fib import PREFIX_DTYPE
+    rng = np.random.default_rng(n + 7)
+    rules = random_fib_rules(rng, n, PREFIX_DTYPE, dflt, nest_p=0.4)
+    tree = check_layout(lpm, orc, lpm.FibTable(3, rules), n_random=3000, value_bytes=2,
+                        leaf_format=lpm.fib.LEAF_HALF)
+    assert tree.geometry.leaf_words == 8
 
 
 @pytest.mark.parametrize("n,dflt", [(0, False), (1, True), (13, False), (14, True), (300, False), (5000, True)])
