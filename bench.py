@@ -328,11 +328,16 @@ def roofline_object(geom, vb, cfg, lps, l2_gbs, smem_gbs, hbm_gbs, hbm_src, work
            "measured": {"l2_gather_gbs": l2_gbs, "smem_gbs": smem_gbs, "hbm_gbs": hbm_gbs}}
     if m:
         clk = sm_mhz or m["sm_clock_mhz"]
-        ceil = 148 * clk * 1e6 / m["lsu_wavefronts_per_query"] / 1e9
+        # both L1TEX data pipes move one wavefront per SM per clock
+        ceil_lsu = 148 * clk * 1e6 / m["lsu_wavefronts_per_query"] / 1e9
+        ceil_tex = 148 * clk * 1e6 / m["tex_wavefronts_per_query"] / 1e9 if m["tex_wavefronts_per_query"] else None
+        ceil = min(c for c in (ceil_lsu, ceil_tex) if c)
         obj.update({"limiter_ncu": f"L1 LSU data pipe {m['lsu_data_pipe_pct']:.1f}% of peak, texture data pipe "
                                    f"{m['tex_data_pipe_pct']:.1f}%, issue {m['issue_active_pct']:.1f}% ({m['capture']})",
                     "l1_wavefront_ceiling_glps": ceil, "frac_of_l1_ceiling": lps / 1e9 / ceil,
+                    "l1_ceilings_glps": {"lsu": ceil_lsu, "tex": ceil_tex},
                     "lsu_wavefronts_per_query": m["lsu_wavefronts_per_query"],
+                    "tex_wavefronts_per_query": m["tex_wavefronts_per_query"],
                     "traffic_per_query": m["dram_bytes_per_query"], "ncu_capture": m["capture"]})
     return obj
 

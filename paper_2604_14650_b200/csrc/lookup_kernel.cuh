@@ -69,6 +69,14 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 #ifndef LPM6_TEX_SECTORS
 #define LPM6_TEX_SECTORS 1
 #endif
+// Half-line leaves: a tile's leaf fetches overlap the next tile's Phase A (1).
+#ifndef LPM6_HALF_PIPE
+#define LPM6_HALF_PIPE 1
+#endif
+// Internal texture lines as sector-disjoint halves too (A/B switch; 0 = lane quarters).
+#ifndef LPM6_INT_SECTORS
+#define LPM6_INT_SECTORS 0
+#endif
 
 
 // ---- PTX helpers ------------------------------------------------------------
@@ -298,8 +306,8 @@ __device__ __forceinline__ unsigned group_rank(unsigned long long q, const unsig
 // ballot form's compare + VOTE + LOP + POPC + add (6); the reduction costs two
 // SHFL + two adds per four queries. Lane j's key slots t < 2 / t >= 2 count only
 // when lo / hi is all-ones (leaf lines: slots past kL hold next hops, not keys).
-template <int NS, bool MASKED, int NK = 4>
-__device__ __forceinline__ void group_ranks(const unsigned long long (&qk)[NS], const unsigned long long (&w)[NS][4],
+template <int NS, bool MASKED, int NK = 4, int WN = 4>
+__device__ __forceinline__ void group_ranks(const unsigned long long (&qk)[NS], const unsigned long long (&w)[NS][WN],
                                             unsigned lo, unsigned hi, unsigned (&r)[NS]) {
   // NK keys per lane (4: a 128-byte line, 2: a half-line leaf, where `lo` masks
   // the lane's whole count)
@@ -375,8 +383,8 @@ __device__ __forceinline__ unsigned leaf_value(const unsigned long long (&w)[4],
 }
 
 // Next hop of ordinal `ord` of a half-line leaf from lane 3's words 6-7 (w[0], w[1]).
-template <int VB>
-__device__ __forceinline__ unsigned half_leaf_value(const unsigned long long (&w)[4], unsigned ord) {
+template <int VB, int WN>
+__device__ __forceinline__ unsigned half_leaf_value(const unsigned long long (&w)[WN], unsigned ord) {
   const unsigned o = ord * VB;  // byte offset within words 6-7
   const unsigned long long x = sel64(o >= 8u, w[1], w[0]);
   const unsigned v = static_cast<unsigned>(x >> ((o & 7u) * 8u));
@@ -512,6 +520,24 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
     mbar_wait(&s_bar, 0);
   }
 
+  // Half-line leaves, one tile per warp: a tile's leaf fetches stay in flight while
+  // the warp runs the next tile's shared-memory levels, and are consumed after them
+  // (the leaf wait was the largest stall on C2, ~12 % of samples at the first compare).
+  constexpr bool PIPE = HALF && !CHECKED && INPUT != kInKeyOrd && TILES == 1 && LPM6_HALF_PIPE;
+  unsigned long long pq[4] = {0, 0, 0, 0};  // PIPE: the pending tile's keys (group slots)
+  unsigned long long pw[4][2];               //       its half-leaf words (16 bytes per lane)
+  unsigned long long pst = ~0ull;            //       its tile index, ~0 = none
+  auto finish_half = [&]() {
+    unsigned r[4];
+    group_ranks<4, false, 2, 2>(pq, pw, j < 3u ? ~0u : 0u, 0u, r);  // lane 3 holds the next hops
+    if (j == 3u) {
+      unsigned v[4];
+#pragma unroll
+      for (int s = 0; s < 4; ++s) v[s] = half_leaf_value<VB, 2>(pw[s], r[s] - 1u);
+      store_group<VB>(p, pst * 32ull + gbase, v);
+    }
+  };
+
   for (unsigned long long st = warp0; st * (32ull * TILES) < p.n; st += nwarps) {
     unsigned long long key[TILES];
     unsigned node[TILES];
@@ -605,6 +631,10 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
       continue;
     }
 
+    if constexpr (PIPE) {
+      if (pst != ~0ull) finish_half();  // the previous tile's leaves, fetched before Phase A
+    }
+
     // Phase B: the group's queries, one 128-byte line per query per level.
     unsigned long long qk[NS];
     unsigned nd[NS];
@@ -643,7 +673,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
         // +8 %); leaves through the texture pipe lose on L2-missing workloads
         // (C1 -17 %), so they stay on the LSU path.
         if (TEXL == 1 || (TEXL == 2 && s < NS / 2))
-          tex_line_quarter<false>(p.tex, (line_w + nd[s] * 16u) >> 1, j, w[s]);
+          tex_line_quarter<LPM6_INT_SECTORS != 0>(p.tex, (line_w + nd[s] * 16u) >> 1, j, w[s]);
         else
           ld_line_quarter(p.lines + (base_w + nd[s] * 16u), w[s]);
       }
@@ -663,6 +693,22 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
 #pragma unroll
       for (int s = 0; s < NS; ++s) nd[s] = nd[s] * 16u + group_rank(qk[s], w[s], 4u, gmask);
 #endif
+    }
+    if constexpr (PIPE) {  // issue this tile's leaf fetches; consumed after the next Phase A
+      const unsigned line_w = static_cast<unsigned>(p.level_start[DEPTH]);
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        unsigned long long w4[4];
+        if (LEAFTEX == 1 || LEAFTEX == 3 || (LEAFTEX == 2 && s >= 2))
+          tex_half_leaf(p.tex, ((line_w + nd[s] * kHalfLeafWords) >> 1) + j, w4);
+        else
+          ld_half_leaf(p.lines + line_w + nd[s] * kHalfLeafWords + 2u * j, w4);
+        pw[s][0] = w4[0];
+        pw[s][1] = w4[1];
+        pq[s] = qk[s];
+      }
+      pst = st;
+      continue;
     }
     unsigned leafn[INPUT == kInKeyOrd ? NS : 1];  // kInKeyOrd: leaf node of each query
     constexpr bool half = HALF;  // the FIB's leaf format (half-line leaves: 2-byte next hops)
@@ -771,7 +817,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
         for (int t = 0; t < TILES; ++t) {
           unsigned v[4];
 #pragma unroll
-          for (int s = 0; s < 4; ++s) v[s] = half_leaf_value<VB>(w[4 * t + s], nd[4 * t + s]);
+          for (int s = 0; s < 4; ++s) v[s] = half_leaf_value<VB, 4>(w[4 * t + s], nd[4 * t + s]);
           store_group<VB>(p, (st * TILES + t) * 32ull + gbase, v);
         }
       }
@@ -784,6 +830,9 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
         store_group<VB>(p, (st * TILES + t) * 32ull + gbase, v);
       }
     }
+  }
+  if constexpr (PIPE) {
+    if (pst != ~0ull) finish_half();
   }
   if (CHECKED) {
     if (violations) atomicOr(p.err, violations);
