@@ -69,10 +69,6 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 #ifndef LPM6_TEX_SECTORS
 #define LPM6_TEX_SECTORS 1
 #endif
-// Half-line leaves: a tile's leaf fetches overlap the next tile's Phase A (1).
-#ifndef LPM6_HALF_PIPE
-#define LPM6_HALF_PIPE 1
-#endif
 // Internal texture lines as sector-disjoint halves too (A/B switch; 0 = lane quarters).
 #ifndef LPM6_INT_SECTORS
 #define LPM6_INT_SECTORS 0
@@ -520,24 +516,6 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
     mbar_wait(&s_bar, 0);
   }
 
-  // Half-line leaves, one tile per warp: a tile's leaf fetches stay in flight while
-  // the warp runs the next tile's shared-memory levels, and are consumed after them
-  // (the leaf wait was the largest stall on C2, ~12 % of samples at the first compare).
-  constexpr bool PIPE = HALF && !CHECKED && INPUT != kInKeyOrd && TILES == 1 && LPM6_HALF_PIPE;
-  unsigned long long pq[4] = {0, 0, 0, 0};  // PIPE: the pending tile's keys (group slots)
-  unsigned long long pw[4][2];               //       its half-leaf words (16 bytes per lane)
-  unsigned long long pst = ~0ull;            //       its tile index, ~0 = none
-  auto finish_half = [&]() {
-    unsigned r[4];
-    group_ranks<4, false, 2, 2>(pq, pw, j < 3u ? ~0u : 0u, 0u, r);  // lane 3 holds the next hops
-    if (j == 3u) {
-      unsigned v[4];
-#pragma unroll
-      for (int s = 0; s < 4; ++s) v[s] = half_leaf_value<VB, 2>(pw[s], r[s] - 1u);
-      store_group<VB>(p, pst * 32ull + gbase, v);
-    }
-  };
-
   for (unsigned long long st = warp0; st * (32ull * TILES) < p.n; st += nwarps) {
     unsigned long long key[TILES];
     unsigned node[TILES];
@@ -631,10 +609,6 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
       continue;
     }
 
-    if constexpr (PIPE) {
-      if (pst != ~0ull) finish_half();  // the previous tile's leaves, fetched before Phase A
-    }
-
     // Phase B: the group's queries, one 128-byte line per query per level.
     unsigned long long qk[NS];
     unsigned nd[NS];
@@ -693,22 +667,6 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
 #pragma unroll
       for (int s = 0; s < NS; ++s) nd[s] = nd[s] * 16u + group_rank(qk[s], w[s], 4u, gmask);
 #endif
-    }
-    if constexpr (PIPE) {  // issue this tile's leaf fetches; consumed after the next Phase A
-      const unsigned line_w = static_cast<unsigned>(p.level_start[DEPTH]);
-#pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        unsigned long long w4[4];
-        if (LEAFTEX == 1 || LEAFTEX == 3 || (LEAFTEX == 2 && s >= 2))
-          tex_half_leaf(p.tex, ((line_w + nd[s] * kHalfLeafWords) >> 1) + j, w4);
-        else
-          ld_half_leaf(p.lines + line_w + nd[s] * kHalfLeafWords + 2u * j, w4);
-        pw[s][0] = w4[0];
-        pw[s][1] = w4[1];
-        pq[s] = qk[s];
-      }
-      pst = st;
-      continue;
     }
     unsigned leafn[INPUT == kInKeyOrd ? NS : 1];  // kInKeyOrd: leaf node of each query
     constexpr bool half = HALF;  // the FIB's leaf format (half-line leaves: 2-byte next hops)
@@ -830,9 +788,6 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
         store_group<VB>(p, (st * TILES + t) * 32ull + gbase, v);
       }
     }
-  }
-  if constexpr (PIPE) {
-    if (pst != ~0ull) finish_half();
   }
   if (CHECKED) {
     if (violations) atomicOr(p.err, violations);
