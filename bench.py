@@ -908,6 +908,13 @@ def main():
         line["sweep"] = sweep
     if extras is not None:
         line["extras"] = extras
+        if "keys8_e2e" in extras:
+            # the same lookups from host buffers of 8-byte keys — the input of the reference's
+            # batched search (search_batch) — i.e. half the PCIe bytes of `e2e`
+            k = extras["keys8_e2e"]
+            line["e2e_keys"] = {"value": k["value"], "unit": k["unit"], "h2d_bytes_per_step": k["h2d_bytes_per_step"],
+                                "d2h_bytes_per_step": k["d2h_bytes_per_step"], "path": k["path"],
+                                "matches_address_path": k["matches_address_path"]}
     if ws > 1 and shared_gpu_mode():
         line["harness_check"] = "LPM6_BENCH_SHARED_GPU: ranks shared GPUs over gloo; not a bench value"
     print(json.dumps(line), flush=True)

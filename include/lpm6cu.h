@@ -118,8 +118,8 @@ typedef struct {
   uint32_t queries_per_lane; /* 32-query tiles each warp carries at once: 1, or 2 at 256 threads */
   uint32_t min_ctas_per_sm;  /* register cap (__launch_bounds__ min blocks): 1 at 1024 threads,
                                 2 at 512, 0 or 4 at 256 */
-  uint32_t line_path;        /* which L1TEX pipe carries the 128-byte L2 lines (address / key
-                                input, default shape, unchecked): 0 = leaves through the LSU,
+  uint32_t line_path;        /* which L1TEX pipe carries the 128-byte L2 lines (address / key /
+                                packet input, default shape, unchecked): 0 = leaves through the LSU,
                                 internal L2 levels through the texture pipe (default); 1 = leaves
                                 through the texture pipe too, faster when leaf lines often hit L1
                                 (skewed traffic); 2 = half of each warp's leaf lines through each

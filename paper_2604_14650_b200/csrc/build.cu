@@ -62,6 +62,31 @@ cudaMemPool_t build_pool(int device) {
   return pools[device];
 }
 
+}  // namespace
+
+// Line arrays of device-built FIBs come from a second private pool that keeps all of
+// its memory: a FibStore commit allocates one and retires another every time, and
+// cudaMalloc / cudaFree map and unmap device memory through the driver, which took
+// 30-80 ms per call in a process holding tens of GB (measured, tools/gpu/run22.sh).
+cudaMemPool_t lpm6::capi::fib_line_pool(int device) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  if (device < 0 || device >= 64) throw Error(Errc::CudaError, "device index out of range");
+  std::lock_guard<std::mutex> lk(mu);
+  if (!pools[device]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    ck(cudaMemPoolCreate(&pools[device], &props), "cudaMemPoolCreate (FIB lines)");
+    uint64_t keep = ~0ull;
+    ck(cudaMemPoolSetAttribute(pools[device], cudaMemPoolAttrReleaseThreshold, &keep), "cudaMemPoolSetAttribute");
+  }
+  return pools[device];
+}
+
+namespace {
+
 // Device buffer owned for the duration of one build (stream-ordered, build_pool).
 struct DBuf {
   void* p = nullptr;
@@ -310,6 +335,7 @@ DeviceIntervals device_intervals(const lpm6cu_prefix* rules, u64d n, unsigned de
   out.nh = DBuf(nc * 4, s);
 
   const BuildStatus init{~0ull, 0, 0};
+  capi::BuildTrace tr("intervals");
   ck(cudaMemcpyAsync(st.p, &init, sizeof init, cudaMemcpyHostToDevice, s), "H2D status");
   if (n)
     extract_kernel<<<blocks_for(n), 256, 0, s>>>(d_rules, n, top.as<u64d>(), len.as<unsigned>(), nh.as<unsigned>(),
@@ -378,7 +404,9 @@ DeviceIntervals device_intervals(const lpm6cu_prefix* rules, u64d n, unsigned de
   ck(cudaMemcpyAsync(&hs, st.p, sizeof hs, cudaMemcpyDeviceToHost, s), "D2H status");
   ck(cudaMemcpyAsync(&out.m, d_m.p, 8, cudaMemcpyDeviceToHost, s), "D2H m");
   ck(cudaMemcpyAsync(&out.max_nh, d_max.p, 4, cudaMemcpyDeviceToHost, s), "D2H max");
+  tr.mark("enqueue");
   ck(cudaStreamSynchronize(s), "device build");
+  tr.mark("sync");
   if (hs.first_bad != ~0ull) {
     const u64d i = hs.first_bad >> 8;
     switch (hs.first_bad & 0xFF) {
@@ -422,14 +450,19 @@ void* device_layout(const DeviceIntervals& iv, u32 vb, u32 leaf_format, uint32_t
     span *= t.b;
   }
   for (int l = 0; l < kMaxLevels; ++l) g.level_start[l] = t.level_start[l];
-  void* lines_p = nullptr;  // long-lived: a plain allocation owned by the FIB handle
-  ck(cudaMalloc(&lines_p, t.total_words * 8), "cudaMalloc lines");
+  void* lines_p = nullptr;  // long-lived: owned by the FIB handle (fib_line_pool, freed by free_fib_lines)
+  BuildTrace tr("layout");
+  int dev = 0;
+  ck(cudaGetDevice(&dev), "cudaGetDevice");
+  ck(cudaMallocFromPoolAsync(&lines_p, t.total_words * 8, fib_line_pool(dev), s), "allocate lines");
+  tr.mark("alloc");
   struct Owned {
     void* p;
+    cudaStream_t s;
     ~Owned() {
-      if (p) cudaFree(p);
+      if (p) cudaFreeAsync(p, s);
     }
-  } lines{lines_p};
+  } lines{lines_p, s};
   ck(cudaMemsetAsync(lines.p, 0xFF, t.total_words * 8, s), "memset lines");  // sentinel everywhere first
   if (t.depth > 0)
     internal_kernel<<<blocks_for(t.level_start[t.depth]), 256, 0, s>>>(g, iv.bnd.as<u64d>(),
@@ -467,8 +500,12 @@ u32 value_bytes_for(const lpm6cu_build_opts* opts, unsigned max_nh) {
 void* device_build_tree(const lpm6cu_prefix* rules, uint64_t n, uint32_t default_nh, const lpm6cu_build_opts* opts,
                         cudaStream_t s, lpm6cu_geometry* geom) {
   const bool merge = opts ? opts->merge_adjacent != 0 : true;
+  BuildTrace tr("device build");
   DeviceIntervals iv = device_intervals(rules, n, default_nh, merge, s);
-  return device_layout(iv, value_bytes_for(opts, iv.max_nh), opts ? opts->leaf_format : 0u, default_nh, s, geom);
+  tr.mark("intervals");
+  void* lines = device_layout(iv, value_bytes_for(opts, iv.max_nh), opts ? opts->leaf_format : 0u, default_nh, s, geom);
+  tr.mark("layout");
+  return lines;
 }
 
 // Step 6 only, from host intervals already validated by the caller (a loaded

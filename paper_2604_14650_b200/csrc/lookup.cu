@@ -79,6 +79,8 @@ struct lpm6cu_fib {
   unsigned long long* d_lines = nullptr;
   unsigned int* d_err = nullptr;  // non-null: checked mode; [0] violation bits, [2..3] u64 node visits
   bool owns = true;
+  bool pooled = false;  // d_lines from capi::fib_line_pool (device builds): cudaFreeAsync, no unmap
+  bool quiesced = false;  // the owner knows no lookup can still read d_lines (FibStore reclaim)
   lpm6cu_kernel_config cfg{};  // resolved
   int num_sms = 0;
   size_t max_smem_optin = 0;
@@ -113,7 +115,16 @@ struct lpm6cu_fib {
     if (tex) cudaDestroyTextureObject(tex);
     if (zc_stream) cudaStreamDestroy(zc_stream);
     if (zc_event) cudaEventDestroy(zc_event);
-    if (owns && d_lines) cudaFree(d_lines);
+    if (owns && d_lines) {
+      if (pooled) {
+        // cudaFree would have waited for the whole device; keep that guarantee for a
+        // plain destroy, and let an owner that already fenced its readers skip it.
+        if (!quiesced) cudaDeviceSynchronize();
+        cudaFreeAsync(d_lines, nullptr);
+      } else {
+        cudaFree(d_lines);
+      }
+    }
     if (d_err) cudaFree(d_err);
     if (prev >= 0) cudaSetDevice(prev);
   }
@@ -242,7 +253,7 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
   // 2 split leaves, 3 texture leaves + split internal L2 levels, 4 texture leaves
   // with the select extraction of 1-byte next hops (= 1 for wider next hops).
   const int plan_lp = static_cast<int>(f->cfg.line_path);
-  const int leaftex = plan_lp != 0 && f->tex && !leafs && (input == kInAddr || input == kInKey) &&
+  const int leaftex = plan_lp != 0 && f->tex && !leafs && (input == kInAddr || input == kInKey || input == kInPacket) &&
                               f->d_err == nullptr && tiles == 1 && threads_cta == 1024 && minb == 1 && f->g.depth >= 1
                           ? (plan_lp == 2 ? 2 : (plan_lp == 4 && f->g.value_bytes == 1) ? 3 : 1)
                           : 0;
@@ -470,6 +481,12 @@ void lookup_host(lpm6cu_fib* f, const void* addrs, unsigned long long n, void* o
 
 }  // namespace
 
+void lpm6::capi::fib_destroy_quiesced(lpm6cu_fib* f) {
+  if (!f) return;
+  f->quiesced = true;
+  delete f;
+}
+
 extern "C" {
 
 int lpm6cu_fib_create(int device, const lpm6cu_geometry* g, const uint64_t* lines, lpm6cu_fib** out) {
@@ -545,17 +562,22 @@ int lpm6cu_fib_build_device(int device, const lpm6cu_prefix* rules, uint64_t n, 
     if (n > 0 && !rules) throw Error(Errc::InvalidArgument, "rules is NULL");
     if (!out) throw Error(Errc::InvalidArgument, "NULL out");
     DeviceGuard dg(device);
+    capi::BuildTrace tr("fib_build_device");
     lpm6cu_geometry g;
     void* lines = capi::device_build_tree(rules, n, default_nh, opts, static_cast<cudaStream_t>(stream), &g);
+    tr.mark("tree");
     std::unique_ptr<lpm6cu_fib> f;
     try {
       f.reset(new_fib(device, &g));
     } catch (...) {
-      cudaFree(lines);
+      cudaFreeAsync(lines, static_cast<cudaStream_t>(stream));
       throw;
     }
+    tr.mark("handle");
     f->d_lines = static_cast<unsigned long long*>(lines);
+    f->pooled = true;
     load_root(f.get());
+    tr.mark("root");
     *out = f.release();
   });
 }
@@ -813,10 +835,11 @@ int lpm6cu_fib_build_from_intervals(int device, const uint64_t* boundaries, cons
     try {
       f.reset(new_fib(device, &g));
     } catch (...) {
-      cudaFree(lines);
+      cudaFreeAsync(lines, static_cast<cudaStream_t>(stream));
       throw;
     }
     f->d_lines = static_cast<unsigned long long*>(lines);
+    f->pooled = true;
     load_root(f.get());
     *out = f.release();
   });

@@ -815,7 +815,7 @@ KernelFn pick_depth_texl(int depth) {
   }
 }
 
-// Leaf lines through the texture pipe (default shape, unchecked, address / key input).
+// Leaf lines through the texture pipe (default shape, unchecked, address / key / packet input).
 // texl: internal-level mode (0 LSU, 1 texture, 2 split); mode: leaf mode (1 texture,
 // 2 split, 3 texture with the select extraction of 1-byte next hops). Instantiated:
 // texl 0/1 with leaf modes 1 and 2, texl 2 with texture leaves, mode 3 for VB = 1.
@@ -871,6 +871,7 @@ KernelFn pick_kernel_fmt(const PickArgs& a) {
     switch (a.input) {
       case kInAddr: return pick_leaftex<VB, kInAddr, HALF>(depth, a.texl, a.leaftex);
       case kInKey: return pick_leaftex<VB, kInKey, HALF>(depth, a.texl, a.leaftex);
+      case kInPacket: return pick_leaftex<VB, kInPacket, HALF>(depth, a.texl, a.leaftex);
       default: return nullptr;
     }
   }

@@ -22,6 +22,7 @@
 #include <mutex>
 #include <vector>
 
+#include "capi_internal.hpp"
 #include "capi_util.hpp"
 #include "lpm6/fib.hpp"
 #include "lpm6/update.hpp"
@@ -107,8 +108,10 @@ struct lpm6cu_snapshot {
   uint64_t refs = 0;
   std::vector<Fence> fences;
 
+  // Only reclaim() deletes snapshots, after their fences completed (store_destroy
+  // waits for them): no lookup can still read the FIB.
   ~lpm6cu_snapshot() {
-    if (fib) lpm6cu_fib_destroy(fib);
+    if (fib) capi::fib_destroy_quiesced(fib);
   }
 };
 
@@ -322,7 +325,9 @@ int lpm6cu_store_commit(lpm6cu_store* s, uint64_t* epoch) {
       s->stats.active_rules = next->rules.size();
       ++s->stats.commits;
     }
+    capi::BuildTrace tr("store commit");
     s->reclaim(false);
+    tr.mark("reclaim");
     if (epoch) *epoch = next->epoch;
   });
 }

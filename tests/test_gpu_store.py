@@ -373,7 +373,7 @@ def test_first_commit_is_warm(lpm, cuda, st):
     store = st.FibStore(fib, 0, value_bytes=1)
     rng = np.random.default_rng(1)
     rules = fib.rules
-    times = []
+    times, builds = [], []
     for _ in range(3):
         idx = rng.integers(0, len(rules), 1000)
         store.stage([st.UpdateOp(st.ANNOUNCE, Prefix(int(rules[i]["value_hi"]) << 64, int(rules[i]["length"]),
@@ -381,6 +381,7 @@ def test_first_commit_is_warm(lpm, cuda, st):
         t0 = time.perf_counter()
         store.commit()
         times.append((time.perf_counter() - t0) * 1e3)
+        builds.append(store.stats.last_build_ms)
     store.close()
-    assert times[0] <= 15.0, times
-    assert times[0] <= 3 * max(min(times[1:]), 2.0), times
+    assert times[0] <= 15.0, (times, builds)
+    assert times[0] <= 3 * max(min(times[1:]), 2.0), (times, builds)
