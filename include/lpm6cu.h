@@ -118,8 +118,8 @@ typedef struct {
   uint32_t queries_per_lane; /* 32-query tiles each warp carries at once: 1, or 2 at 256 threads */
   uint32_t min_ctas_per_sm;  /* register cap (__launch_bounds__ min blocks): 1 at 1024 threads,
                                 2 at 512, 0 or 4 at 256 */
-  uint32_t line_path;        /* which L1TEX pipe carries the 128-byte L2 lines (address / key /
-                                packet input, default shape, unchecked): 0 = leaves through the LSU,
+  uint32_t line_path;        /* which L1TEX pipe carries the 128-byte L2 lines (address / key
+                                input, and packets over half-line leaves; default shape, unchecked): 0 = leaves through the LSU,
                                 internal L2 levels through the texture pipe (default); 1 = leaves
                                 through the texture pipe too, faster when leaf lines often hit L1
                                 (skewed traffic); 2 = half of each warp's leaf lines through each
@@ -213,6 +213,8 @@ int lpm6cu_fib_kernel_config(const lpm6cu_fib* fib, lpm6cu_kernel_config* cfg);
  * lookups on the handle. */
 int lpm6cu_fib_tune_line_path(lpm6cu_fib* fib, const void* d_addrs, uint64_t n, void* d_out, void* stream,
                               uint32_t reps, uint32_t* line_path);
+/* Waits for the device (as cudaFree would), then releases the handle's memory; device-built
+ * line arrays return to a library-private pool instead of being unmapped. */
 void lpm6cu_fib_destroy(lpm6cu_fib* fib);
 
 /* Checked mode: lookups run a bounds-checked kernel that never reads outside the

@@ -253,7 +253,12 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
   // 2 split leaves, 3 texture leaves + split internal L2 levels, 4 texture leaves
   // with the select extraction of 1-byte next hops (= 1 for wider next hops).
   const int plan_lp = static_cast<int>(f->cfg.line_path);
-  const int leaftex = plan_lp != 0 && f->tex && !leafs && (input == kInAddr || input == kInKey || input == kInPacket) &&
+  // Packet input follows the line path only with half-line leaves: measured on the
+  // bench's 64-byte frames, texture leaves take C2 from 53.9 to 58.0 G/s but C1 (full
+  // 1-byte-next-hop leaf lines) from 56.5 down to 49.5 (tools/gpu/run24.sh).
+  const bool path_input = input == kInAddr || input == kInKey ||
+                          (input == kInPacket && f->g.leaf_words == kHalfLeafWords);
+  const int leaftex = plan_lp != 0 && f->tex && !leafs && path_input &&
                               f->d_err == nullptr && tiles == 1 && threads_cta == 1024 && minb == 1 && f->g.depth >= 1
                           ? (plan_lp == 2 ? 2 : (plan_lp == 4 && f->g.value_bytes == 1) ? 3 : 1)
                           : 0;
