@@ -273,7 +273,8 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
     if (!slot.valid) {
       KernelFn fn = pick_kernel(static_cast<int>(f->g.value_bytes), static_cast<int>(f->g.depth),
                                 static_cast<int>(tiles), threads, static_cast<int>(minb), f->d_err != nullptr, input,
-                                leafs, texl_mode, leaftex, f->g.leaf_words == kHalfLeafWords);
+                                leafs, texl_mode, leaftex, f->g.leaf_words == kHalfLeafWords,
+                                static_cast<int>(std::min<unsigned>(smem_levels, f->g.depth)));
       if (!fn) throw Error(Errc::InvalidArgument, "no kernel instantiated for this configuration");
       // The attribute belongs to the kernel, which every FIB of this depth and
       // next-hop width shares: always set it to the device's opt-in maximum, never

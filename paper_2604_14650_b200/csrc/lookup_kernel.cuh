@@ -73,6 +73,11 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 #ifndef LPM6_INT_SECTORS
 #define LPM6_INT_SECTORS 0
 #endif
+// Staged-level count as a template constant in the texture line-path kernels (1) or
+// always read from the launch (0). A/B switch.
+#ifndef LPM6_STATIC_TA
+#define LPM6_STATIC_TA 1
+#endif
 
 
 // ---- PTX helpers ------------------------------------------------------------
@@ -253,6 +258,29 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // ---- kernel -----------------------------------------------------------------
 
 
+
+// Rank of q in the root (the kernel-parameter copy, LookupParams::root): the same
+// 4-probe search. ROOT_WALK keeps the probe position as a byte offset advanced by
+// predicated adds — each probe one LDC at register + immediate, two compares and one
+// add — instead of rebuilding an indexed address per probe.
+#ifndef LPM6_ROOT_WALK
+#define LPM6_ROOT_WALK 1
+#endif
+__device__ __forceinline__ unsigned root_rank(const LookupParams& p, unsigned long long q) {
+#if LPM6_ROOT_WALK
+  unsigned o = (p.root[7] <= q) ? 64u : 0u;  // byte offset of the candidate position
+  o += (p.root[(o >> 3) + 3u] <= q) ? 32u : 0u;
+  o += (p.root[(o >> 3) + 1u] <= q) ? 16u : 0u;
+  o += (p.root[o >> 3] <= q) ? 8u : 0u;
+  return o >> 3;
+#else
+  unsigned c = (p.root[7] <= q) ? 8u : 0u;
+  c |= (p.root[c | 3u] <= q) ? 4u : 0u;
+  c |= (p.root[c | 1u] <= q) ? 2u : 0u;
+  c |= (p.root[c] <= q) ? 1u : 0u;
+  return c;
+#endif
+}
 
 // Count of the 15 separators of node n of a shared-memory image level that are
 // <= q: a branch-free 4-probe binary search (16 outcomes). The probe positions
@@ -451,8 +479,12 @@ __device__ __forceinline__ unsigned leaf_search_smem(const unsigned long long* l
 // traffic the texture path's miss throughput is lower (C1 -27 % with 1, +1.2 %
 // with 2), so the host picks the line path by measurement
 // (lpm6cu_fib_tune_line_path).
+// TAS > 0: the number of staged levels is a compile-time constant (= p.smem_levels),
+// so Phase A's level loop and Phase B's internal-level loop have no runtime level
+// checks (the texture line paths are instantiated for TAS = DEPTH and DEPTH - 1, the
+// staging every BASELINE FIB uses; TAS = 0 reads the count from the launch).
 template <int DEPTH, int VB, int TILES, int THREADS, int MINB, bool CHECKED, int INPUT = kInAddr, bool LEAFS = false,
-          int TEXL = 0, int LEAFTEX = 0, bool HALF = false>
+          int TEXL = 0, int LEAFTEX = 0, bool HALF = false, int TAS = 0>
 __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const LookupParams p) {
   using F = LeafFmt<VB>;
   // Texture leaf fetches as sector-disjoint halves (tex_line_quarter) for 1-byte next
@@ -472,7 +504,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
   const unsigned long long warp0 = (static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const unsigned long long nwarps = (static_cast<unsigned long long>(gridDim.x) * blockDim.x) >> 5;
   const uint64_t pol_stream = policy_evict_first();
-  const unsigned TA = p.smem_levels;
+  const unsigned TA = TAS > 0 ? static_cast<unsigned>(TAS) : p.smem_levels;
   const uint32_t s_base = smem_u32(s_lines);  // shared-space byte address of the image
   const unsigned leaf_valid = (F::kL - 4 * static_cast<int>(j)) < 0 ? 0u
                               : (F::kL - 4 * static_cast<int>(j)) > 4 ? 4u
@@ -542,10 +574,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
         // Root from the kernel-parameter constant bank: all lanes start at the
         // same node, so the probes are (nearly) uniform LDCs and keep the
         // shared-memory data pipe free for the deeper levels.
-        unsigned c = (p.root[7] <= q) ? 8u : 0u;
-        c |= (p.root[c | 3u] <= q) ? 4u : 0u;
-        c |= (p.root[c | 1u] <= q) ? 2u : 0u;
-        c |= (p.root[c] <= q) ? 1u : 0u;
+        const unsigned c = root_rank(p, q);
         if (TA == 1) {
           node[t] = c;
           continue;
@@ -801,16 +830,28 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
 // Instantiated shapes: (queries per lane, min CTAs per SM) for every depth; one
 // next-hop width per translation unit (lookup_vb{1,2,4}.cu), so the ~150 kernels
 // of each width compile in parallel. bench.py --sweep measures the shapes.
+// The default-shape kernel of one depth: the staged-level count as a template
+// constant when it is DEPTH or DEPTH - 1 (TAS), else read from the launch.
+template <int D, int VB, int INPUT, int TEXL, int LEAFTEX, bool HALF>
+KernelFn pick_ta(int ta) {
+  if constexpr (LPM6_STATIC_TA != 0) {
+    if (ta == D) return lpm6_lookup_kernel<D, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF, D>;
+    if constexpr (D >= 2)
+      if (ta == D - 1) return lpm6_lookup_kernel<D, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF, D - 1>;
+  }
+  return lpm6_lookup_kernel<D, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF>;
+}
+
 template <int VB, int INPUT, int TEXL, int LEAFTEX, bool HALF>
-KernelFn pick_depth_texl(int depth) {
+KernelFn pick_depth_texl(int depth, int ta = 0) {
   switch (depth) {
-    case 1: return lpm6_lookup_kernel<1, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF>;
-    case 2: return lpm6_lookup_kernel<2, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF>;
-    case 3: return lpm6_lookup_kernel<3, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF>;
-    case 4: return lpm6_lookup_kernel<4, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF>;
-    case 5: return lpm6_lookup_kernel<5, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF>;
-    case 6: return lpm6_lookup_kernel<6, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF>;
-    case 7: return lpm6_lookup_kernel<7, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF>;
+    case 1: return pick_ta<1, VB, INPUT, TEXL, LEAFTEX, HALF>(ta);
+    case 2: return pick_ta<2, VB, INPUT, TEXL, LEAFTEX, HALF>(ta);
+    case 3: return pick_ta<3, VB, INPUT, TEXL, LEAFTEX, HALF>(ta);
+    case 4: return pick_ta<4, VB, INPUT, TEXL, LEAFTEX, HALF>(ta);
+    case 5: return pick_ta<5, VB, INPUT, TEXL, LEAFTEX, HALF>(ta);
+    case 6: return pick_ta<6, VB, INPUT, TEXL, LEAFTEX, HALF>(ta);
+    case 7: return pick_ta<7, VB, INPUT, TEXL, LEAFTEX, HALF>(ta);
     default: return nullptr;
   }
 }
@@ -820,17 +861,17 @@ KernelFn pick_depth_texl(int depth) {
 // 2 split, 3 texture with the select extraction of 1-byte next hops). Instantiated:
 // texl 0/1 with leaf modes 1 and 2, texl 2 with texture leaves, mode 3 for VB = 1.
 template <int VB, int INPUT, bool HALF>
-KernelFn pick_leaftex(int depth, int texl, int mode) {
+KernelFn pick_leaftex(int depth, int texl, int mode, int ta) {
   if (mode == 3) {  // texture leaves with the select extraction: 1-byte next hops only
     if constexpr (VB == 1 && !HALF)
-      return texl == 1 ? pick_depth_texl<VB, INPUT, 1, 3, HALF>(depth)
-             : texl == 0 ? pick_depth_texl<VB, INPUT, 0, 3, HALF>(depth) : nullptr;
+      return texl == 1 ? pick_depth_texl<VB, INPUT, 1, 3, HALF>(depth, ta)
+             : texl == 0 ? pick_depth_texl<VB, INPUT, 0, 3, HALF>(depth, ta) : nullptr;
     return nullptr;
   }
-  if (texl == 2) return mode == 1 ? pick_depth_texl<VB, INPUT, 2, 1, HALF>(depth) : nullptr;
+  if (texl == 2) return mode == 1 ? pick_depth_texl<VB, INPUT, 2, 1, HALF>(depth, ta) : nullptr;
   if (mode == 2)
-    return texl ? pick_depth_texl<VB, INPUT, 1, 2, HALF>(depth) : pick_depth_texl<VB, INPUT, 0, 2, HALF>(depth);
-  return texl ? pick_depth_texl<VB, INPUT, 1, 1, HALF>(depth) : pick_depth_texl<VB, INPUT, 0, 1, HALF>(depth);
+    return texl ? pick_depth_texl<VB, INPUT, 1, 2, HALF>(depth, ta) : pick_depth_texl<VB, INPUT, 0, 2, HALF>(depth, ta);
+  return texl ? pick_depth_texl<VB, INPUT, 1, 1, HALF>(depth, ta) : pick_depth_texl<VB, INPUT, 0, 1, HALF>(depth, ta);
 }
 
 template <int VB, bool CHECKED>
@@ -869,9 +910,9 @@ KernelFn pick_kernel_fmt(const PickArgs& a) {
   if (a.leaftex) {  // default shape, unchecked, no leaf image, depth >= 1
     if (a.leafs || a.checked || !dflt) return nullptr;
     switch (a.input) {
-      case kInAddr: return pick_leaftex<VB, kInAddr, HALF>(depth, a.texl, a.leaftex);
-      case kInKey: return pick_leaftex<VB, kInKey, HALF>(depth, a.texl, a.leaftex);
-      case kInPacket: return pick_leaftex<VB, kInPacket, HALF>(depth, a.texl, a.leaftex);
+      case kInAddr: return pick_leaftex<VB, kInAddr, HALF>(depth, a.texl, a.leaftex, a.ta);
+      case kInKey: return pick_leaftex<VB, kInKey, HALF>(depth, a.texl, a.leaftex, a.ta);
+      case kInPacket: return pick_leaftex<VB, kInPacket, HALF>(depth, a.texl, a.leaftex, a.ta);
       default: return nullptr;
     }
   }

@@ -52,6 +52,7 @@ struct PickArgs {
   bool leafs = false;
   int texl = 0, leaftex = 0;
   bool half = false;  // half-line leaves (layout.hpp kHalfLeafWords; 2-byte next hops)
+  int ta = 0;         // staged levels (smem_levels) of the launch: compile-time in the texture line-path kernels
 };
 
 KernelFn pick_kernel_vb1(const PickArgs& a);  // lookup_vb1.cu
@@ -61,7 +62,7 @@ KernelFn pick_kernel_vb4(const PickArgs& a);  // lookup_vb4.cu
 // nullptr when that combination is not instantiated.
 inline KernelFn pick_kernel(int vb, int depth, int tiles, int threads, int minb, bool checked = false,
                             int input = kInAddr, bool leafs = false, int texl = 0, int leaftex = 0,
-                            bool half = false) {
+                            bool half = false, int ta = 0) {
   PickArgs a;
   a.depth = depth;
   a.tiles = tiles;
@@ -73,6 +74,7 @@ inline KernelFn pick_kernel(int vb, int depth, int tiles, int threads, int minb,
   a.texl = texl;
   a.leaftex = leaftex;
   a.half = half;
+  a.ta = ta;
   switch (vb) {
     case 1: return pick_kernel_vb1(a);
     case 2: return pick_kernel_vb2(a);
