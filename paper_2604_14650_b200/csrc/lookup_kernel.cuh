@@ -178,6 +178,14 @@ __device__ __forceinline__ unsigned long long load_dst_key(const unsigned char* 
   return bswap64(le);  // network order: first byte is the most significant
 }
 
+// One 16-byte texel (SASS TLD.LZ on the int4 texture object over the line array).
+__device__ __forceinline__ void tex16(unsigned long long tex, unsigned texel, unsigned long long& lo,
+                                      unsigned long long& hi) {
+  const int4 v = tex1Dfetch<int4>(static_cast<cudaTextureObject_t>(tex), static_cast<int>(texel));
+  lo = static_cast<unsigned>(v.x) | (static_cast<unsigned long long>(static_cast<unsigned>(v.y)) << 32);
+  hi = static_cast<unsigned>(v.z) | (static_cast<unsigned long long>(static_cast<unsigned>(v.w)) << 32);
+}
+
 // 32 bytes of a line through the texture path: two 16-byte texels. Line texel
 // t0 + 0..7; lane j of the 4-lane group fetches texels (2j, 2j+1) — words 4j..4j+3,
 // the same quarter an LSU lane loads — or, with SECTORS, texels (j, j+4): words
@@ -189,20 +197,19 @@ __device__ __forceinline__ unsigned long long load_dst_key(const unsigned char* 
 // line fetched ~1.5 times from L2 when the compiler spreads a slot's two fetches
 // apart). Counting ranks does not depend on which lane holds which key; the leaf
 // formats where it matters are handled at the call site.
+// The lane's texel base of a level (line word offset / 2 + its first texel), so that
+// a fetch pair is texel = base + 8 * node (one IMAD); with a per-slot address instead,
+// ptxas also gave every TLD its own uniform copy of the texture handle (R2UR pairs).
 template <bool SECTORS>
-__device__ __forceinline__ void tex_line_quarter(unsigned long long tex, unsigned t0, unsigned j,
-                                                 unsigned long long (&w)[4]) {
-  const unsigned ta = SECTORS ? t0 + j : t0 + 2u * j;
-  const unsigned tb = SECTORS ? ta + 4u : ta + 1u;
-  int a0, a1, a2, a3, b0, b1, b2, b3;
-  asm volatile("tex.1d.v4.s32.s32 {%0,%1,%2,%3}, [%4, {%5}];"
-               : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3) : "l"(tex), "r"(ta));
-  asm volatile("tex.1d.v4.s32.s32 {%0,%1,%2,%3}, [%4, {%5}];"
-               : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3) : "l"(tex), "r"(tb));
-  w[0] = static_cast<unsigned>(a0) | (static_cast<unsigned long long>(static_cast<unsigned>(a1)) << 32);
-  w[1] = static_cast<unsigned>(a2) | (static_cast<unsigned long long>(static_cast<unsigned>(a3)) << 32);
-  w[2] = static_cast<unsigned>(b0) | (static_cast<unsigned long long>(static_cast<unsigned>(b1)) << 32);
-  w[3] = static_cast<unsigned>(b2) | (static_cast<unsigned long long>(static_cast<unsigned>(b3)) << 32);
+__device__ __forceinline__ unsigned tex_lane_base(unsigned line_w, unsigned j) {
+  return (line_w >> 1) + (SECTORS ? j : 2u * j);
+}
+template <bool SECTORS>
+__device__ __forceinline__ void tex_line_at(unsigned long long tex, unsigned base, unsigned node,
+                                            unsigned long long (&w)[4]) {
+  const unsigned ta = base + node * 8u;
+  tex16(tex, ta, w[0], w[1]);
+  tex16(tex, ta + (SECTORS ? 4u : 1u), w[2], w[3]);
 }
 
 // Half-line leaves: 16 bytes per lane (words 2j, 2j+1), by a 16-byte load or one
@@ -211,11 +218,7 @@ __device__ __forceinline__ void ld_half_leaf(const unsigned long long* p, unsign
   asm volatile("ld.global.nc.v2.u64 {%0,%1}, [%2];" : "=l"(w[0]), "=l"(w[1]) : "l"(p));
 }
 __device__ __forceinline__ void tex_half_leaf(unsigned long long tex, unsigned texel, unsigned long long (&w)[4]) {
-  int a0, a1, a2, a3;
-  asm volatile("tex.1d.v4.s32.s32 {%0,%1,%2,%3}, [%4, {%5}];"
-               : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3) : "l"(tex), "r"(texel));
-  w[0] = static_cast<unsigned>(a0) | (static_cast<unsigned long long>(static_cast<unsigned>(a1)) << 32);
-  w[1] = static_cast<unsigned>(a2) | (static_cast<unsigned long long>(static_cast<unsigned>(a3)) << 32);
+  tex16(tex, texel, w[0], w[1]);
 }
 
 __device__ __forceinline__ void ld_line_quarter(const unsigned long long* p, unsigned long long (&w)[4]) {
@@ -487,7 +490,7 @@ template <int DEPTH, int VB, int TILES, int THREADS, int MINB, bool CHECKED, int
           int TEXL = 0, int LEAFTEX = 0, bool HALF = false, int TAS = 0>
 __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const LookupParams p) {
   using F = LeafFmt<VB>;
-  // Texture leaf fetches as sector-disjoint halves (tex_line_quarter) for 1-byte next
+  // Texture leaf fetches as sector-disjoint halves (tex_line_at) for 1-byte next
   // hops. (2-byte ones would need their values gathered from lanes 2 and 3; measured
   // on C2: no gain on texture leaves, 56 vs 55 G/s, so they keep lane quarters.)
   constexpr bool kLeafSectors = LPM6_TEX_SECTORS != 0 && VB == 1;
@@ -676,7 +679,9 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
         // +8 %); leaves through the texture pipe lose on L2-missing workloads
         // (C1 -17 %), so they stay on the LSU path.
         if (TEXL == 1 || (TEXL == 2 && s < NS / 2))
-          tex_line_quarter<LPM6_INT_SECTORS != 0>(p.tex, (line_w + nd[s] * 16u) >> 1, j, w[s]);
+          // (the per-slot texel form here: the lane-base form cost C2 0.35 %, 64 vs 60 registers)
+          tex_line_at<LPM6_INT_SECTORS != 0>(p.tex, ((line_w + nd[s] * 16u) >> 1) + (LPM6_INT_SECTORS ? j : 2u * j),
+                                             0u, w[s]);
         else
           ld_line_quarter(p.lines + (base_w + nd[s] * 16u), w[s]);
       }
@@ -752,7 +757,7 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
           // sector-disjoint fetches (kLeafSectors): for 1-byte next hops the leaf
           // keeps the same key slots and value lane in both orders (the values are
           // words 14-15 = lane 3's second texel either way)
-          tex_line_quarter<kLeafSectors>(p.tex, (line_w + nd[s] * 16u) >> 1, j, w[s]);
+          tex_line_at<kLeafSectors>(p.tex, tex_lane_base<kLeafSectors>(line_w, j), nd[s], w[s]);
         else
           ld_line_quarter(p.lines + (base_w + nd[s] * 16u), w[s]);
       }
