@@ -231,6 +231,23 @@ int lpm6cu_store_create(int device, const lpm6cu_prefix* rules, uint64_t n, uint
       cudaStreamDestroy(s->build_stream);
       throw;
     }
+    // Reserve room for the next snapshot's line array too: every commit builds a new
+    // array while the active one is still alive, and growing the pool maps device
+    // memory through the driver (tens of ms in a process that holds a lot of it).
+    // The pool keeps freed memory, so the first commit then allocates from it.
+    {
+      lpm6cu_geometry g{};
+      if (lpm6cu_fib_geometry(s->active->fib, &g) == LPM6CU_OK && g.total_words) {
+        void* spare = nullptr;
+        const size_t bytes = static_cast<size_t>(g.total_words) * 8 + (static_cast<size_t>(g.total_words) * 8) / 4;
+        if (cudaMallocFromPoolAsync(&spare, bytes, capi::fib_line_pool(device), s->build_stream) == cudaSuccess) {
+          cudaFreeAsync(spare, s->build_stream);
+          cudaStreamSynchronize(s->build_stream);
+        } else {
+          cudaGetLastError();  // only a warm-up: the first commit grows the pool instead
+        }
+      }
+    }
     s->stats.epoch = 1;
     s->stats.active_rules = s->active->rules.size();
     *out = s.release();
