@@ -115,7 +115,10 @@ typedef struct {
                                thread per query; 0xFF = auto */
   uint32_t ctas_per_sm;      /* cap on resident CTAs per SM used for the grid; 0 = occupancy */
   uint32_t threads_per_cta;  /* 1024 (default), 512 or 256 */
-  uint32_t queries_per_lane; /* 32-query tiles each warp carries at once: 1, or 2 at 256 threads */
+  uint32_t queries_per_lane; /* 32-query tiles each warp carries at once: 1; 2 at 256 threads; 2 or
+                                4 at 1024 threads on the texture leaf paths 1 and 4 (the tiles'
+                                shared-memory descents overlap, their L2 levels run one tile at a
+                                time; other line paths then run one tile). The tuner picks it. */
   uint32_t min_ctas_per_sm;  /* register cap (__launch_bounds__ min blocks): 1 at 1024 threads,
                                 2 at 512, 0 or 4 at 256 */
   uint32_t line_path;        /* which L1TEX pipe carries the 128-byte L2 lines (address / key
@@ -205,8 +208,9 @@ int lpm6cu_fib_set_kernel_config(lpm6cu_fib* fib, const lpm6cu_kernel_config* cf
 int lpm6cu_fib_kernel_config(const lpm6cu_fib* fib, lpm6cu_kernel_config* cfg);
 /* Times the line paths on a representative batch (device buffers; two interleaved
  * rounds of `reps` timed launches per path after one untimed, the faster round
- * kept; on `stream`, which it synchronizes), keeps the
- * fastest in the kernel config and returns it in *line_path (0..4, see
+ * kept; on `stream`, which it synchronizes) — the texture leaf paths 1 and 4 also
+ * with 2 and 4 tiles per warp (queries_per_lane, at 1024 threads) — keeps the
+ * fastest in the kernel config and returns its line path in *line_path (0..4, see
  * lpm6cu_kernel_config; 3 only when the tree has internal L2 levels, 4 only with
  * 1-byte next hops). Results are
  * identical on every path; like the other tuning calls it must not race with

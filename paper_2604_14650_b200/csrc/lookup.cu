@@ -176,8 +176,12 @@ void resolve_config(lpm6cu_fib* f, const lpm6cu_kernel_config* req) {
   if (c.queries_per_lane == 0) c.queries_per_lane = 1;
   if (c.min_ctas_per_sm == 0 && c.threads_per_cta == 512) c.min_ctas_per_sm = 2;
   if (c.min_ctas_per_sm == 0 && c.threads_per_cta == 1024) c.min_ctas_per_sm = 1;
-  if (!pick_kernel(1, 0, static_cast<int>(c.queries_per_lane), static_cast<int>(c.threads_per_cta),
-                   static_cast<int>(c.min_ctas_per_sm)))
+  // 2 or 4 tiles per warp at 1024 threads: Phase A overlaps the tiles' probe chains, Phase B
+  // takes one tile at a time (texture leaf paths 1 and 4; other plans run one tile)
+  const bool two_tiles = (c.queries_per_lane == 2 || c.queries_per_lane == 4) && c.threads_per_cta == 1024 &&
+                         c.min_ctas_per_sm == 1;
+  if (!two_tiles && !pick_kernel(1, 0, static_cast<int>(c.queries_per_lane), static_cast<int>(c.threads_per_cta),
+                                 static_cast<int>(c.min_ctas_per_sm)))
     throw Error(Errc::InvalidArgument, "no kernel for queries_per_lane=" + std::to_string(c.queries_per_lane) +
                                            " threads_per_cta=" + std::to_string(c.threads_per_cta) +
                                            " min_ctas_per_sm=" + std::to_string(c.min_ctas_per_sm));
@@ -240,15 +244,17 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
     return;
   }
   const bool dflt = input != kInAddr;
-  const unsigned tiles = dflt ? 1 : f->cfg.queries_per_lane;
+  const unsigned tiles_cfg = dflt ? 1 : f->cfg.queries_per_lane;
   const unsigned threads_cta = dflt ? 1024 : f->cfg.threads_per_cta;
   const unsigned minb = dflt ? 1 : f->cfg.min_ctas_per_sm;
   // Leaf-image mode serves address input; key / packet input uses the internal image only.
   const bool leafs = leaf_image_mode(f) && input == kInAddr;
   // Texture pipe for internal L2 levels when the tree has any (smem_levels < depth).
   const unsigned smem_levels = leaf_image_mode(f) && !leafs ? f->g.depth : f->cfg.smem_levels;
+  // texture line paths: the default shape, and 2 or 4 tiles per warp at 1024 threads (address input)
+  const bool tex_shape = threads_cta == 1024 && minb == 1 && (tiles_cfg == 1 || input == kInAddr);
   const bool texl = f->tex && !leafs && input != kInKeyOrd && f->d_err == nullptr && smem_levels < f->g.depth &&
-                    tiles == 1 && threads_cta == 1024 && minb == 1 && f->g.depth >= 2;
+                    tex_shape && f->g.depth >= 2;
   // Line path plan (lpm6cu_kernel_config.line_path): 0 LSU leaves, 1 texture leaves,
   // 2 split leaves, 3 texture leaves + split internal L2 levels, 4 texture leaves
   // with the select extraction of 1-byte next hops (= 1 for wider next hops).
@@ -259,10 +265,15 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
   const bool path_input = input == kInAddr || input == kInKey ||
                           (input == kInPacket && f->g.leaf_words == kHalfLeafWords);
   const int leaftex = plan_lp != 0 && f->tex && !leafs && path_input &&
-                              f->d_err == nullptr && tiles == 1 && threads_cta == 1024 && minb == 1 && f->g.depth >= 1
+                              f->d_err == nullptr && tex_shape && f->g.depth >= 1
                           ? (plan_lp == 2 ? 2 : (plan_lp == 4 && f->g.value_bytes == 1) ? 3 : 1)
                           : 0;
   const int texl_mode = !texl ? 0 : (plan_lp == 3 && leaftex == 1) ? 2 : 1;
+  // 2 or 4 tiles per warp at 1024 threads exist for texture leaves (paths 1 and 4) with
+  // internal L2 levels on one pipe; any other plan of such a config runs one tile.
+  const unsigned tiles = threads_cta == 1024 && tiles_cfg > 1 && !((leaftex == 1 || leaftex == 3) && texl_mode <= 1)
+                             ? 1u
+                             : tiles_cfg;
   const size_t smem = image_bytes_of(f->g, smem_levels);
   const int threads = static_cast<int>(threads_cta);
   LaunchPlan plan;
@@ -639,8 +650,13 @@ int lpm6cu_fib_tune_line_path(lpm6cu_fib* f, const void* d_addrs, uint64_t n, vo
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     lpm6cu_kernel_config c = f->cfg;
     const bool possible = f->tex && f->d_err == nullptr && !leaf_image_mode(f) && f->g.depth >= 1 &&
-                          c.queries_per_lane == 1 && c.threads_per_cta == 1024 && c.min_ctas_per_sm == 1;
-    unsigned best = 0;
+                          c.threads_per_cta == 1024 && c.min_ctas_per_sm == 1 &&
+                          (c.queries_per_lane == 1 || c.queries_per_lane == 2 || c.queries_per_lane == 4);
+    // Candidates: every applicable line path with one tile per warp, and the texture
+    // leaf paths (1, 4) with 2 and 4 tiles (Phase A of the tiles overlapped).
+    constexpr unsigned kTiles[3] = {1, 2, 4};
+    auto tiles_apply = [&](unsigned path, unsigned ti) { return ti == 0 || path == 1 || path == 4; };
+    unsigned best = 0, best_ti = 0;
     if (possible) {
       cudaEvent_t ev[2];
       check_cuda(cudaEventCreate(&ev[0]), "cudaEventCreate");
@@ -648,41 +664,49 @@ int lpm6cu_fib_tune_line_path(lpm6cu_fib* f, const void* d_addrs, uint64_t n, vo
         cudaEventDestroy(ev[0]);
         throw Error(Errc::CudaError, "cudaEventCreate");
       }
-      float ms[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+      float ms[5][3] = {};
       try {
         const unsigned r = reps ? reps : 3;
         // Plan 3 differs from plan 1 only when the tree has internal L2 levels.
         // Two interleaved rounds, the faster of each plan's two timings kept, so a
         // clock ramp or a neighbour's burst during one plan's turn cannot pick it.
         for (unsigned round = 0; round < 2; ++round)
-          for (unsigned path = 0; path < 5; ++path) {
-            if (!plan_applies(f, path)) continue;
-            c.line_path = path;
-            f->cfg = c;
-            f->invalidate_plans();
-            launch_lookup(f, d_addrs, n, d_out, st);  // untimed: resolves the plan, warms L2
-            check_cuda(cudaEventRecord(ev[0], st), "cudaEventRecord");
-            for (unsigned i = 0; i < r; ++i) launch_lookup(f, d_addrs, n, d_out, st);
-            check_cuda(cudaEventRecord(ev[1], st), "cudaEventRecord");
-            check_cuda(cudaEventSynchronize(ev[1]), "cudaEventSynchronize");
-            float t = 0.f;
-            check_cuda(cudaEventElapsedTime(&t, ev[0], ev[1]), "cudaEventElapsedTime");
-            ms[path] = round == 0 ? t : std::min(ms[path], t);
-          }
+          for (unsigned path = 0; path < 5; ++path)
+            for (unsigned ti = 0; ti < 3; ++ti) {
+              if (!plan_applies(f, path) || !tiles_apply(path, ti)) continue;
+              c.line_path = path;
+              c.queries_per_lane = kTiles[ti];
+              f->cfg = c;
+              f->invalidate_plans();
+              launch_lookup(f, d_addrs, n, d_out, st);  // untimed: resolves the plan, warms L2
+              check_cuda(cudaEventRecord(ev[0], st), "cudaEventRecord");
+              for (unsigned i = 0; i < r; ++i) launch_lookup(f, d_addrs, n, d_out, st);
+              check_cuda(cudaEventRecord(ev[1], st), "cudaEventRecord");
+              check_cuda(cudaEventSynchronize(ev[1]), "cudaEventSynchronize");
+              float t = 0.f;
+              check_cuda(cudaEventElapsedTime(&t, ev[0], ev[1]), "cudaEventElapsedTime");
+              ms[path][ti] = round == 0 ? t : std::min(ms[path][ti], t);
+            }
       } catch (...) {
         cudaEventDestroy(ev[0]);
         cudaEventDestroy(ev[1]);
         c.line_path = 0;
+        c.queries_per_lane = 1;
         f->cfg = c;
         f->invalidate_plans();
         throw;
       }
       cudaEventDestroy(ev[0]);
       cudaEventDestroy(ev[1]);
-      for (unsigned path = 1; path < 5; ++path)
-        if (plan_applies(f, path) && ms[path] < ms[best]) best = path;
+      for (unsigned path = 0; path < 5; ++path)
+        for (unsigned ti = 0; ti < 3; ++ti)
+          if (plan_applies(f, path) && tiles_apply(path, ti) && ms[path][ti] < ms[best][best_ti]) {
+            best = path;
+            best_ti = ti;
+          }
     }
     c.line_path = best;
+    if (possible) c.queries_per_lane = kTiles[best_ti];
     f->cfg = c;
     f->invalidate_plans();
     if (line_path) *line_path = best;

@@ -25,6 +25,11 @@
 //    and writes them with one coalesced streaming store. Small trees (LEAFS)
 //    stage the leaves too and finish each query in shared memory.
 //
+// With 2 or 4 tiles per warp (PBSEQ, chosen by the line-path tuner) Phase A runs
+// all tiles' descents together — their dependent probe chains overlap — and Phase B
+// then takes one tile at a time, so the registers holding line quarters stay those of
+// one tile.
+//
 // Query addresses are read with coalesced loads of the top word (L1::no_allocate,
 // L2 evict_first), one tile ahead of their use; tree lines use evict_last. CTAs
 // are persistent (grid = SMs x resident CTAs, default one 1024-thread CTA per
@@ -487,7 +492,7 @@ __device__ __forceinline__ unsigned leaf_search_smem(const unsigned long long* l
 // checks (the texture line paths are instantiated for TAS = DEPTH and DEPTH - 1, the
 // staging every BASELINE FIB uses; TAS = 0 reads the count from the launch).
 template <int DEPTH, int VB, int TILES, int THREADS, int MINB, bool CHECKED, int INPUT = kInAddr, bool LEAFS = false,
-          int TEXL = 0, int LEAFTEX = 0, bool HALF = false, int TAS = 0>
+          int TEXL = 0, int LEAFTEX = 0, bool HALF = false, int TAS = 0, bool PBSEQ = false>
 __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const LookupParams p) {
   using F = LeafFmt<VB>;
   // Texture leaf fetches as sector-disjoint halves (tex_line_at) for 1-byte next
@@ -641,185 +646,209 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
       continue;
     }
 
-    // Phase B: the group's queries, one 128-byte line per query per level.
-    unsigned long long qk[NS];
-    unsigned nd[NS];
+    // PBSEQ: Phase A runs TILES tiles at once (their dependent probe chains overlap)
+    // and Phase B then takes one tile at a time, so its line registers stay those of
+    // one tile; otherwise Phase B carries all TILES tiles together.
+    constexpr int PBT = PBSEQ ? 1 : TILES;  // tiles per Phase B pass
+    constexpr int NSB = 4 * PBT;            // queries in flight per 4-lane group
+#pragma unroll 1
+    for (int pb = 0; pb < (PBSEQ ? TILES : 1); ++pb) {
+      unsigned long long kcur[PBT];
+      unsigned ncur[PBT];
 #pragma unroll
-    for (int t = 0; t < TILES; ++t)
+      for (int t = 0; t < PBT; ++t) {
+        kcur[t] = key[t];
+        ncur[t] = node[t];
+        if constexpr (PBSEQ) {
 #pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        qk[4 * t + s] = __shfl_sync(kFull, key[t], s, 4);
-        nd[4 * t + s] = __shfl_sync(kFull, node[t], s, 4);
+          for (int u = 1; u < TILES; ++u)
+            if (pb == u) {
+              kcur[t] = key[u];
+              ncur[t] = node[u];
+            }
+        }
       }
-    unsigned long long w[NS][4];
-    // Internal L2 levels [TA, DEPTH): a runtime-count loop (one back-edge per
-    // level instead of a compare-and-branch per possible level), then the leaf.
-#pragma unroll
-    for (int li = 0; li < DEPTH; ++li) {
-      // Fully unrolled (static register indexing, scheduled across levels); the
-      // level index is TA-relative so the common TA == DEPTH case skips it with
-      // one uniform branch.
-      if (li >= DEPTH - static_cast<int>(TA)) break;
-      const unsigned l = TA + li;
-      // 32-bit word offsets (the layout keeps the array below 2^32 words).
-      const unsigned line_w = static_cast<unsigned>(p.level_start[l]);
-      const unsigned base_w = line_w + j * 4u;
-      if (CHECKED) {
-#pragma unroll
-        for (int s = 0; s < NS; ++s)
-          if (nd[s] >= p.level_nodes[l]) {
-            violations |= 2u;
-            nd[s] = 0;
-          }
+      const int tb0 = PBSEQ ? pb : 0;
+      // Phase B: the group's queries, one 128-byte line per query per level.
+      unsigned long long qk[NSB];
+      unsigned nd[NSB];
+  #pragma unroll
+      for (int t = 0; t < PBT; ++t)
+  #pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          qk[4 * t + s] = __shfl_sync(kFull, kcur[t], s, 4);
+          nd[4 * t + s] = __shfl_sync(kFull, ncur[t], s, 4);
+        }
+      unsigned long long w[NSB][4];
+      // Internal L2 levels [TA, DEPTH): a runtime-count loop (one back-edge per
+      // level instead of a compare-and-branch per possible level), then the leaf.
+  #pragma unroll
+      for (int li = 0; li < DEPTH; ++li) {
+        // Fully unrolled (static register indexing, scheduled across levels); the
+        // level index is TA-relative so the common TA == DEPTH case skips it with
+        // one uniform branch.
+        if (li >= DEPTH - static_cast<int>(TA)) break;
+        const unsigned l = TA + li;
+        // 32-bit word offsets (the layout keeps the array below 2^32 words).
+        const unsigned line_w = static_cast<unsigned>(p.level_start[l]);
+        const unsigned base_w = line_w + j * 4u;
+        if (CHECKED) {
+  #pragma unroll
+          for (int s = 0; s < NSB; ++s)
+            if (nd[s] >= p.level_nodes[l]) {
+              violations |= 2u;
+              nd[s] = 0;
+            }
+        }
+  #pragma unroll
+        for (int s = 0; s < NSB; ++s) {
+          // Internal L2 levels through the texture pipe, leaves through the LSU:
+          // the two pipes of L1TEX share the load, which helps the deep trees (C2:
+          // +8 %); leaves through the texture pipe lose on L2-missing workloads
+          // (C1 -17 %), so they stay on the LSU path.
+          if (TEXL == 1 || (TEXL == 2 && s < NSB / 2))
+            // (the per-slot texel form here: the lane-base form cost C2 0.35 %, 64 vs 60 registers)
+            tex_line_at<LPM6_INT_SECTORS != 0>(p.tex, ((line_w + nd[s] * 16u) >> 1) + (LPM6_INT_SECTORS ? j : 2u * j),
+                                               0u, w[s]);
+          else
+            ld_line_quarter(p.lines + (base_w + nd[s] * 16u), w[s]);
+        }
+        if (CHECKED) {  // one line per query: the lane owning query (t, j) counts it
+  #pragma unroll
+          for (int t = 0; t < PBT; ++t)
+            if ((st * TILES + tb0 + t) * 32ull + lane < p.n) ++visits;
+        }
+  #if LPM6_RANK_MODE == 1
+        {
+          unsigned r[NSB];
+          group_ranks<NSB, false>(qk, w, ~0u, ~0u, r);
+  #pragma unroll
+          for (int s = 0; s < NSB; ++s) nd[s] = nd[s] * 16u + r[s];
+        }
+  #else
+  #pragma unroll
+        for (int s = 0; s < NSB; ++s) nd[s] = nd[s] * 16u + group_rank(qk[s], w[s], 4u, gmask);
+  #endif
       }
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        // Internal L2 levels through the texture pipe, leaves through the LSU:
-        // the two pipes of L1TEX share the load, which helps the deep trees (C2:
-        // +8 %); leaves through the texture pipe lose on L2-missing workloads
-        // (C1 -17 %), so they stay on the LSU path.
-        if (TEXL == 1 || (TEXL == 2 && s < NS / 2))
-          // (the per-slot texel form here: the lane-base form cost C2 0.35 %, 64 vs 60 registers)
-          tex_line_at<LPM6_INT_SECTORS != 0>(p.tex, ((line_w + nd[s] * 16u) >> 1) + (LPM6_INT_SECTORS ? j : 2u * j),
-                                             0u, w[s]);
-        else
-          ld_line_quarter(p.lines + (base_w + nd[s] * 16u), w[s]);
-      }
-      if (CHECKED) {  // one line per query: the lane owning query (t, j) counts it
-#pragma unroll
-        for (int t = 0; t < TILES; ++t)
-          if ((st * TILES + t) * 32ull + lane < p.n) ++visits;
-      }
-#if LPM6_RANK_MODE == 1
-      {
-        unsigned r[NS];
-        group_ranks<NS, false>(qk, w, ~0u, ~0u, r);
-#pragma unroll
-        for (int s = 0; s < NS; ++s) nd[s] = nd[s] * 16u + r[s];
-      }
-#else
-#pragma unroll
-      for (int s = 0; s < NS; ++s) nd[s] = nd[s] * 16u + group_rank(qk[s], w[s], 4u, gmask);
-#endif
-    }
-    unsigned leafn[INPUT == kInKeyOrd ? NS : 1];  // kInKeyOrd: leaf node of each query
-    constexpr bool half = HALF;  // the FIB's leaf format (half-line leaves: 2-byte next hops)
-    if constexpr (half) {  // half-line leaves (layout.hpp): lane j reads words 2j, 2j+1 of its leaf
-      const unsigned line_w = static_cast<unsigned>(p.level_start[DEPTH]);
-      if (CHECKED) {
-#pragma unroll
-        for (int s = 0; s < NS; ++s)
-          if (nd[s] >= p.level_nodes[DEPTH]) {
-            violations |= 2u;
-            nd[s] = 0;
-          }
-      }
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        // 16 bytes per lane: one texture fetch, or one 16-byte load
-        if (LEAFTEX == 1 || LEAFTEX == 3 || (LEAFTEX == 2 && s >= NS / 2))
-          tex_half_leaf(p.tex, ((line_w + nd[s] * kHalfLeafWords) >> 1) + j, w[s]);
-        else
-          ld_half_leaf(p.lines + line_w + nd[s] * kHalfLeafWords + 2u * j, w[s]);
-      }
-      if constexpr (INPUT == kInKeyOrd) {
-#pragma unroll
-        for (int s = 0; s < NS; ++s) leafn[s] = nd[s];
-      }
-      if (CHECKED) {
-#pragma unroll
-        for (int t = 0; t < TILES; ++t)
-          if ((st * TILES + t) * 32ull + lane < p.n) ++visits;
-      }
-      unsigned r[NS];
-      group_ranks<NS, false, 2>(qk, w, j < 3u ? ~0u : 0u, 0u, r);  // lane 3 holds the next hops
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        if (CHECKED && r[s] == 0) violations |= 4u;
-        nd[s] = CHECKED && r[s] == 0 ? 0u : r[s] - 1u;
-      }
-    } else {  // the leaf line: ordinal = rank - 1
-      const unsigned line_w = static_cast<unsigned>(p.level_start[DEPTH]);
-      const unsigned base_w = line_w + j * 4u;
-      if (CHECKED) {
-#pragma unroll
-        for (int s = 0; s < NS; ++s)
-          if (nd[s] >= p.level_nodes[DEPTH]) {
-            violations |= 2u;
-            nd[s] = 0;
-          }
-      }
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        // LEAFTEX 1: every slot through the texture pipe; 2: the upper half of the
-        // group's slots (compile-time split, both pipes busy in one warp).
-        if (LEAFTEX == 1 || LEAFTEX == 3 || (LEAFTEX == 2 && s >= NS / 2))
-          // sector-disjoint fetches (kLeafSectors): for 1-byte next hops the leaf
-          // keeps the same key slots and value lane in both orders (the values are
-          // words 14-15 = lane 3's second texel either way)
-          tex_line_at<kLeafSectors>(p.tex, tex_lane_base<kLeafSectors>(line_w, j), nd[s], w[s]);
-        else
-          ld_line_quarter(p.lines + (base_w + nd[s] * 16u), w[s]);
-      }
-      if constexpr (INPUT == kInKeyOrd) {
-#pragma unroll
-        for (int s = 0; s < NS; ++s) leafn[s] = nd[s];
-      }
-      if (CHECKED) {
-#pragma unroll
-        for (int t = 0; t < TILES; ++t)
-          if ((st * TILES + t) * 32ull + lane < p.n) ++visits;
-      }
-#if LPM6_RANK_MODE == 1
-      {
-        unsigned r[NS];
-        group_ranks<NS, true>(qk, w, leaf_valid >= 2 ? ~0u : 0u, leaf_valid >= 4 ? ~0u : 0u, r);
-#pragma unroll
-        for (int s = 0; s < NS; ++s) {
+      unsigned leafn[INPUT == kInKeyOrd ? NSB : 1];  // kInKeyOrd: leaf node of each query
+      constexpr bool half = HALF;  // the FIB's leaf format (half-line leaves: 2-byte next hops)
+      if constexpr (half) {  // half-line leaves (layout.hpp): lane j reads words 2j, 2j+1 of its leaf
+        const unsigned line_w = static_cast<unsigned>(p.level_start[DEPTH]);
+        if (CHECKED) {
+  #pragma unroll
+          for (int s = 0; s < NSB; ++s)
+            if (nd[s] >= p.level_nodes[DEPTH]) {
+              violations |= 2u;
+              nd[s] = 0;
+            }
+        }
+  #pragma unroll
+        for (int s = 0; s < NSB; ++s) {
+          // 16 bytes per lane: one texture fetch, or one 16-byte load
+          if (LEAFTEX == 1 || LEAFTEX == 3 || (LEAFTEX == 2 && s >= NSB / 2))
+            tex_half_leaf(p.tex, ((line_w + nd[s] * kHalfLeafWords) >> 1) + j, w[s]);
+          else
+            ld_half_leaf(p.lines + line_w + nd[s] * kHalfLeafWords + 2u * j, w[s]);
+        }
+        if constexpr (INPUT == kInKeyOrd) {
+  #pragma unroll
+          for (int s = 0; s < NSB; ++s) leafn[s] = nd[s];
+        }
+        if (CHECKED) {
+  #pragma unroll
+          for (int t = 0; t < PBT; ++t)
+            if ((st * TILES + tb0 + t) * 32ull + lane < p.n) ++visits;
+        }
+        unsigned r[NSB];
+        group_ranks<NSB, false, 2>(qk, w, j < 3u ? ~0u : 0u, 0u, r);  // lane 3 holds the next hops
+  #pragma unroll
+        for (int s = 0; s < NSB; ++s) {
           if (CHECKED && r[s] == 0) violations |= 4u;
           nd[s] = CHECKED && r[s] == 0 ? 0u : r[s] - 1u;
         }
-      }
-#else
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        const unsigned r = group_rank(qk[s], w[s], leaf_valid, gmask);
-        if (CHECKED && r == 0) violations |= 4u;
-        nd[s] = CHECKED && r == 0 ? 0u : r - 1u;
-      }
-#endif
-    }
-
-    if constexpr (INPUT == kInKeyOrd) {  // lane j stores the ordinal of its own query (4t + j of the group)
-#pragma unroll
-      for (int t = 0; t < TILES; ++t) {
-        const unsigned kl = half ? kHalfLeafKeys : static_cast<unsigned>(F::kL);
-        unsigned o = leafn[4 * t] * kl + nd[4 * t];
-#pragma unroll
-        for (int s = 1; s < 4; ++s) o = j == static_cast<unsigned>(s) ? leafn[4 * t + s] * kl + nd[4 * t + s] : o;
-        const unsigned long long qi = (st * TILES + t) * 32ull + lane;
-        if (qi < p.n) asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p.ord + qi), "r"(o));
-      }
-      if (p.out == nullptr) continue;  // ordinals only
-    }
-    // Leaf values: the value lane extracts the group's next hops and stores them.
-    if constexpr (half) {
-      if (j == 3u) {  // half-line leaves: lane 3 holds words 6-7, the next hops
-#pragma unroll
-        for (int t = 0; t < TILES; ++t) {
-          unsigned v[4];
-#pragma unroll
-          for (int s = 0; s < 4; ++s) v[s] = half_leaf_value<VB, 4>(w[4 * t + s], nd[4 * t + s]);
-          store_group<VB>(p, (st * TILES + t) * 32ull + gbase, v);
+      } else {  // the leaf line: ordinal = rank - 1
+        const unsigned line_w = static_cast<unsigned>(p.level_start[DEPTH]);
+        const unsigned base_w = line_w + j * 4u;
+        if (CHECKED) {
+  #pragma unroll
+          for (int s = 0; s < NSB; ++s)
+            if (nd[s] >= p.level_nodes[DEPTH]) {
+              violations |= 2u;
+              nd[s] = 0;
+            }
         }
+  #pragma unroll
+        for (int s = 0; s < NSB; ++s) {
+          // LEAFTEX 1: every slot through the texture pipe; 2: the upper half of the
+          // group's slots (compile-time split, both pipes busy in one warp).
+          if (LEAFTEX == 1 || LEAFTEX == 3 || (LEAFTEX == 2 && s >= NSB / 2))
+            // sector-disjoint fetches (kLeafSectors): for 1-byte next hops the leaf
+            // keeps the same key slots and value lane in both orders (the values are
+            // words 14-15 = lane 3's second texel either way)
+            tex_line_at<kLeafSectors>(p.tex, tex_lane_base<kLeafSectors>(line_w, j), nd[s], w[s]);
+          else
+            ld_line_quarter(p.lines + (base_w + nd[s] * 16u), w[s]);
+        }
+        if constexpr (INPUT == kInKeyOrd) {
+  #pragma unroll
+          for (int s = 0; s < NSB; ++s) leafn[s] = nd[s];
+        }
+        if (CHECKED) {
+  #pragma unroll
+          for (int t = 0; t < PBT; ++t)
+            if ((st * TILES + tb0 + t) * 32ull + lane < p.n) ++visits;
+        }
+  #if LPM6_RANK_MODE == 1
+        {
+          unsigned r[NSB];
+          group_ranks<NSB, true>(qk, w, leaf_valid >= 2 ? ~0u : 0u, leaf_valid >= 4 ? ~0u : 0u, r);
+  #pragma unroll
+          for (int s = 0; s < NSB; ++s) {
+            if (CHECKED && r[s] == 0) violations |= 4u;
+            nd[s] = CHECKED && r[s] == 0 ? 0u : r[s] - 1u;
+          }
+        }
+  #else
+  #pragma unroll
+        for (int s = 0; s < NSB; ++s) {
+          const unsigned r = group_rank(qk[s], w[s], leaf_valid, gmask);
+          if (CHECKED && r == 0) violations |= 4u;
+          nd[s] = CHECKED && r == 0 ? 0u : r - 1u;
+        }
+  #endif
       }
-    } else if (j == static_cast<unsigned>(F::kValueLane)) {
-#pragma unroll
-      for (int t = 0; t < TILES; ++t) {
-        unsigned v[4];
-#pragma unroll
-        for (int s = 0; s < 4; ++s) v[s] = leaf_value<VB, VB != 1 || LEAFTEX == 3>(w[4 * t + s], nd[4 * t + s]);
-        store_group<VB>(p, (st * TILES + t) * 32ull + gbase, v);
+
+      if constexpr (INPUT == kInKeyOrd) {  // lane j stores the ordinal of its own query (4t + j of the group)
+  #pragma unroll
+        for (int t = 0; t < PBT; ++t) {
+          const unsigned kl = half ? kHalfLeafKeys : static_cast<unsigned>(F::kL);
+          unsigned o = leafn[4 * t] * kl + nd[4 * t];
+  #pragma unroll
+          for (int s = 1; s < 4; ++s) o = j == static_cast<unsigned>(s) ? leafn[4 * t + s] * kl + nd[4 * t + s] : o;
+          const unsigned long long qi = (st * TILES + tb0 + t) * 32ull + lane;
+          if (qi < p.n) asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p.ord + qi), "r"(o));
+        }
+        if (p.out == nullptr) continue;  // ordinals only
+      }
+      // Leaf values: the value lane extracts the group's next hops and stores them.
+      if constexpr (half) {
+        if (j == 3u) {  // half-line leaves: lane 3 holds words 6-7, the next hops
+  #pragma unroll
+          for (int t = 0; t < PBT; ++t) {
+            unsigned v[4];
+  #pragma unroll
+            for (int s = 0; s < 4; ++s) v[s] = half_leaf_value<VB, 4>(w[4 * t + s], nd[4 * t + s]);
+            store_group<VB>(p, (st * TILES + tb0 + t) * 32ull + gbase, v);
+          }
+        }
+      } else if (j == static_cast<unsigned>(F::kValueLane)) {
+  #pragma unroll
+        for (int t = 0; t < PBT; ++t) {
+          unsigned v[4];
+  #pragma unroll
+          for (int s = 0; s < 4; ++s) v[s] = leaf_value<VB, VB != 1 || LEAFTEX == 3>(w[4 * t + s], nd[4 * t + s]);
+          store_group<VB>(p, (st * TILES + tb0 + t) * 32ull + gbase, v);
+        }
       }
     }
   }
@@ -837,26 +866,30 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
 // of each width compile in parallel. bench.py --sweep measures the shapes.
 // The default-shape kernel of one depth: the staged-level count as a template
 // constant when it is DEPTH or DEPTH - 1 (TAS), else read from the launch.
-template <int D, int VB, int INPUT, int TEXL, int LEAFTEX, bool HALF>
+// TL = 2: two tiles per warp iteration through Phase A, Phase B one tile at a time
+// (PBSEQ; 1024 threads, texture line paths, address input).
+template <int D, int VB, int INPUT, int TEXL, int LEAFTEX, bool HALF, int TL = 1>
 KernelFn pick_ta(int ta) {
+  constexpr bool SEQ = TL > 1;
   if constexpr (LPM6_STATIC_TA != 0) {
-    if (ta == D) return lpm6_lookup_kernel<D, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF, D>;
+    if (ta == D) return lpm6_lookup_kernel<D, VB, TL, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF, D, SEQ>;
     if constexpr (D >= 2)
-      if (ta == D - 1) return lpm6_lookup_kernel<D, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF, D - 1>;
+      if (ta == D - 1)
+        return lpm6_lookup_kernel<D, VB, TL, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF, D - 1, SEQ>;
   }
-  return lpm6_lookup_kernel<D, VB, 1, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF>;
+  return lpm6_lookup_kernel<D, VB, TL, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF, 0, SEQ>;
 }
 
-template <int VB, int INPUT, int TEXL, int LEAFTEX, bool HALF>
+template <int VB, int INPUT, int TEXL, int LEAFTEX, bool HALF, int TL = 1>
 KernelFn pick_depth_texl(int depth, int ta = 0) {
   switch (depth) {
-    case 1: return pick_ta<1, VB, INPUT, TEXL, LEAFTEX, HALF>(ta);
-    case 2: return pick_ta<2, VB, INPUT, TEXL, LEAFTEX, HALF>(ta);
-    case 3: return pick_ta<3, VB, INPUT, TEXL, LEAFTEX, HALF>(ta);
-    case 4: return pick_ta<4, VB, INPUT, TEXL, LEAFTEX, HALF>(ta);
-    case 5: return pick_ta<5, VB, INPUT, TEXL, LEAFTEX, HALF>(ta);
-    case 6: return pick_ta<6, VB, INPUT, TEXL, LEAFTEX, HALF>(ta);
-    case 7: return pick_ta<7, VB, INPUT, TEXL, LEAFTEX, HALF>(ta);
+    case 1: return pick_ta<1, VB, INPUT, TEXL, LEAFTEX, HALF, TL>(ta);
+    case 2: return pick_ta<2, VB, INPUT, TEXL, LEAFTEX, HALF, TL>(ta);
+    case 3: return pick_ta<3, VB, INPUT, TEXL, LEAFTEX, HALF, TL>(ta);
+    case 4: return pick_ta<4, VB, INPUT, TEXL, LEAFTEX, HALF, TL>(ta);
+    case 5: return pick_ta<5, VB, INPUT, TEXL, LEAFTEX, HALF, TL>(ta);
+    case 6: return pick_ta<6, VB, INPUT, TEXL, LEAFTEX, HALF, TL>(ta);
+    case 7: return pick_ta<7, VB, INPUT, TEXL, LEAFTEX, HALF, TL>(ta);
     default: return nullptr;
   }
 }
@@ -912,6 +945,23 @@ template <int VB, bool HALF>
 KernelFn pick_kernel_fmt(const PickArgs& a) {
   const int depth = a.depth;
   const bool dflt = a.tiles == 1 && a.threads == 1024 && a.minb == 1;
+  if (a.leaftex && (a.tiles == 2 || a.tiles == 4) && a.threads == 1024 && a.minb == 1) {
+    // 2 or 4 tiles per warp through Phase A, Phase B one tile at a time (PBSEQ):
+    // address input, texture leaves (modes 1 and 3), internal L2 levels on one pipe
+    if (a.leafs || a.checked || a.input != kInAddr || a.texl > 1) return nullptr;
+    if (a.leaftex == 1)
+      return a.tiles == 4 ? (a.texl ? pick_depth_texl<VB, kInAddr, 1, 1, HALF, 4>(depth, a.ta)
+                                    : pick_depth_texl<VB, kInAddr, 0, 1, HALF, 4>(depth, a.ta))
+                          : (a.texl ? pick_depth_texl<VB, kInAddr, 1, 1, HALF, 2>(depth, a.ta)
+                                    : pick_depth_texl<VB, kInAddr, 0, 1, HALF, 2>(depth, a.ta));
+    if constexpr (VB == 1 && !HALF)
+      if (a.leaftex == 3)
+        return a.tiles == 4 ? (a.texl ? pick_depth_texl<VB, kInAddr, 1, 3, HALF, 4>(depth, a.ta)
+                                      : pick_depth_texl<VB, kInAddr, 0, 3, HALF, 4>(depth, a.ta))
+                            : (a.texl ? pick_depth_texl<VB, kInAddr, 1, 3, HALF, 2>(depth, a.ta)
+                                      : pick_depth_texl<VB, kInAddr, 0, 3, HALF, 2>(depth, a.ta));
+    return nullptr;
+  }
   if (a.leaftex) {  // default shape, unchecked, no leaf image, depth >= 1
     if (a.leafs || a.checked || !dflt) return nullptr;
     switch (a.input) {

@@ -1,5 +1,6 @@
 """Line paths (lpm6cu_kernel_config.line_path: which L1TEX pipe carries the leaf
-and internal L2 lines) and the measured choice between them
+and internal L2 lines), the tiles per warp of the texture leaf paths
+(queries_per_lane 1, 2 or 4 at 1024 threads) and the measured choice between them
 (lpm6cu_fib_tune_line_path).
 
 A line path changes only how a line reaches registers, so every answer must
@@ -44,6 +45,21 @@ def test_texture_line_path_matches_oracle_on_workloads(lpm, orc, cuda, workload)
         torch.cuda.synchronize()
         np.testing.assert_array_equal(got.cpu().numpy().view(view).astype(np.uint32), want, err_msg=f"lp={lp}")
         np.testing.assert_array_equal(gk.cpu().numpy().view(view).astype(np.uint32), want, err_msg=f"keys lp={lp}")
+    # 2 and 4 tiles per warp (Phase A over all tiles, Phase B one tile at a time): the
+    # texture leaf paths run them, the others fall back to one tile; results unchanged
+    for qpl in (2, 4):
+        for lp in (1, 4, 0, 2, 3):
+            cfg = dev.set_kernel_config(line_path=lp, threads_per_cta=1024, queries_per_lane=qpl)
+            assert cfg["queries_per_lane"] == qpl and cfg["line_path"] == lp
+            # ragged batch: not a multiple of the 32 * qpl queries a warp takes per iteration
+            m = len(da) - 77
+            got = dev.lookup_batch(da[:m])
+            gk = dev.lookup_keys(dk)
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(got.cpu().numpy().view(view).astype(np.uint32), want[:m],
+                                          err_msg=f"qpl={qpl} lp={lp}")
+            np.testing.assert_array_equal(gk.cpu().numpy().view(view).astype(np.uint32), want,
+                                          err_msg=f"keys qpl={qpl} lp={lp}")
 
 
 def test_tuner_picks_a_path_and_keeps_results(lpm, orc, cuda):
@@ -59,7 +75,10 @@ def test_tuner_picks_a_path_and_keeps_results(lpm, orc, cuda):
         base = dev.lookup_batch(d).clone()
         chosen = dev.tune_line_path(d)
         assert chosen in (0, 1, 2, 3, 4)
-        assert dev.kernel_config()["line_path"] == chosen
+        cfg = dev.kernel_config()
+        assert cfg["line_path"] == chosen
+        # the tuner also picks the tiles per warp: 2 or 4 only on the texture leaf paths
+        assert cfg["queries_per_lane"] in ((1, 2, 4) if chosen in (1, 4) else (1,))
         again = dev.lookup_batch(d)
         torch.cuda.synchronize()
         assert torch.equal(base, again)

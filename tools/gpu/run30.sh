@@ -1,0 +1,12 @@
+# Two tiles per warp through Phase A, Phase B one tile at a time (queries_per_lane 2 at
+# 1024 threads) vs one tile, on the texture line path; parity on the bench sample.
+cd $GRAFT_REPO_ROOT
+O=gpurun_out
+for r in 1 2; do for w in C2 C1 C3b C3a; do for qpl in 1 2; do
+  timeout 300 python bench.py --workload $w --line-path tex --queries-per-lane $qpl --threads 1024 \
+    --no-cpu --no-e2e --no-extras --steps 10 --warmup 3 2>$O/r30_err.txt | python -c "
+import json,sys
+t=sys.stdin.read().strip().splitlines()
+if not t: print('$w qpl $qpl FAILED', open('$O/r30_err.txt').read()[-400:].replace(chr(10),' ')); sys.exit()
+d=json.loads(t[-1]); print('$w', 'qpl', $qpl, round(d['value'],2), d['kernel'], d['parity_sample']['mismatches'])" >> $O/r30_ab.log
+done; done; done
