@@ -78,6 +78,11 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 #ifndef LPM6_INT_SECTORS
 #define LPM6_INT_SECTORS 0
 #endif
+// PBSEQ: Phase B's per-tile passes unrolled (1: ptxas may overlap one tile's leaf
+// fetch with the next tile's internal level) or kept a loop (0). A/B switch.
+#ifndef LPM6_PB_UNROLL
+#define LPM6_PB_UNROLL 1
+#endif
 // Staged-level count as a template constant in the texture line-path kernels (1) or
 // always read from the launch (0). A/B switch.
 #ifndef LPM6_STATIC_TA
@@ -651,7 +656,11 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
     // one tile; otherwise Phase B carries all TILES tiles together.
     constexpr int PBT = PBSEQ ? 1 : TILES;  // tiles per Phase B pass
     constexpr int NSB = 4 * PBT;            // queries in flight per 4-lane group
+#if LPM6_PB_UNROLL
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
     for (int pb = 0; pb < (PBSEQ ? TILES : 1); ++pb) {
       unsigned long long kcur[PBT];
       unsigned ncur[PBT];
