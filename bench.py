@@ -84,17 +84,29 @@ def shared_gpu_mode():
     return os.environ.get("LPM6_BENCH_SHARED_GPU", "") not in ("", "0")
 
 
+def force_dist_mode():
+    """LPM6_BENCH_FORCE_DIST=1: create the process group at world size 1 too, so that a
+    one-GPU box runs every collective of the multi-rank path (the line-array broadcast,
+    the MAX reductions, the gathers and barriers) through NCCL itself. The line says so."""
+    return os.environ.get("LPM6_BENCH_FORCE_DIST", "") not in ("", "0")
+
+
 def init_dist(ws, local, backend="nccl"):
     import torch
     import torch.distributed as dist
-    if ws > 1 and not dist.is_initialized():
+    force = force_dist_mode()
+    if (ws > 1 or force) and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if ws == 1:  # forced: a standalone rendezvous when not under torchrun
+            os.environ.setdefault("MASTER_PORT", "29537")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         if backend == "nccl":
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
-    return dist if ws > 1 else None
+    return dist if (ws > 1 or force) else None
 
 
 # ---- clocks ---------------------------------------------------------------------------
@@ -670,6 +682,8 @@ def run_chunked(args, lpm, dispatch, fdev, fib, info, geom, cfg, ws, rank, dev_i
     }
     if ws > 1 and shared_gpu_mode():
         line["harness_check"] = "LPM6_BENCH_SHARED_GPU: ranks shared GPUs over gloo; not a bench value"
+    if ws == 1 and force_dist_mode():
+        line["harness_check"] = "LPM6_BENCH_FORCE_DIST: the multi-rank collectives ran through NCCL at world size 1"
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
@@ -917,6 +931,8 @@ def main():
                                 "matches_address_path": k["matches_address_path"]}
     if ws > 1 and shared_gpu_mode():
         line["harness_check"] = "LPM6_BENCH_SHARED_GPU: ranks shared GPUs over gloo; not a bench value"
+    if ws == 1 and force_dist_mode():
+        line["harness_check"] = "LPM6_BENCH_FORCE_DIST: the multi-rank collectives ran through NCCL at world size 1"
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()

@@ -12,16 +12,19 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
 OBJ = ROOT / "build" / "obj"
 # (label, object, template args of lpm6_lookup_kernel<DEPTH, VB, TILES, THREADS, MINB, CHECKED, INPUT, LEAFS, TEXL,
-#  LEAFTEX, HALF, TAS>)
+#  LEAFTEX, HALF, TAS, PBSEQ>)
 KERNELS = [
-    ("C2/C4 bench kernel, line path 1, half-line leaves (depth 5, u16)", "lookup_vb2.cu.o",
-     "ILi5ELi2ELi1ELi1024ELi1ELb0ELi0ELb0ELi1ELi1ELb1ELi4EE"),
-    ("C2/C4 line path 3 (half of the level-4 lines on the LSU), half-line leaves", "lookup_vb2.cu.o",
-     "ILi5ELi2ELi1ELi1024ELi1ELb0ELi0ELb0ELi2ELi1ELb1ELi4EE"),
-    ("C1/C3b bench kernel, line path 1 (depth 4, u8)", "lookup_vb1.cu.o", "ILi4ELi1ELi1ELi1024ELi1ELb0ELi0ELb0ELi0ELi1ELb0ELi4EE"),
-    ("C3a bench kernel, line path 4", "lookup_vb1.cu.o", "ILi4ELi1ELi1ELi1024ELi1ELb0ELi0ELb0ELi0ELi3ELb0ELi4EE"),
-    ("C1 line path 2 (split leaves)", "lookup_vb1.cu.o", "ILi4ELi1ELi1ELi1024ELi1ELb0ELi0ELb0ELi0ELi2ELb0ELi4EE"),
-    ("C0 leaf image (depth 2, u8)", "lookup_vb1.cu.o", "ILi2ELi1ELi1ELi1024ELi1ELb0ELi0ELb1ELi0ELi0ELb0ELi0EE"),
+    ("C2/C4 bench kernel: line path 1, half-line leaves, 4 tiles per warp, PBSEQ (depth 5, u16)", "lookup_vb2.cu.o",
+     "ILi5ELi2ELi4ELi1024ELi1ELb0ELi0ELb0ELi1ELi1ELb1ELi4ELb1EE"),
+    ("C2/C4 one tile per warp, line path 1, half-line leaves", "lookup_vb2.cu.o",
+     "ILi5ELi2ELi1ELi1024ELi1ELb0ELi0ELb0ELi1ELi1ELb1ELi4ELb0EE"),
+    ("C1/C3b bench kernel: line path 1, 2 tiles per warp, PBSEQ (depth 4, u8)", "lookup_vb1.cu.o",
+     "ILi4ELi1ELi2ELi1024ELi1ELb0ELi0ELb0ELi0ELi1ELb0ELi4ELb1EE"),
+    ("C3a bench kernel: line path 4, 2 tiles per warp, PBSEQ", "lookup_vb1.cu.o",
+     "ILi4ELi1ELi2ELi1024ELi1ELb0ELi0ELb0ELi0ELi3ELb0ELi4ELb1EE"),
+    ("C1 one tile per warp, line path 1", "lookup_vb1.cu.o", "ILi4ELi1ELi1ELi1024ELi1ELb0ELi0ELb0ELi0ELi1ELb0ELi4ELb0EE"),
+    ("C1 line path 2 (split leaves)", "lookup_vb1.cu.o", "ILi4ELi1ELi1ELi1024ELi1ELb0ELi0ELb0ELi0ELi2ELb0ELi4ELb0EE"),
+    ("C0 leaf image (depth 2, u8)", "lookup_vb1.cu.o", "ILi2ELi1ELi1ELi1024ELi1ELb0ELi0ELb1ELi0ELi0ELb0ELi0ELb0EE"),
 ]
 WATCH = ["UBLKCP", "SYNCS", "ELECT", "LDS", "LDG", "TLD", "SHFL", "VOTE", "POPC", "PRMT", "ISETP", "STG", "LDL", "STL",
          "BRA", "EXIT"]
