@@ -83,6 +83,14 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 #ifndef LPM6_PB_UNROLL
 #define LPM6_PB_UNROLL 1
 #endif
+// Phase B's query keys: 0 = broadcast from the owner lane by shuffles (two SHFL per
+// query), 1 = every lane of a 4-lane group loads its group's four keys from the
+// address / key stream itself (one 8-byte load per query: the stream was read one
+// iteration ago, so it comes from L2) at the start of each Phase B pass, 2 = the same,
+// issued one pass ahead (pass 0's before Phase A). A/B switch.
+#ifndef LPM6_GROUP_KEY_LOAD
+#define LPM6_GROUP_KEY_LOAD 0
+#endif
 // Staged-level count as a template constant in the texture line-path kernels (1) or
 // always read from the launch (0). A/B switch.
 #ifndef LPM6_STATIC_TA
@@ -540,6 +548,20 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
     }
     return k;
   };
+  // Clamped key of query (tile, group lane s) for Phase B, loaded by every lane of the
+  // group (LPM6_GROUP_KEY_LOAD): 8 distinct 8-byte words per warp instruction.
+  constexpr bool kGroupLoad = LPM6_GROUP_KEY_LOAD != 0 && (INPUT == kInAddr || INPUT == kInKey);
+  auto load_group_key = [&](unsigned long long tile, int s) -> unsigned long long {
+    const unsigned long long qi = tile * 32ull + gbase + s;
+    unsigned long long k = 0;
+    if (qi < p.n) {
+      if constexpr (INPUT == kInKey)
+        k = ld_stream<unsigned long long>(p.keys + qi, pol_stream);
+      else
+        k = ld_stream<unsigned long long>(reinterpret_cast<const unsigned long long*>(p.addrs + qi) + 1, pol_stream);
+    }
+    return k > kMaxQueryKey ? kMaxQueryKey : k;  // types.hpp:25
+  };
   unsigned long long next_key[TILES];
 #pragma unroll
   for (int t = 0; t < TILES; ++t) next_key[t] = load_key(warp0, t);
@@ -569,6 +591,14 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
       key[t] = next_key[t] > kMaxQueryKey ? kMaxQueryKey : next_key[t];  // types.hpp:25
       node[t] = 0;
       next_key[t] = load_key(st + nwarps, t);  // prefetch; consumed next iteration
+    }
+
+    // LPM6_GROUP_KEY_LOAD 2: the first Phase B pass's group keys, requested before Phase A.
+    constexpr bool kGroupAhead = kGroupLoad && LPM6_GROUP_KEY_LOAD == 2 && (PBSEQ || TILES == 1);
+    unsigned long long gk[4] = {0, 0, 0, 0};
+    if constexpr (kGroupAhead) {
+#pragma unroll
+      for (int s = 0; s < 4; ++s) gk[s] = load_group_key(st * TILES, s);
     }
 
     // Phase A: this thread's own queries through the shared-memory levels.
@@ -685,9 +715,20 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
       for (int t = 0; t < PBT; ++t)
   #pragma unroll
         for (int s = 0; s < 4; ++s) {
-          qk[4 * t + s] = __shfl_sync(kFull, kcur[t], s, 4);
+          if constexpr (kGroupAhead)
+            qk[4 * t + s] = gk[s];
+          else if constexpr (kGroupLoad)
+            qk[4 * t + s] = load_group_key(st * TILES + tb0 + t, s);
+          else
+            qk[4 * t + s] = __shfl_sync(kFull, kcur[t], s, 4);
           nd[4 * t + s] = __shfl_sync(kFull, ncur[t], s, 4);
         }
+      if constexpr (kGroupAhead && PBSEQ) {  // the next pass's group keys, consumed one pass later
+        if (pb + 1 < TILES) {
+  #pragma unroll
+          for (int s = 0; s < 4; ++s) gk[s] = load_group_key(st * TILES + pb + 1, s);
+        }
+      }
       unsigned long long w[NSB][4];
       // Internal L2 levels [TA, DEPTH): a runtime-count loop (one back-edge per
       // level instead of a compare-and-branch per possible level), then the leaf.
