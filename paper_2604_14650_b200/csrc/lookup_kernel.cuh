@@ -91,6 +91,12 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 #ifndef LPM6_GROUP_KEY_LOAD
 #define LPM6_GROUP_KEY_LOAD 0
 #endif
+// Phase B's query keys handed to the 4-lane groups through a per-warp shared-memory
+// slot (one STS.64 and four broadcast LDS.64 per lane and tile) instead of eight
+// shuffles, when the launch has room for the slots (LookupParams::key_slot_off). A/B switch.
+#ifndef LPM6_KEY_SMEM
+#define LPM6_KEY_SMEM 0
+#endif
 // Staged-level count as a template constant in the texture line-path kernels (1) or
 // always read from the launch (0). A/B switch.
 #ifndef LPM6_STATIC_TA
@@ -562,6 +568,10 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
     }
     return k > kMaxQueryKey ? kMaxQueryKey : k;  // types.hpp:25
   };
+  // LPM6_KEY_SMEM: this warp's key slot; word L + (L >> 4) holds lane L's key, so the
+  // store and each group read (8 distinct words, one per group) are conflict-free.
+  const bool use_slot = LPM6_KEY_SMEM != 0 && !LEAFS && p.key_slot_off != 0;
+  const uint32_t wslot = s_base + p.key_slot_off + (threadIdx.x >> 5) * kKeySlotBytes;
   unsigned long long next_key[TILES];
 #pragma unroll
   for (int t = 0; t < TILES; ++t) next_key[t] = load_key(warp0, t);
@@ -711,6 +721,22 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
       // Phase B: the group's queries, one 128-byte line per query per level.
       unsigned long long qk[NSB];
       unsigned nd[NSB];
+      if (use_slot) {
+  #pragma unroll
+        for (int t = 0; t < PBT; ++t) {
+          __syncwarp();  // the previous tile's reads of the slot are done
+          asm volatile("st.shared.u64 [%0], %1;" ::"r"(wslot + (lane + (lane >> 4)) * 8u), "l"(kcur[t]) : "memory");
+          __syncwarp();
+  #pragma unroll
+          for (int s = 0; s < 4; ++s) {
+            asm volatile("ld.shared.u64 %0, [%1];"
+                         : "=l"(qk[4 * t + s])
+                         : "r"(wslot + (gbase + s + (lane >> 4)) * 8u)
+                         : "memory");
+            nd[4 * t + s] = __shfl_sync(kFull, ncur[t], s, 4);
+          }
+        }
+      } else
   #pragma unroll
       for (int t = 0; t < PBT; ++t)
   #pragma unroll
