@@ -276,15 +276,6 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
                              : tiles_cfg;
   const size_t smem = image_bytes_of(f->g, smem_levels);
   const int threads = static_cast<int>(threads_cta);
-  // LPM6_KEY_SMEM (A/B build switch): per-warp key slots after the image when they fit.
-  size_t smem_total = smem;
-  unsigned key_slot_off = 0;
-#if defined(LPM6_KEY_SMEM) && LPM6_KEY_SMEM
-  if (smem > 0 && !leafs && (smem + 15) / 16 * 16 + (threads / 32) * kKeySlotBytes <= f->max_smem_optin) {
-    key_slot_off = static_cast<unsigned>((smem + 15) / 16 * 16);
-    smem_total = key_slot_off + (threads / 32) * kKeySlotBytes;
-  }
-#endif
   LaunchPlan plan;
   {
     auto* mf = const_cast<lpm6cu_fib*>(f);
@@ -299,12 +290,12 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
       // The attribute belongs to the kernel, which every FIB of this depth and
       // next-hop width shares: always set it to the device's opt-in maximum, never
       // to this FIB's own image size, so that no FIB can lower it under another.
-      if (smem_total > 48 * 1024)
+      if (smem > 48 * 1024)
         check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(f->max_smem_optin)),
                    "cudaFuncSetAttribute");
       int per_sm = 0;
-      check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem_total), "occupancy");
+      check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem), "occupancy");
       if (per_sm < 1) throw Error(Errc::CudaError, "lookup kernel cannot be resident with this configuration");
       if (f->cfg.ctas_per_sm > 0) per_sm = std::min<int>(per_sm, static_cast<int>(f->cfg.ctas_per_sm));
       slot.fn = fn;
@@ -337,7 +328,6 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
   p.err = f->d_err;
   std::memcpy(p.root, f->root, sizeof p.root);
   p.tex = f->tex;
-  p.key_slot_off = key_slot_off;
   {
     auto off = [&](unsigned l) { return static_cast<unsigned>((f->g.level_start[l] / kLineWords) * kNodeKeys * 8); };
     const unsigned ta = p.smem_levels;
@@ -348,7 +338,7 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
   const unsigned long long warps_per_cta = threads / 32;
   unsigned long long grid = static_cast<unsigned long long>(f->num_sms) * plan.per_sm;
   grid = std::min(grid, (ntiles + warps_per_cta - 1) / warps_per_cta);
-  plan.fn<<<static_cast<unsigned>(grid), threads, smem_total, stream>>>(p);
+  plan.fn<<<static_cast<unsigned>(grid), threads, smem, stream>>>(p);
   check_cuda(cudaGetLastError(), "lookup launch");
 }
 

@@ -83,20 +83,6 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 #ifndef LPM6_PB_UNROLL
 #define LPM6_PB_UNROLL 1
 #endif
-// Phase B's query keys: 0 = broadcast from the owner lane by shuffles (two SHFL per
-// query), 1 = every lane of a 4-lane group loads its group's four keys from the
-// address / key stream itself (one 8-byte load per query: the stream was read one
-// iteration ago, so it comes from L2) at the start of each Phase B pass, 2 = the same,
-// issued one pass ahead (pass 0's before Phase A). A/B switch.
-#ifndef LPM6_GROUP_KEY_LOAD
-#define LPM6_GROUP_KEY_LOAD 0
-#endif
-// Phase B's query keys handed to the 4-lane groups through a per-warp shared-memory
-// slot (one STS.64 and four broadcast LDS.64 per lane and tile) instead of eight
-// shuffles, when the launch has room for the slots (LookupParams::key_slot_off). A/B switch.
-#ifndef LPM6_KEY_SMEM
-#define LPM6_KEY_SMEM 0
-#endif
 // Staged-level count as a template constant in the texture line-path kernels (1) or
 // always read from the launch (0). A/B switch.
 #ifndef LPM6_STATIC_TA
@@ -554,24 +540,6 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
     }
     return k;
   };
-  // Clamped key of query (tile, group lane s) for Phase B, loaded by every lane of the
-  // group (LPM6_GROUP_KEY_LOAD): 8 distinct 8-byte words per warp instruction.
-  constexpr bool kGroupLoad = LPM6_GROUP_KEY_LOAD != 0 && (INPUT == kInAddr || INPUT == kInKey);
-  auto load_group_key = [&](unsigned long long tile, int s) -> unsigned long long {
-    const unsigned long long qi = tile * 32ull + gbase + s;
-    unsigned long long k = 0;
-    if (qi < p.n) {
-      if constexpr (INPUT == kInKey)
-        k = ld_stream<unsigned long long>(p.keys + qi, pol_stream);
-      else
-        k = ld_stream<unsigned long long>(reinterpret_cast<const unsigned long long*>(p.addrs + qi) + 1, pol_stream);
-    }
-    return k > kMaxQueryKey ? kMaxQueryKey : k;  // types.hpp:25
-  };
-  // LPM6_KEY_SMEM: this warp's key slot; word L + (L >> 4) holds lane L's key, so the
-  // store and each group read (8 distinct words, one per group) are conflict-free.
-  const bool use_slot = LPM6_KEY_SMEM != 0 && !LEAFS && p.key_slot_off != 0;
-  const uint32_t wslot = s_base + p.key_slot_off + (threadIdx.x >> 5) * kKeySlotBytes;
   unsigned long long next_key[TILES];
 #pragma unroll
   for (int t = 0; t < TILES; ++t) next_key[t] = load_key(warp0, t);
@@ -601,14 +569,6 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
       key[t] = next_key[t] > kMaxQueryKey ? kMaxQueryKey : next_key[t];  // types.hpp:25
       node[t] = 0;
       next_key[t] = load_key(st + nwarps, t);  // prefetch; consumed next iteration
-    }
-
-    // LPM6_GROUP_KEY_LOAD 2: the first Phase B pass's group keys, requested before Phase A.
-    constexpr bool kGroupAhead = kGroupLoad && LPM6_GROUP_KEY_LOAD == 2 && (PBSEQ || TILES == 1);
-    unsigned long long gk[4] = {0, 0, 0, 0};
-    if constexpr (kGroupAhead) {
-#pragma unroll
-      for (int s = 0; s < 4; ++s) gk[s] = load_group_key(st * TILES, s);
     }
 
     // Phase A: this thread's own queries through the shared-memory levels.
@@ -721,40 +681,13 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
       // Phase B: the group's queries, one 128-byte line per query per level.
       unsigned long long qk[NSB];
       unsigned nd[NSB];
-      if (use_slot) {
-  #pragma unroll
-        for (int t = 0; t < PBT; ++t) {
-          __syncwarp();  // the previous tile's reads of the slot are done
-          asm volatile("st.shared.u64 [%0], %1;" ::"r"(wslot + (lane + (lane >> 4)) * 8u), "l"(kcur[t]) : "memory");
-          __syncwarp();
-  #pragma unroll
-          for (int s = 0; s < 4; ++s) {
-            asm volatile("ld.shared.u64 %0, [%1];"
-                         : "=l"(qk[4 * t + s])
-                         : "r"(wslot + (gbase + s + (lane >> 4)) * 8u)
-                         : "memory");
-            nd[4 * t + s] = __shfl_sync(kFull, ncur[t], s, 4);
-          }
-        }
-      } else
   #pragma unroll
       for (int t = 0; t < PBT; ++t)
   #pragma unroll
         for (int s = 0; s < 4; ++s) {
-          if constexpr (kGroupAhead)
-            qk[4 * t + s] = gk[s];
-          else if constexpr (kGroupLoad)
-            qk[4 * t + s] = load_group_key(st * TILES + tb0 + t, s);
-          else
-            qk[4 * t + s] = __shfl_sync(kFull, kcur[t], s, 4);
+          qk[4 * t + s] = __shfl_sync(kFull, kcur[t], s, 4);
           nd[4 * t + s] = __shfl_sync(kFull, ncur[t], s, 4);
         }
-      if constexpr (kGroupAhead && PBSEQ) {  // the next pass's group keys, consumed one pass later
-        if (pb + 1 < TILES) {
-  #pragma unroll
-          for (int s = 0; s < 4; ++s) gk[s] = load_group_key(st * TILES + pb + 1, s);
-        }
-      }
       unsigned long long w[NSB][4];
       // Internal L2 levels [TA, DEPTH): a runtime-count loop (one back-edge per
       // level instead of a compare-and-branch per possible level), then the leaf.

@@ -38,12 +38,7 @@ struct LookupParams {
   // in the shared-memory image: img_step[0] = off(1); img_step[l] = off(l+1) -
   // 16 off(l) for 1 <= l < smem_levels - 1; img_step[smem_levels - 1] = -16 off(l).
   unsigned int img_step[LPM6CU_MAX_LEVELS];
-  // LPM6_KEY_SMEM (A/B): byte offset in dynamic shared memory of the per-warp key slots
-  // (kKeySlotBytes each) Phase B's query keys are handed over through; 0 = shuffles.
-  unsigned int key_slot_off;
 };
-
-constexpr unsigned kKeySlotBytes = 264;  // 32 keys + one word of skew between the half-warps
 
 using KernelFn = void (*)(const LookupParams);
 

@@ -1,4 +1,4 @@
-# A/B: Phase B's query keys loaded by every lane of the group from the address stream
+# (code: commit 0d11088) A/B: Phase B's query keys loaded by every lane of the group from the address stream
 # (libGKL1: at the start of each pass; libGKL2: one pass ahead) vs broadcast by shuffles.
 cd $GRAFT_REPO_ROOT
 O=gpurun_out

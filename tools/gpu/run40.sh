@@ -1,4 +1,4 @@
-# A/B: Phase B's query keys through a per-warp shared-memory slot (libKSM: one STS.64 and
+# (code: commit 2c8c686) A/B: Phase B's query keys through a per-warp shared-memory slot (libKSM: one STS.64 and
 # four broadcast LDS.64 per lane and tile; node indices still shuffled) vs eight shuffles,
 # on the final PBSEQ kernels (C1's image leaves room for the 8.4 KB of key slots).
 cd $GRAFT_REPO_ROOT
