@@ -385,3 +385,41 @@ def test_first_commit_is_warm(lpm, cuda, st):
     store.close()
     assert times[0] <= 15.0, (times, builds)
     assert times[0] <= 3 * max(min(times[1:]), 2.0), (times, builds)
+
+
+def test_commit_then_replicate_snapshot(lpm, orc, cuda, st):
+    """Re-broadcast on commit: the committed snapshot's device FIB goes to
+    every visible GPU by lpm6cu_fib_replicate (one grouped NCCL broadcast); the replicas
+    hold the committed line array and answer with the new epoch's next hops."""
+    from paper_2604_14650_b200.gpu import device_lines
+    torch = cuda
+    rng = np.random.default_rng(11)
+    fib = lpm.workload_fib(0)
+    store = st.FibStore(fib)
+    devices = list(range(torch.cuda.device_count()))
+    view = fib
+    for epoch in (2, 3):
+        ops = random_ops(st, rng, view, 300)
+        store.stage(ops)
+        view, _, _ = st.apply_updates(view, ops)
+        assert store.commit() == epoch
+        addrs = probe_addrs(lpm, view, rng)
+        want = expected(lpm, orc, view, addrs)
+        with store.acquire() as snap:
+            assert snap.epoch == epoch
+            reps = snap.fib.replicate(devices)
+            try:
+                lines = device_lines(snap.fib)
+                for r, d in zip(reps, devices):
+                    assert r.geometry == snap.fib.geometry
+                    np.testing.assert_array_equal(device_lines(r), lines)
+                    with torch.cuda.device(d):
+                        a = torch.from_numpy(addrs.view(np.uint8).reshape(-1, 16)).to(f"cuda:{d}")
+                        out = r.lookup_batch(a)
+                        torch.cuda.synchronize(d)
+                    view_t = {1: np.uint8, 2: np.uint16, 4: np.uint32}[out.element_size()]
+                    np.testing.assert_array_equal(out.cpu().numpy().view(view_t).astype(np.uint32), want)
+            finally:
+                for r in reps:
+                    r.close()
+    store.close()
