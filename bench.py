@@ -49,7 +49,9 @@ def parse_args():
     ap.add_argument("--lanes", type=int, default=0, help="lanes per query (4/8/16), 0 = auto")
     ap.add_argument("--smem-levels", type=int, default=None, help="levels staged in smem, default auto")
     ap.add_argument("--ctas-per-sm", type=int, default=0)
-    ap.add_argument("--queries-per-lane", type=int, default=0, help="32-query tiles per warp iteration (1/2)")
+    ap.add_argument("--queries-per-lane", type=int, default=0, help="32-query tiles per warp iteration (1/2/4)")
+    ap.add_argument("--plane-levels", type=int, default=0,
+                    help="split-plane descent of staged levels 1..P-1 (with a fixed --line-path; the tuner picks its own)")
     ap.add_argument("--min-ctas", type=int, default=0, help="register cap: min CTAs/SM launch bound")
     ap.add_argument("--threads", type=int, default=0, help="threads per CTA (256/512/1024)")
     ap.add_argument("--queries", type=int, default=0, help="override queries per GPU (testing only)")
@@ -594,7 +596,8 @@ def choose_line_path(args, fdev, addrs, out, stream):
         fdev.set_kernel_config(lanes_per_query=c["lanes_per_query"], smem_levels=c["smem_levels"],
                                ctas_per_sm=c["ctas_per_sm"], threads_per_cta=c["threads_per_cta"],
                                queries_per_lane=c["queries_per_lane"], min_ctas_per_sm=c["min_ctas_per_sm"],
-                               line_path={"lsu": 0, "tex": 1, "split": 2, "tex-split": 3, "tex-select": 4}[args.line_path])
+                               line_path={"lsu": 0, "tex": 1, "split": 2, "tex-split": 3, "tex-select": 4}[args.line_path],
+                               plane_levels=args.plane_levels)
     cfg = fdev.kernel_config()
     cfg["line_path_choice"] = args.line_path
     return cfg
@@ -857,7 +860,7 @@ def main():
         fdev.set_kernel_config(lanes_per_query=args.lanes, smem_levels=args.smem_levels,
                                ctas_per_sm=args.ctas_per_sm, queries_per_lane=args.queries_per_lane,
                                min_ctas_per_sm=args.min_ctas, threads_per_cta=args.threads,
-                               line_path=cfg["line_path"])
+                               line_path=cfg["line_path"], plane_levels=cfg.get("plane_levels", 0))
 
     # -- other inputs and the update store (rank 0; extra keys, not the headline) ---------------------
     extras = None

@@ -130,6 +130,18 @@ typedef struct {
                                 LSU; 4 = as 1 with another extraction of 1-byte next hops (same as 1
                                 for wider ones). Pick it on representative traffic with
                                 lpm6cu_fib_tune_line_path. */
+  uint32_t plane_levels;     /* split-plane descent of the staged levels (2 or 4 tiles per warp on
+                                line paths 1 and 4; other plans ignore it): P >= 2 = levels 1 .. P - 1
+                                are staged as a plane of the nodes' high 32-bit words followed by a
+                                plane of their low words and probed with 4-byte loads (fewer
+                                shared-memory bank conflicts), a low word read only when a lane of
+                                the warp ties on a high word; deeper staged levels keep the packed
+                                8-byte keys. 0 (default) or 1 = packed everywhere. Kernels exist for
+                                P = 2, 3 and every staged level (P >= smem_levels, reported as
+                                smem_levels; other values run as 3), on trees of depth >= 3 with all
+                                or all but one internal level staged. Results are identical; the
+                                tuner picks P with the line path (levels whose high words tie often
+                                are better left packed). */
 } lpm6cu_kernel_config;
 
 typedef struct lpm6cu_fib lpm6cu_fib;

@@ -54,7 +54,7 @@ class BuildOpts_t(C.Structure):
 class KernelConfig_t(C.Structure):
     _fields_ = [("lanes_per_query", C.c_uint32), ("smem_levels", C.c_uint32), ("ctas_per_sm", C.c_uint32),
                 ("threads_per_cta", C.c_uint32), ("queries_per_lane", C.c_uint32), ("min_ctas_per_sm", C.c_uint32),
-                ("line_path", C.c_uint32)]
+                ("line_path", C.c_uint32), ("plane_levels", C.c_uint32)]
 
 
 class WorkloadInfo_t(C.Structure):

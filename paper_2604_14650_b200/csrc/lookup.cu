@@ -39,6 +39,30 @@ __global__ void lpm6_querygen_kernel(const QuerySpec spec, unsigned long long fi
   }
 }
 
+// The staged image re-laid out for the split-plane Phase A (lookup_kernel.cuh PLANES):
+// levels below `pu` as a plane of high words followed by a plane of low words, the
+// others word for word. lvl_w[l] = first image word of level l (lvl_w[levels] = the end).
+struct PlaneLevels {
+  unsigned lvl_w[LPM6CU_MAX_LEVELS + 1];
+  unsigned levels, pu;
+};
+__global__ void lpm6_planes_kernel(const unsigned long long* image, unsigned* out, const PlaneLevels pl) {
+  const unsigned total = pl.lvl_w[pl.levels];
+  for (unsigned w = blockIdx.x * blockDim.x + threadIdx.x; w < total; w += gridDim.x * blockDim.x) {
+    unsigned l = 0;
+    while (l + 1 < pl.levels && w >= pl.lvl_w[l + 1]) ++l;
+    const unsigned long long k = image[w];
+    if (l < pl.pu) {
+      const unsigned w0 = pl.lvl_w[l], nw = pl.lvl_w[l + 1] - w0;
+      out[2 * w0 + (w - w0)] = static_cast<unsigned>(k >> 32);
+      out[2 * w0 + nw + (w - w0)] = static_cast<unsigned>(k);
+    } else {
+      out[2 * w] = static_cast<unsigned>(k);
+      out[2 * w + 1] = static_cast<unsigned>(k >> 32);
+    }
+  }
+}
+
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {
@@ -93,6 +117,8 @@ struct lpm6cu_fib {
   cudaStream_t zc_stream = nullptr;  // zero-copy host path (small pinned batches)
   cudaEvent_t zc_event = nullptr;
   bool root_ready = false;
+  unsigned* d_planes = nullptr;  // the staged image as split planes (cfg.plane_levels >= 2), from fib_line_pool
+  unsigned planes_pu = 0;        // the plane_levels d_planes was laid out for
 
   void invalidate_plans() {
     std::lock_guard<std::mutex> lk(plan_mu);
@@ -126,6 +152,10 @@ struct lpm6cu_fib {
       }
     }
     if (d_err) cudaFree(d_err);
+    if (d_planes) {
+      if (!quiesced) cudaDeviceSynchronize();
+      cudaFreeAsync(d_planes, nullptr);
+    }
     if (prev >= 0) cudaSetDevice(prev);
   }
 };
@@ -161,6 +191,30 @@ unsigned long long image_bytes_of(const lpm6cu_geometry& g, unsigned levels) {
 // Shape of the default kernel (the only one with the leaf-image variant).
 bool default_shape(const lpm6cu_kernel_config& c) {
   return c.queries_per_lane == 1 && c.threads_per_cta == 1024 && c.min_ctas_per_sm == 1;
+}
+
+// (Re)build the plane image for f->cfg.plane_levels (a no-op when it is current or not
+// asked for). Synchronous: the tuning / configuration calls are not on the lookup path.
+void ensure_planes(lpm6cu_fib* f) {
+  const unsigned pu = f->cfg.plane_levels;
+  if (pu < 2 || !f->d_lines || (f->d_planes && f->planes_pu == pu)) return;
+  const unsigned levels = std::min<unsigned>(f->g.image_levels, f->g.depth);
+  PlaneLevels pl{};
+  pl.levels = levels;
+  pl.pu = pu;
+  for (unsigned l = 0; l <= levels; ++l)
+    pl.lvl_w[l] = static_cast<unsigned>(f->g.level_start[l] / kLineWords * kNodeKeys);
+  const size_t bytes = static_cast<size_t>(pl.lvl_w[levels]) * 8;
+  if (bytes == 0) return;
+  DeviceGuard dg(f->device);
+  if (!f->d_planes)
+    check_cuda(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&f->d_planes), (bytes + 15) / 16 * 16,
+                                       capi::fib_line_pool(f->device), nullptr),
+               "cudaMallocFromPoolAsync planes");
+  lpm6_planes_kernel<<<32, 256>>>(f->d_lines + f->g.image_start, f->d_planes, pl);
+  check_cuda(cudaGetLastError(), "planes launch");
+  check_cuda(cudaStreamSynchronize(nullptr), "planes sync");
+  f->planes_pu = pu;
 }
 
 // Resolve automatic kernel settings against the device and the tree.
@@ -209,8 +263,15 @@ void resolve_config(lpm6cu_fib* f, const lpm6cu_kernel_config* req) {
   if (staged > budget)
     throw Error(Errc::InvalidArgument, "smem_levels=" + std::to_string(c.smem_levels) + " needs " +
                                            std::to_string(staged) + " B of shared memory");
+  // Split-plane Phase A: levels 1 .. plane_levels - 1; 0 or 1 = none, clamped to the staged levels.
+  if (c.plane_levels > LPM6CU_MAX_LEVELS) throw Error(Errc::InvalidArgument, "plane_levels above the level count");
+  // The kernels exist for P = 2, 3 and every staged level (reported as smem_levels).
+  if (c.plane_levels < 2 || c.smem_levels < 2 || c.smem_levels > depth) c.plane_levels = 0;
+  if (c.plane_levels >= c.smem_levels) c.plane_levels = c.smem_levels;
+  else if (c.plane_levels > 3) c.plane_levels = 3;
   f->cfg = c;
   f->invalidate_plans();
+  ensure_planes(f);
 }
 
 bool leaf_image_mode(const lpm6cu_fib* f) { return f->cfg.smem_levels > f->g.depth; }
@@ -276,6 +337,13 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
                              : tiles_cfg;
   const size_t smem = image_bytes_of(f->g, smem_levels);
   const int threads = static_cast<int>(threads_cta);
+  // Split-plane Phase A: the 2- and 4-tile kernels of the texture leaf paths, when the
+  // plane image is laid out for the configured level count.
+  const bool planes_on = tiles > 1 && threads_cta == 1024 && f->cfg.plane_levels >= 2 && f->d_planes != nullptr &&
+                         f->planes_pu == f->cfg.plane_levels && smem_levels >= 2 && f->g.depth >= 3 &&
+                         (smem_levels == f->g.depth || smem_levels + 1 == f->g.depth);
+  const unsigned pu = std::min<unsigned>(f->cfg.plane_levels, smem_levels);
+  const int planes = !planes_on ? 0 : pu >= smem_levels ? kAllPlanes : pu >= 3 ? 3 : 2;
   LaunchPlan plan;
   {
     auto* mf = const_cast<lpm6cu_fib*>(f);
@@ -285,7 +353,7 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
       KernelFn fn = pick_kernel(static_cast<int>(f->g.value_bytes), static_cast<int>(f->g.depth),
                                 static_cast<int>(tiles), threads, static_cast<int>(minb), f->d_err != nullptr, input,
                                 leafs, texl_mode, leaftex, f->g.leaf_words == kHalfLeafWords,
-                                static_cast<int>(std::min<unsigned>(smem_levels, f->g.depth)));
+                                static_cast<int>(std::min<unsigned>(smem_levels, f->g.depth)), planes);
       if (!fn) throw Error(Errc::InvalidArgument, "no kernel instantiated for this configuration");
       // The attribute belongs to the kernel, which every FIB of this depth and
       // next-hop width shares: always set it to the device's opt-in maximum, never
@@ -324,6 +392,13 @@ void launch_lookup(const lpm6cu_fib* f, const void* d_in, unsigned long long n, 
   p.smem_levels = std::min<unsigned>(smem_levels, f->g.depth);
   p.leaf_image_off = static_cast<unsigned>(image_bytes_of(f->g, f->g.depth) / 8);
   p.image = f->d_lines + f->g.image_start;
+  if (planes) {
+    auto offb = [&](unsigned l) { return static_cast<unsigned>((f->g.level_start[l] / kLineWords) * kNodeKeys * 8); };
+    p.image = reinterpret_cast<const unsigned long long*>(f->d_planes);
+    for (unsigned l = 0; l < smem_levels; ++l)
+      p.lo_delta[l] = static_cast<unsigned>((f->g.level_start[l + 1] - f->g.level_start[l]) / kLineWords * kNodeKeys * 4);
+    if (pu < smem_levels) p.pl2pk = offb(pu) - 32u * offb(pu - 1);
+  }
   for (int l = 0; l < LPM6CU_MAX_LEVELS; ++l) p.level_nodes[l] = f->g.level_nodes[l];
   p.err = f->d_err;
   std::memcpy(p.root, f->root, sizeof p.root);
@@ -649,6 +724,7 @@ int lpm6cu_fib_tune_line_path(lpm6cu_fib* f, const void* d_addrs, uint64_t n, vo
       throw Error(Errc::InvalidArgument, "addresses must be 16-byte aligned");
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     lpm6cu_kernel_config c = f->cfg;
+    c.plane_levels = 0;  // the line paths and tile counts are timed on the packed image first
     const bool possible = f->tex && f->d_err == nullptr && !leaf_image_mode(f) && f->g.depth >= 1 &&
                           c.threads_per_cta == 1024 && c.min_ctas_per_sm == 1 &&
                           (c.queries_per_lane == 1 || c.queries_per_lane == 2 || c.queries_per_lane == 4);
@@ -696,19 +772,73 @@ int lpm6cu_fib_tune_line_path(lpm6cu_fib* f, const void* d_addrs, uint64_t n, vo
         f->invalidate_plans();
         throw;
       }
-      cudaEventDestroy(ev[0]);
-      cudaEventDestroy(ev[1]);
       for (unsigned path = 0; path < 5; ++path)
         for (unsigned ti = 0; ti < 3; ++ti)
           if (plan_applies(f, path) && tiles_apply(path, ti) && ms[path][ti] < ms[best][best_ti]) {
             best = path;
             best_ti = ti;
           }
+      // Split-plane Phase A: on each texture leaf path (1 and 4) with 2 and 4 tiles, plane
+      // levels P = 2, 3 and every staged level; the fastest of all — packed or
+      // planes — is kept (planes only when at least 0.5 % faster than the best packed plan).
+      unsigned best_pu = 0;
+      const unsigned ta = std::min<unsigned>(c.smem_levels, f->g.depth);
+      if (f->g.depth >= 3 && ta >= 2 && (ta == f->g.depth || ta + 1 == f->g.depth)) {
+        float best_ms = ms[best][best_ti] * 0.995f;
+        unsigned cand[3] = {2u, 3u, ta};
+        try {
+          const unsigned r = reps ? reps : 3;
+          for (unsigned path = 1; path <= 4; path += 3) {
+            if (!plan_applies(f, path)) continue;
+            for (unsigned ti = 1; ti < 3; ++ti)  // 2 and 4 tiles
+            for (unsigned k = 0; k < 3; ++k) {
+              c.line_path = path;
+              c.queries_per_lane = kTiles[ti];
+              const unsigned pu = cand[k];
+              if (pu > ta || (k < 2 && pu == ta)) continue;  // 2 and 3 only below the staged levels
+              c.plane_levels = pu;
+              f->cfg = c;
+              f->invalidate_plans();
+              ensure_planes(f);
+              float tmin = 0.f;
+              for (unsigned round = 0; round < 2; ++round) {
+                launch_lookup(f, d_addrs, n, d_out, st);
+                check_cuda(cudaEventRecord(ev[0], st), "cudaEventRecord");
+                for (unsigned i = 0; i < r; ++i) launch_lookup(f, d_addrs, n, d_out, st);
+                check_cuda(cudaEventRecord(ev[1], st), "cudaEventRecord");
+                check_cuda(cudaEventSynchronize(ev[1]), "cudaEventSynchronize");
+                float t = 0.f;
+                check_cuda(cudaEventElapsedTime(&t, ev[0], ev[1]), "cudaEventElapsedTime");
+                tmin = round == 0 ? t : std::min(tmin, t);
+              }
+              if (tmin < best_ms) {
+                best_ms = tmin;
+                best_pu = pu;
+                best = path;
+                best_ti = ti;
+              }
+            }
+          }
+        } catch (...) {
+          cudaEventDestroy(ev[0]);
+          cudaEventDestroy(ev[1]);
+          c.line_path = 0;
+          c.queries_per_lane = 1;
+          c.plane_levels = 0;
+          f->cfg = c;
+          f->invalidate_plans();
+          throw;
+        }
+      }
+      c.plane_levels = best_pu;
+      cudaEventDestroy(ev[0]);
+      cudaEventDestroy(ev[1]);
     }
     c.line_path = best;
     if (possible) c.queries_per_lane = kTiles[best_ti];
     f->cfg = c;
     f->invalidate_plans();
+    ensure_planes(f);
     if (line_path) *line_path = best;
   });
 }

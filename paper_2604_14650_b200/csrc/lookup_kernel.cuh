@@ -30,6 +30,12 @@
 // then takes one tile at a time, so the registers holding line quarters stay those of
 // one tile.
 //
+// PLANES (chosen by the tuner with the line path, lpm6cu_kernel_config.plane_levels): the
+// upper staged levels are stored as split planes — a node's 15 high words, then its 15
+// low words — and probed with one LDS.32 of the high word (32 banks instead of 16 bank
+// pairs: fewer random bank conflicts); the low word is read only when some lane of the
+// warp ties on the high word, a warp-uniform branch shared by the warp's tiles.
+//
 // Query addresses are read with coalesced loads of the top word (L1::no_allocate,
 // L2 evict_first), one tile ahead of their use; tree lines use evict_last. CTAs
 // are persistent (grid = SMs x resident CTAs, default one 1024-thread CTA per
@@ -492,12 +498,17 @@ __device__ __forceinline__ unsigned leaf_search_smem(const unsigned long long* l
 // traffic the texture path's miss throughput is lower (C1 -27 % with 1, +1.2 %
 // with 2), so the host picks the line path by measurement
 // (lpm6cu_fib_tune_line_path).
+// PLANES (0 = none; 2, 3 or kAllPlanes): split-plane Phase A. With P = PLANES, staged levels 1 .. P - 1 are
+// probed in the plane format (4-byte high words, 60 bytes per node; a low word only on a
+// tie) and levels P .. TA - 1 in the packed format; the walk's child step between two
+// plane levels is the packed one (the strides scale alike), from a plane level to a
+// packed one it is 2 a + 30 a' + (off(P) - 32 off(P - 1)) (LookupParams::pl2pk).
 // TAS > 0: the number of staged levels is a compile-time constant (= p.smem_levels),
 // so Phase A's level loop and Phase B's internal-level loop have no runtime level
 // checks (the texture line paths are instantiated for TAS = DEPTH and DEPTH - 1, the
 // staging every BASELINE FIB uses; TAS = 0 reads the count from the launch).
 template <int DEPTH, int VB, int TILES, int THREADS, int MINB, bool CHECKED, int INPUT = kInAddr, bool LEAFS = false,
-          int TEXL = 0, int LEAFTEX = 0, bool HALF = false, int TAS = 0, bool PBSEQ = false>
+          int TEXL = 0, int LEAFTEX = 0, bool HALF = false, int TAS = 0, bool PBSEQ = false, int PLANES = 0>
 __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const LookupParams p) {
   using F = LeafFmt<VB>;
   // Texture leaf fetches as sector-disjoint halves (tex_line_at) for 1-byte next
@@ -572,7 +583,75 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
     }
 
     // Phase A: this thread's own queries through the shared-memory levels.
-    if constexpr (!CHECKED && LPM6_PHASEA_WALK) {
+    if constexpr (PLANES != 0 && !CHECKED && !LEAFS) {
+      constexpr unsigned PU = PLANES;
+      uint32_t a[TILES];
+      unsigned qh[TILES], ql[TILES];
+#pragma unroll
+      for (int t = 0; t < TILES; ++t) {
+        const unsigned c = root_rank(p, key[t]);
+        a[t] = s_base + p.img_step[0] + c * 60u;
+        qh[t] = static_cast<unsigned>(key[t] >> 32);
+        ql[t] = static_cast<unsigned>(key[t]);
+      }
+      auto lds32 = [](uint32_t addr) {
+        unsigned v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+        return v;
+      };
+      // One probe of every tile: high words first; low words only if a lane of the warp ties.
+      auto probe = [&](uint32_t off, uint32_t step, uint32_t lod) {
+        unsigned h[TILES];
+        bool gt[TILES], eq[TILES];
+        bool anyeq = false;
+#pragma unroll
+        for (int t = 0; t < TILES; ++t) h[t] = lds32(a[t] + off);
+#pragma unroll
+        for (int t = 0; t < TILES; ++t) {
+          gt[t] = qh[t] > h[t];
+          eq[t] = qh[t] == h[t];
+          anyeq |= eq[t];
+        }
+        if (__any_sync(kFull, anyeq)) {
+#pragma unroll
+          for (int t = 0; t < TILES; ++t)
+            if (eq[t]) gt[t] = ql[t] >= lds32(a[t] + off + lod);
+        }
+#pragma unroll
+        for (int t = 0; t < TILES; ++t) a[t] += gt[t] ? step : 0u;
+      };
+#pragma unroll
+      for (int l = 1; l < DEPTH; ++l) {
+        if (static_cast<unsigned>(l) >= TA) break;
+        if (static_cast<unsigned>(l) < PU) {
+          uint32_t a0[TILES];
+#pragma unroll
+          for (int t = 0; t < TILES; ++t) a0[t] = a[t];
+          const uint32_t lod = p.lo_delta[l];
+          probe(28u, 32u, lod);
+          probe(12u, 16u, lod);
+          probe(4u, 8u, lod);
+          probe(0u, 4u, lod);
+          if (static_cast<unsigned>(l + 1) == PU && static_cast<unsigned>(l + 1) < TA) {  // next level packed
+#pragma unroll
+            for (int t = 0; t < TILES; ++t) a[t] = 2u * a0[t] + 30u * a[t] + (p.pl2pk - 31u * s_base);
+          } else {
+#pragma unroll
+            for (int t = 0; t < TILES; ++t) a[t] = a0[t] + 15u * a[t] + (p.img_step[l] - 15u * s_base);
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < TILES; ++t) {
+            const uint32_t af = a[t] + node_rank_saddr(a[t], key[t]);
+            a[t] = a[t] + 15u * af + (p.img_step[l] - 15u * s_base);
+          }
+        }
+      }
+      // a - s_base = 60 x node after a plane level, 120 x node after a packed one
+      const unsigned sh = TA > PU ? 3u : 2u;
+#pragma unroll
+      for (int t = 0; t < TILES; ++t) node[t] = ((a[t] - s_base) >> sh) * 0xEEEEEEEFu;
+    } else if constexpr (!CHECKED && LPM6_PHASEA_WALK) {
       // As a walk over shared-memory byte addresses: with a = the address of node
       // n of level l and a' = a + 8 * rank after the four probes, the child's
       // address in level l + 1 is img(l+1) + (16 n + rank) * 120 =
@@ -877,28 +956,43 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
 // constant when it is DEPTH or DEPTH - 1 (TAS), else read from the launch.
 // TL = 2: two tiles per warp iteration through Phase A, Phase B one tile at a time
 // (PBSEQ; 1024 threads, texture line paths, address input).
-template <int D, int VB, int INPUT, int TEXL, int LEAFTEX, bool HALF, int TL = 1>
+template <int D, int VB, int INPUT, int TEXL, int LEAFTEX, bool HALF, int TL = 1, int PLN = 0>
 KernelFn pick_ta(int ta) {
   constexpr bool SEQ = TL > 1;
-  if constexpr (LPM6_STATIC_TA != 0) {
-    if (ta == D) return lpm6_lookup_kernel<D, VB, TL, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF, D, SEQ>;
-    if constexpr (D >= 2)
-      if (ta == D - 1)
-        return lpm6_lookup_kernel<D, VB, TL, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF, D - 1, SEQ>;
+  if constexpr (PLN != 0) {
+    // split-plane Phase A: trees of depth >= 3 with every internal level staged (then no
+    // internal level is read from L2: TEXL 0) or all but the last (read through the
+    // texture pipe: TEXL 1) — the stagings and pipes the 2- and 4-tile plans use
+    if constexpr (D >= 3) {
+      if constexpr (TEXL == 0) {
+        if (ta == D) return lpm6_lookup_kernel<D, VB, TL, 1024, 1, false, INPUT, false, 0, LEAFTEX, HALF, D, SEQ, PLN>;
+      } else {
+        if (ta == D - 1)
+          return lpm6_lookup_kernel<D, VB, TL, 1024, 1, false, INPUT, false, 1, LEAFTEX, HALF, D - 1, SEQ, PLN>;
+      }
+    }
+    return nullptr;
+  } else {
+    if constexpr (LPM6_STATIC_TA != 0) {
+      if (ta == D) return lpm6_lookup_kernel<D, VB, TL, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF, D, SEQ>;
+      if constexpr (D >= 2)
+        if (ta == D - 1)
+          return lpm6_lookup_kernel<D, VB, TL, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF, D - 1, SEQ>;
+    }
+    return lpm6_lookup_kernel<D, VB, TL, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF, 0, SEQ>;
   }
-  return lpm6_lookup_kernel<D, VB, TL, 1024, 1, false, INPUT, false, TEXL, LEAFTEX, HALF, 0, SEQ>;
 }
 
-template <int VB, int INPUT, int TEXL, int LEAFTEX, bool HALF, int TL = 1>
+template <int VB, int INPUT, int TEXL, int LEAFTEX, bool HALF, int TL = 1, int PLN = 0>
 KernelFn pick_depth_texl(int depth, int ta = 0) {
   switch (depth) {
-    case 1: return pick_ta<1, VB, INPUT, TEXL, LEAFTEX, HALF, TL>(ta);
-    case 2: return pick_ta<2, VB, INPUT, TEXL, LEAFTEX, HALF, TL>(ta);
-    case 3: return pick_ta<3, VB, INPUT, TEXL, LEAFTEX, HALF, TL>(ta);
-    case 4: return pick_ta<4, VB, INPUT, TEXL, LEAFTEX, HALF, TL>(ta);
-    case 5: return pick_ta<5, VB, INPUT, TEXL, LEAFTEX, HALF, TL>(ta);
-    case 6: return pick_ta<6, VB, INPUT, TEXL, LEAFTEX, HALF, TL>(ta);
-    case 7: return pick_ta<7, VB, INPUT, TEXL, LEAFTEX, HALF, TL>(ta);
+    case 1: return pick_ta<1, VB, INPUT, TEXL, LEAFTEX, HALF, TL, PLN>(ta);
+    case 2: return pick_ta<2, VB, INPUT, TEXL, LEAFTEX, HALF, TL, PLN>(ta);
+    case 3: return pick_ta<3, VB, INPUT, TEXL, LEAFTEX, HALF, TL, PLN>(ta);
+    case 4: return pick_ta<4, VB, INPUT, TEXL, LEAFTEX, HALF, TL, PLN>(ta);
+    case 5: return pick_ta<5, VB, INPUT, TEXL, LEAFTEX, HALF, TL, PLN>(ta);
+    case 6: return pick_ta<6, VB, INPUT, TEXL, LEAFTEX, HALF, TL, PLN>(ta);
+    case 7: return pick_ta<7, VB, INPUT, TEXL, LEAFTEX, HALF, TL, PLN>(ta);
     default: return nullptr;
   }
 }
@@ -947,6 +1041,30 @@ KernelFn pick_depth(int depth) {
   }
 }
 
+// Split-plane kernels (PLANES = a.planes: 2, 3 or kAllPlanes): 2 or 4 tiles per warp, texture
+// leaves (modes 1 and 3), address input.
+template <int VB, bool HALF, int LT, int TL, int PLN>
+KernelFn pick_planes_texl(const PickArgs& a) {
+  return a.texl ? pick_depth_texl<VB, kInAddr, 1, LT, HALF, TL, PLN>(a.depth, a.ta)
+                : pick_depth_texl<VB, kInAddr, 0, LT, HALF, TL, PLN>(a.depth, a.ta);
+}
+template <int VB, bool HALF, int LT, int TL>
+KernelFn pick_planes_pu(const PickArgs& a) {
+  switch (a.planes) {
+    case 2: return pick_planes_texl<VB, HALF, LT, TL, 2>(a);
+    case 3: return pick_planes_texl<VB, HALF, LT, TL, 3>(a);
+    case kAllPlanes: return pick_planes_texl<VB, HALF, LT, TL, kAllPlanes>(a);
+    default: return nullptr;
+  }
+}
+template <int VB, bool HALF>
+KernelFn pick_planes(const PickArgs& a) {
+  if (a.leaftex == 1) return a.tiles == 4 ? pick_planes_pu<VB, HALF, 1, 4>(a) : pick_planes_pu<VB, HALF, 1, 2>(a);
+  if constexpr (VB == 1 && !HALF)
+    if (a.leaftex == 3) return a.tiles == 4 ? pick_planes_pu<VB, HALF, 3, 4>(a) : pick_planes_pu<VB, HALF, 3, 2>(a);
+  return nullptr;
+}
+
 // The kernels of one leaf format. HALF (half-line leaves, 2-byte next hops only) is
 // instantiated for the default shape: every input format, checked and unchecked,
 // every line path; the other shapes exist for full leaf lines.
@@ -958,6 +1076,7 @@ KernelFn pick_kernel_fmt(const PickArgs& a) {
     // 2 or 4 tiles per warp through Phase A, Phase B one tile at a time (PBSEQ):
     // address input, texture leaves (modes 1 and 3), internal L2 levels on one pipe
     if (a.leafs || a.checked || a.input != kInAddr || a.texl > 1) return nullptr;
+    if (a.planes) return pick_planes<VB, HALF>(a);  // split-plane Phase A: the same shapes
     if (a.leaftex == 1)
       return a.tiles == 4 ? (a.texl ? pick_depth_texl<VB, kInAddr, 1, 1, HALF, 4>(depth, a.ta)
                                     : pick_depth_texl<VB, kInAddr, 0, 1, HALF, 4>(depth, a.ta))
@@ -971,6 +1090,7 @@ KernelFn pick_kernel_fmt(const PickArgs& a) {
                                       : pick_depth_texl<VB, kInAddr, 0, 3, HALF, 2>(depth, a.ta));
     return nullptr;
   }
+  if (a.planes) return nullptr;  // split planes exist for 2 or 4 tiles per warp on the texture leaf paths only
   if (a.leaftex) {  // default shape, unchecked, no leaf image, depth >= 1
     if (a.leafs || a.checked || !dflt) return nullptr;
     switch (a.input) {

@@ -13,6 +13,7 @@ namespace lpm6::kern {
 enum : int { kInAddr = 0, kInKey = 1, kInPacket = 2, kInKeyOrd = 3 };  // kInKeyOrd: keys in, ordinals out too
 
 constexpr int kMaxKernelDepth = 7;
+constexpr int kAllPlanes = 8;  // PLANES value: every staged level below the root as planes
 
 struct LookupParams {
   const unsigned long long* lines;                     // the tree, 16 u64 words per line
@@ -38,6 +39,11 @@ struct LookupParams {
   // in the shared-memory image: img_step[0] = off(1); img_step[l] = off(l+1) -
   // 16 off(l) for 1 <= l < smem_levels - 1; img_step[smem_levels - 1] = -16 off(l).
   unsigned int img_step[LPM6CU_MAX_LEVELS];
+  // Split-plane Phase A (PLANES kernels; lpm6cu_kernel_config.plane_levels): the plane
+  // levels are stored as their nodes' high words (15 u32 per node) followed, lo_delta[l]
+  // bytes further, by their low words; deeper staged levels stay packed.
+  unsigned int lo_delta[LPM6CU_MAX_LEVELS];
+  unsigned int pl2pk;  // off(P) - 32 off(P - 1): the walk's step from the last plane level to a packed one
 };
 
 using KernelFn = void (*)(const LookupParams);
@@ -53,6 +59,7 @@ struct PickArgs {
   int texl = 0, leaftex = 0;
   bool half = false;  // half-line leaves (layout.hpp kHalfLeafWords; 2-byte next hops)
   int ta = 0;         // staged levels (smem_levels) of the launch: compile-time in the texture line-path kernels
+  int planes = 0;  // split-plane Phase A (2 or 4 tiles per warp on the texture leaf paths): 0, 2, 3 or kAllPlanes
 };
 
 KernelFn pick_kernel_vb1(const PickArgs& a);  // lookup_vb1.cu
@@ -62,7 +69,7 @@ KernelFn pick_kernel_vb4(const PickArgs& a);  // lookup_vb4.cu
 // nullptr when that combination is not instantiated.
 inline KernelFn pick_kernel(int vb, int depth, int tiles, int threads, int minb, bool checked = false,
                             int input = kInAddr, bool leafs = false, int texl = 0, int leaftex = 0,
-                            bool half = false, int ta = 0) {
+                            bool half = false, int ta = 0, int planes = 0) {
   PickArgs a;
   a.depth = depth;
   a.tiles = tiles;
@@ -75,6 +82,7 @@ inline KernelFn pick_kernel(int vb, int depth, int tiles, int threads, int minb,
   a.leaftex = leaftex;
   a.half = half;
   a.ta = ta;
+  a.planes = planes;
   switch (vb) {
     case 1: return pick_kernel_vb1(a);
     case 2: return pick_kernel_vb2(a);

@@ -163,13 +163,14 @@ class Fib:
         return {"lanes_per_query": c.lanes_per_query, "smem_levels": c.smem_levels,
                 "ctas_per_sm": c.ctas_per_sm, "threads_per_cta": c.threads_per_cta,
                 "queries_per_lane": c.queries_per_lane, "min_ctas_per_sm": c.min_ctas_per_sm,
-                "line_path": c.line_path}
+                "line_path": c.line_path, "plane_levels": c.plane_levels}
 
     def set_kernel_config(self, lanes_per_query: int = 0, smem_levels: int | None = None,
                           ctas_per_sm: int = 0, threads_per_cta: int = 0, queries_per_lane: int = 0,
-                          min_ctas_per_sm: int = 0, line_path: int = 0) -> dict:
+                          min_ctas_per_sm: int = 0, line_path: int = 0, plane_levels: int = 0) -> dict:
         c = KernelConfig_t()
         c.line_path = line_path
+        c.plane_levels = plane_levels
         c.lanes_per_query = lanes_per_query
         c.smem_levels = 0xFF if smem_levels is None else smem_levels
         c.ctas_per_sm = ctas_per_sm

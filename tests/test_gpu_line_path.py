@@ -1,6 +1,7 @@
 """Line paths (lpm6cu_kernel_config.line_path: which L1TEX pipe carries the leaf
 and internal L2 lines), the tiles per warp of the texture leaf paths
-(queries_per_lane 1, 2 or 4 at 1024 threads) and the measured choice between them
+(queries_per_lane 1, 2 or 4 at 1024 threads), the split-plane descent of the staged
+levels (plane_levels) and the measured choice between them
 (lpm6cu_fib_tune_line_path).
 
 A line path changes only how a line reaches registers, so every answer must
@@ -62,6 +63,25 @@ def test_texture_line_path_matches_oracle_on_workloads(lpm, orc, cuda, workload)
                                           err_msg=f"keys qpl={qpl} lp={lp}")
 
 
+    # split-plane descent of the staged levels (plane_levels P: levels 1 .. P - 1 as high /
+    # low word planes, the rest packed), every P, on the shapes that run it and on those
+    # that ignore it; smem_levels one below the depth as well (C2's other static staging)
+    depth = dev.geometry.depth
+    for t in (None, depth - 1):
+        for pu in range(2, depth + 2):
+            for qpl, lp in ((2, 1), (4, 1), (2, 4), (4, 4), (1, 1), (2, 2)):
+                cfg = dev.set_kernel_config(smem_levels=t, line_path=lp, threads_per_cta=1024, queries_per_lane=qpl,
+                                            plane_levels=pu)
+                # kernels exist for P = 2, 3 and every staged level (reported as smem_levels)
+                assert cfg["plane_levels"] == (cfg["smem_levels"] if pu >= cfg["smem_levels"] else min(pu, 3))
+                m = len(da) - 77
+                got = dev.lookup_batch(da[:m])
+                torch.cuda.synchronize()
+                np.testing.assert_array_equal(got.cpu().numpy().view(view).astype(np.uint32), want[:m],
+                                              err_msg=f"planes {pu} smem_levels {t} qpl={qpl} lp={lp}")
+    assert dev.set_kernel_config(plane_levels=1)["plane_levels"] == 0  # no plane level: packed
+
+
 def test_tuner_picks_a_path_and_keeps_results(lpm, orc, cuda):
     torch = cuda
     for workload in ("C1", "C2", "C3b"):
@@ -79,6 +99,8 @@ def test_tuner_picks_a_path_and_keeps_results(lpm, orc, cuda):
         assert cfg["line_path"] == chosen
         # the tuner also picks the tiles per warp: 2 or 4 only on the texture leaf paths
         assert cfg["queries_per_lane"] in ((1, 2, 4) if chosen in (1, 4) else (1,))
+        # ... and the plane levels of the split-plane descent, only with 2 or 4 tiles
+        assert cfg["plane_levels"] == 0 or (cfg["queries_per_lane"] > 1 and 2 <= cfg["plane_levels"] <= cfg["smem_levels"])
         again = dev.lookup_batch(d)
         torch.cuda.synchronize()
         assert torch.equal(base, again)

@@ -41,15 +41,18 @@ def test_random_fibs_every_mode(lpm, orc, cuda):
         for t in [None] + list(range(g.depth + g.leaf_image + 1)):
             # line paths (which L1TEX pipe carries the L2 lines) x tiles per warp (2 and 4
             # exist on the texture leaf paths 1 and 4)
-            for lp, qpl in ((0, 1), (1, 1), (2, 1), (3, 1), (4, 1), (1, 2), (1, 4), (4, 2), (4, 4)):
-                dev.set_kernel_config(smem_levels=t, line_path=lp, threads_per_cta=1024, queries_per_lane=qpl)
+            # ... x split-plane descent (plane_levels; runs on the 2- and 4-tile kernels)
+            for lp, qpl, pu in ((0, 1, 0), (1, 1, 0), (2, 1, 0), (3, 1, 0), (4, 1, 0), (1, 2, 0), (1, 4, 0), (4, 2, 0),
+                                (4, 4, 0), (1, 2, 2), (1, 4, 3), (4, 2, 8), (1, 4, 8), (4, 4, 2), (1, 1, 3)):
+                dev.set_kernel_config(smem_levels=t, line_path=lp, threads_per_cta=1024, queries_per_lane=qpl,
+                                      plane_levels=pu)
                 for checked in (False, True):
                     dev.set_checked(checked)
                     for mode, got in (("addr", dev.lookup_batch(da)), ("keys", dev.lookup_keys(dk)),
                                       ("search", dev.search_batch(dk)[1])):
                         torch.cuda.synchronize()
                         if not np.array_equal(got.cpu().numpy().view(view).astype(np.uint32), want):
-                            failures.append((it, n, t, lp, qpl, checked, mode, g.depth, g.value_bytes))
+                            failures.append((it, n, t, lp, qpl, pu, checked, mode, g.depth, g.value_bytes))
                     if checked and dev.violations():
                         failures.append((it, "violations"))
         dev.set_checked(False)
