@@ -15,16 +15,20 @@ OBJ = ROOT / "build" / "obj"
 #  LEAFTEX, HALF, TAS, PBSEQ>)
 KERNELS = [
     ("C2/C4 bench kernel: line path 1, half-line leaves, 4 tiles per warp, PBSEQ (depth 5, u16)", "lookup_vb2.cu.o",
-     "ILi5ELi2ELi4ELi1024ELi1ELb0ELi0ELb0ELi1ELi1ELb1ELi4ELb1EE"),
+     "ILi5ELi2ELi4ELi1024ELi1ELb0ELi0ELb0ELi1ELi1ELb1ELi4ELb1ELi0EE"),
     ("C2/C4 one tile per warp, line path 1, half-line leaves", "lookup_vb2.cu.o",
-     "ILi5ELi2ELi1ELi1024ELi1ELb0ELi0ELb0ELi1ELi1ELb1ELi4ELb0EE"),
-    ("C1/C3b bench kernel: line path 1, 2 tiles per warp, PBSEQ (depth 4, u8)", "lookup_vb1.cu.o",
-     "ILi4ELi1ELi2ELi1024ELi1ELb0ELi0ELb0ELi0ELi1ELb0ELi4ELb1EE"),
+     "ILi5ELi2ELi1ELi1024ELi1ELb0ELi0ELb0ELi1ELi1ELb1ELi4ELb0ELi0EE"),
+    ("C1/C3b packed kernel: line path 1, 2 tiles per warp, PBSEQ (depth 4, u8)", "lookup_vb1.cu.o",
+     "ILi4ELi1ELi2ELi1024ELi1ELb0ELi0ELb0ELi0ELi1ELb0ELi4ELb1ELi0EE"),
+    ("C1 bench kernel (v20): line path 1, 2 tiles per warp, split planes on levels 1-2 (PLANES = 3)", "lookup_vb1.cu.o",
+     "ILi4ELi1ELi2ELi1024ELi1ELb0ELi0ELb0ELi0ELi1ELb0ELi4ELb1ELi3EE"),
+    ("C3b bench kernel (v20): line path 4, 2 tiles per warp, split planes on every staged level", "lookup_vb1.cu.o",
+     "ILi4ELi1ELi2ELi1024ELi1ELb0ELi0ELb0ELi0ELi3ELb0ELi4ELb1ELi8EE"),
     ("C3a bench kernel: line path 4, 2 tiles per warp, PBSEQ", "lookup_vb1.cu.o",
-     "ILi4ELi1ELi2ELi1024ELi1ELb0ELi0ELb0ELi0ELi3ELb0ELi4ELb1EE"),
-    ("C1 one tile per warp, line path 1", "lookup_vb1.cu.o", "ILi4ELi1ELi1ELi1024ELi1ELb0ELi0ELb0ELi0ELi1ELb0ELi4ELb0EE"),
-    ("C1 line path 2 (split leaves)", "lookup_vb1.cu.o", "ILi4ELi1ELi1ELi1024ELi1ELb0ELi0ELb0ELi0ELi2ELb0ELi4ELb0EE"),
-    ("C0 leaf image (depth 2, u8)", "lookup_vb1.cu.o", "ILi2ELi1ELi1ELi1024ELi1ELb0ELi0ELb1ELi0ELi0ELb0ELi0ELb0EE"),
+     "ILi4ELi1ELi2ELi1024ELi1ELb0ELi0ELb0ELi0ELi3ELb0ELi4ELb1ELi0EE"),
+    ("C1 one tile per warp, line path 1", "lookup_vb1.cu.o", "ILi4ELi1ELi1ELi1024ELi1ELb0ELi0ELb0ELi0ELi1ELb0ELi4ELb0ELi0EE"),
+    ("C1 line path 2 (split leaves)", "lookup_vb1.cu.o", "ILi4ELi1ELi1ELi1024ELi1ELb0ELi0ELb0ELi0ELi2ELb0ELi4ELb0ELi0EE"),
+    ("C0 leaf image (depth 2, u8)", "lookup_vb1.cu.o", "ILi2ELi1ELi1ELi1024ELi1ELb0ELi0ELb1ELi0ELi0ELb0ELi0ELb0ELi0EE"),
 ]
 WATCH = ["UBLKCP", "SYNCS", "ELECT", "LDS", "LDG", "TLD", "SHFL", "VOTE", "POPC", "PRMT", "ISETP", "STG", "LDL", "STL",
          "BRA", "EXIT"]
