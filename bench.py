@@ -306,13 +306,13 @@ NCU_METRICS = ROOT / "profiles" / "r02_ncu_metrics.json"
 
 def ncu_metrics(workload):
     """Per-query figures of the committed `ncu --set full` capture of this workload's
-    bench kernel (profiles/r02_ncu_metrics.json, tools/ncu_metrics.py); C3a/C3b fall
-    back to C1's and C4 to C2's (same FIB and kernel)."""
+    bench kernel (profiles/r02_ncu_metrics.json, tools/ncu_metrics.py); C3a falls back
+    to C1's packed-key capture and C4 to C2's (same FIB and kernel)."""
     try:
         t = json.loads(NCU_METRICS.read_text())
     except Exception:
         return None
-    return t.get(workload) or t.get({"C3a": "C1", "C3b": "C1", "C4": "C2"}.get(workload, workload))
+    return t.get(workload) or t.get({"C3a": "C1_packed", "C3b": "C1", "C4": "C2"}.get(workload, workload))
 
 
 def roofline_object(geom, vb, cfg, lps, l2_gbs, smem_gbs, hbm_gbs, hbm_src, workload, n_per_launch, sm_mhz):
