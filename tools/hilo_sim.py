@@ -1,5 +1,6 @@
-"""Host model (no GPU) of a split-plane Phase A: every staged node stored as 15 high
-words then 15 low words (the same 120 bytes), probed with one LDS.32 of the high word;
+"""Host model (no GPU) of the split-plane Phase A (lookup_kernel.cuh PLANES): every staged
+level stored as a plane of its nodes' 15 high words followed by a plane of their low
+words, probed with one LDS.32 of the high word;
 the low word is read only when some lane of the warp ties on the high word (a
 warp-uniform branch). Replays a workload's queries in warp order and reports, per
 level and probe, the per-lane tie rate, the share of warp steps with any tie (1, 2 and 4
@@ -54,8 +55,9 @@ for l in range(T):
             any1 = tie.reshape(-1, 32).any(axis=1)
             any2 = tie[: nw // 2 * 64].reshape(-1, 64).any(axis=1)
             any4 = tie[: nw // 4 * 128].reshape(-1, 128).any(axis=1)
-            hi_word = (off[l] + n * 15) * 2 + pos          # 4-byte word index of the high word
-            lo_word = hi_word + 15
+            nodes_l = (g.level_start[l + 1] - g.level_start[l]) // 16
+            hi_word = off[l] * 2 + n * 15 + pos            # 4-byte word index in the level's high plane
+            lo_word = hi_word + nodes_l * 15               # the low plane follows the high plane
             w32 = max_load(hi_word, 32, 32)
             w64 = max_load(off[l] + n * 15 + pos, 16, 16) * 1.0
             # slow path: the tying lanes' low-word loads (one more LDS.32, only those lanes)
