@@ -1,4 +1,5 @@
-# Parity soak: the randomised every-mode stress test (random FIBs x every shared-memory
+# Parity soak (re-run on the v20 kernels: the stress test now covers the split-plane descent too):
+# the randomised every-mode stress test (random FIBs x every shared-memory
 # split x line path x tile count x checked/unchecked x address/key/search input, against
 # the CPU oracle on every boundary +-1) under 10 more seeds x 200 FIBs each.
 cd $GRAFT_REPO_ROOT
