@@ -221,7 +221,8 @@ int lpm6cu_fib_kernel_config(const lpm6cu_fib* fib, lpm6cu_kernel_config* cfg);
 /* Times the line paths on a representative batch (device buffers; two interleaved
  * rounds of `reps` timed launches per path after one untimed, the faster round
  * kept; on `stream`, which it synchronizes) — the texture leaf paths 1 and 4 also
- * with 2 and 4 tiles per warp (queries_per_lane, at 1024 threads) — keeps the
+ * with 2 and 4 tiles per warp (queries_per_lane, at 1024 threads) and, on those, the
+ * split-plane descent (plane_levels 2, 3 and every staged level) — keeps the
  * fastest in the kernel config and returns its line path in *line_path (0..4, see
  * lpm6cu_kernel_config; 3 only when the tree has internal L2 levels, 4 only with
  * 1-byte next hops). Results are

@@ -193,6 +193,18 @@ bool default_shape(const lpm6cu_kernel_config& c) {
   return c.queries_per_lane == 1 && c.threads_per_cta == 1024 && c.min_ctas_per_sm == 1;
 }
 
+// A non-blocking stream per device for the plane-image kernel: the legacy default stream
+// would also wait for whatever the caller's blocking streams have queued (a store commit
+// carries the kernel config to the new FIB while readers keep looking up).
+cudaStream_t planes_stream(int device) {
+  static std::mutex mu;
+  static cudaStream_t streams[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (device < 0 || device >= 64) return nullptr;
+  if (!streams[device]) check_cuda(cudaStreamCreateWithFlags(&streams[device], cudaStreamNonBlocking), "planes stream");
+  return streams[device];
+}
+
 // (Re)build the plane image for f->cfg.plane_levels (a no-op when it is current or not
 // asked for). Synchronous: the tuning / configuration calls are not on the lookup path.
 void ensure_planes(lpm6cu_fib* f) {
@@ -207,13 +219,14 @@ void ensure_planes(lpm6cu_fib* f) {
   const size_t bytes = static_cast<size_t>(pl.lvl_w[levels]) * 8;
   if (bytes == 0) return;
   DeviceGuard dg(f->device);
+  const cudaStream_t st = planes_stream(f->device);
   if (!f->d_planes)
     check_cuda(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&f->d_planes), (bytes + 15) / 16 * 16,
-                                       capi::fib_line_pool(f->device), nullptr),
+                                       capi::fib_line_pool(f->device), st),
                "cudaMallocFromPoolAsync planes");
-  lpm6_planes_kernel<<<32, 256>>>(f->d_lines + f->g.image_start, f->d_planes, pl);
+  lpm6_planes_kernel<<<32, 256, 0, st>>>(f->d_lines + f->g.image_start, f->d_planes, pl);
   check_cuda(cudaGetLastError(), "planes launch");
-  check_cuda(cudaStreamSynchronize(nullptr), "planes sync");
+  check_cuda(cudaStreamSynchronize(st), "planes sync");
   f->planes_pu = pu;
 }
 
