@@ -206,6 +206,17 @@ def test_commit_keeps_the_tuned_kernel_config(lpm, orc, cuda, st):
         assert cfg["line_path"] == 2 and cfg["smem_levels"] == snap.fib.geometry.image_levels
         addrs = probe_addrs(lpm, view, rng)
         np.testing.assert_array_equal(lookup(cuda, snap, addrs), expected(lpm, orc, view, addrs))
+        # the split-plane descent travels too: the next snapshot lays out its own plane image
+        snap.fib.set_kernel_config(line_path=1, threads_per_cta=1024, queries_per_lane=2, plane_levels=3)
+    ops2 = [st.UpdateOp(st.ANNOUNCE, Prefix((0x2002 << 112) | (i << 64), 64, 9)) for i in range(50)]
+    store.stage(ops2)
+    store.commit()
+    view, _, _ = st.apply_updates(view, ops2)
+    with store.acquire() as snap:
+        cfg = snap.fib.kernel_config()
+        assert (cfg["line_path"], cfg["queries_per_lane"], cfg["plane_levels"]) == (1, 2, 3)
+        addrs = probe_addrs(lpm, view, rng, n_random=1 << 16)
+        np.testing.assert_array_equal(lookup(cuda, snap, addrs), expected(lpm, orc, view, addrs))
     store.close()
 
 
