@@ -517,14 +517,13 @@ __global__ void __launch_bounds__(THREADS, MINB) lpm6_lookup_kernel(const Lookup
   constexpr bool kLeafSectors = LPM6_TEX_SECTORS != 0 && VB == 1;
   unsigned violations = 0;
   unsigned long long visits = 0;  // CHECKED: lines visited by this lane's own queries
-  constexpr int NS = 4 * TILES;  // queries in flight per 4-lane group
   extern __shared__ __align__(128) unsigned long long s_lines[];
   __shared__ __align__(8) uint64_t s_bar;
 
   const unsigned lane = threadIdx.x & 31u;
   const unsigned j = lane & 3u;                 // lane within the 4-lane group
   const unsigned gbase = lane & ~3u;            // first lane (= first query) of the group
-  const unsigned gmask = 0xFu << gbase;
+  [[maybe_unused]] const unsigned gmask = 0xFu << gbase;  // LPM6_RANK_MODE 0
   const unsigned long long warp0 = (static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const unsigned long long nwarps = (static_cast<unsigned long long>(gridDim.x) * blockDim.x) >> 5;
   const uint64_t pol_stream = policy_evict_first();
